@@ -1,0 +1,278 @@
+#!/usr/bin/env python
+"""Benchmark of the Fast-LSQ assembly hot path (BASELINE.json metric: A-assembly entries/s and
+HBM GB/s, fp64).
+
+One STEP = one pass of the whole hot path of SURVEY §8(a) over the workload:
+  a1 fls_features (W, b from Philox on the device)  +  a2-a8 fls_assemble (prefactor fold,
+  phase, trig, combine, weighted row blocks, rhs, streaming fp64 stores of [A | b]).
+Default workload = BASELINE.json config 5 (3D biharmonic + variable-coefficient Helmholtz,
+2,097,152 rows x 8,192 features = 1.718e10 entries, 137.4 GB of fp64), row-sharded over the
+ranks (strong scaling: the config fixes the total rows).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fls|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Timing: W warm-up steps, then K steps bracketed by barrier + cuda.synchronize, CUDA events on
+the ctx stream, max over ranks.  The output (137 GB) is >1000x L2, so every step streams past
+L2 (no flush needed).  The dominant kernel's duration comes from libfls's own event pairs
+around each assembly launch (fls_ctx_timing).  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "A-assembly entries/s (fp64)"
+UNIT = "entries/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            P = json.load(f)
+        return float(P["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region"""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], 0.0, set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if r[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(problem, rows_budget_s: float = 12.0):
+    """The oracle as it stands on the host cores, on a bounded row sample of the workload."""
+    import oracle
+    W, b = problem.parity_features()
+    R = problem.n_rows
+    n = 16
+    best = None
+    while True:
+        rows = np.linspace(0, R - 1, n).astype(np.int64)
+        t0 = time.perf_counter()
+        oracle.assemble(W, b, problem.blocks, rows=rows, want_scale=False)
+        dt = time.perf_counter() - t0
+        best = (n, dt)
+        if dt > rows_budget_s / 3 or n >= R:
+            break
+        n = min(R, n * 4)
+    n, dt = best
+    ent = n * problem.n_features
+    return {"value": ent / dt, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": f"{n} evenly spaced rows x all {problem.n_features} features of "
+                      f"{problem.name} ({ent:.3g} entries, {dt:.2f} s)"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as the reference arm (tier rules), rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    import workloads as wl
+    p = wl.make_problem(args.workload, "full")
+    W, b = p.parity_features()
+    R, F = p.n_rows, p.n_features
+    n = args.ref_rows
+    times = []
+    for s in range(args.warmup + args.steps):
+        rows = (np.arange(n, dtype=np.int64) * 7919 + s * 104729) % R
+        t0 = time.perf_counter()
+        oracle.assemble(W, b, p.blocks, rows=rows, want_scale=False)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * sum(times) / len(times)
+    val = n * F / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": p.name, "rows": R, "features": F,
+                                            "sample_rows_per_step": n},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": oracle.max_threads(),
+                             "kind": "oracle",
+                             "sample": f"{n} rows/step x {F} features of {p.name}"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="fls", choices=["fls", "reference"])
+    ap.add_argument("--workload", default="c5_biharm3d")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
+    ap.add_argument("--ref-rows", type=int, default=64)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import workloads as wl
+    from paper_2602_10541_b200 import fls
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    p = wl.make_problem(args.workload, "full")
+    F, R, d = p.n_features, p.n_rows, p.dim
+    a, e = wl.shard_range(R, rank, world)
+    n_local = e - a
+    # this rank's points only (inputs resident in HBM before timing)
+    offs = p.block_offsets()
+    blocks = []
+    for blk, o in zip(p.blocks, offs):
+        lo, hi = max(a, o), min(e, o + blk.n)
+        if hi <= lo:
+            continue
+        sl = slice(lo - o, hi - o)
+        blocks.append(fls.Block(torch.from_numpy(np.ascontiguousarray(blk.X[sl])).cuda(), blk.terms,
+                                blk.weight, torch.from_numpy(np.ascontiguousarray(blk.values[sl])).cuda(),
+                                torch.from_numpy(np.ascontiguousarray(blk.fields[sl])).cuda()
+                                if blk.fields is not None else None))
+    ctx = fls.Context(local)
+    bset = fls.BlockSet(blocks, d)
+    lda = fls.round_up(n_local, 4)
+    Ab = torch.empty(((F + 1) * lda,), dtype=torch.float64, device="cuda")
+    W = torch.empty((F, d), dtype=torch.float64, device="cuda")
+    b = torch.empty((F,), dtype=torch.float64, device="cuda")
+    launches_per_step = 1 + 2 * len(blocks)          # features + (prefactor, assemble) per block
+
+    def step():
+        fls.fls_features(ctx, d, F, p.sigma, p.seed, W, b)
+        fls.fls_assemble(ctx, W, b, bset, A=Ab, lda=lda)
+
+    for _ in range(args.warmup):
+        step()
+    fls.fls_sync(ctx)
+    clk = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    time.sleep(0.3)
+    fls.fls_ctx_timing(ctx, True)
+    st = ctx.stream
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(args.steps):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    fls.fls_sync(ctx)
+    ms_total = e0.elapsed_time(e1)
+    k_ms, k_launches = fls.fls_ctx_timing_read(ctx)
+    fls.fls_ctx_timing(ctx, False)
+    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    entries = R * F
+    value = entries / (ms_step / 1e3)
+
+    # roofline of the dominant kernel (assembly): algorithmic bytes = 8 B x entries per launch
+    hbm_peak, peak_kind = _peaks()
+    k_avg_ms = k_ms / max(k_launches, 1)
+    bytes_per_launch = 8.0 * n_local * F / max(len(blocks), 1)
+    achieved = bytes_per_launch / (k_avg_ms / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.workload)
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": p.name, "rows": R, "features": F, "dim": d,
+                   "operator": "biharmonic + 16(1+x1) u" if p.name == "c5_biharm3d" else p.name,
+                   "A_bytes": 8 * R * (F + 1), "parallelism": f"rows{world}",
+                   "l2": "no flush: each step writes the 137 GB output (>1000x the 126 MB L2)"},
+        "hbm_write_gbs": 8.0 * R * (F + 1) / (ms_step / 1e3) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic,
+                     "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                     "kernel": "assemble_cm_kernel", "kernel_ms_avg": k_avg_ms},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(p)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

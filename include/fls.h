@@ -1,0 +1,217 @@
+/*
+ * fls.h -- C ABI of the B200-native Fast-LSQ assembly library (libfls.so).
+ *
+ * Fast-LSQ (arxiv 2602.10541) solves a linear PDE  L[u] = f in Omega,  B[u] = g on dOmega
+ * with the sinusoidal random-feature ansatz (Eq. 1)
+ *
+ *     u_N(x) = s * sum_j beta_j sin(W_j . x + b_j),   s = 1/sqrt(N),
+ *     W_j ~ N(0, sigma^2 I_d),  b_j ~ U(0, 2 pi)  frozen,
+ *
+ * by one least-squares solve of the augmented system (Eq. 3)
+ *
+ *     [ A_pde ; lambda A_bc ] beta = [ f ; lambda g ],   A_ij = L[phi_j](x_i),
+ *
+ * where every entry is the closed form of the cyclic derivative (Eq. 2)
+ *
+ *     D^alpha sin(W_j . x + b_j) = (prod_k W_jk^alpha_k) Phi_{|alpha| mod 4}(W_j . x + b_j),
+ *     Phi_0 = sin, Phi_1 = cos, Phi_2 = -sin, Phi_3 = -cos.
+ *
+ * This library implements Algorithm 1 on one B200 per process:
+ *     fls_features  -- line 1, sample W and b
+ *     fls_assemble  -- lines 3-5 (first half): A_pde, lambda A_bc, (lambda A_ic), rhs
+ *     fls_solve     -- line 5 (second half): beta = argmin ||A beta - b||^2 (+ mu ||beta||^2)
+ *     fls_eval      -- line 6: u_N (or L[u_N]) at arbitrary points
+ * Notation in this header: n_features = N of the paper (BASELINE.json calls it M),
+ * n_points = collocation rows (the paper's M_1, M_2).
+ *
+ * Conventions (all entry points)
+ *   - Every floating-point quantity is fp64.  Pointers are DEVICE pointers (cudaMalloc'd or
+ *     torch CUDA tensors on the ctx's device) unless the comment says "host".
+ *   - Ownership: the caller owns every buffer passed in; the library never frees caller
+ *     memory and never retains a caller pointer after a call returns (the enqueued kernels
+ *     read / write it later on the ctx's stream, so the caller must keep it alive until the
+ *     stream reaches that point).  The ctx owns a small internal workspace (per-feature
+ *     prefactors, O(n_blocks * n_features * (dim + 6)) doubles), grown on demand.
+ *   - Streams: work is enqueued on the stream borrowed at fls_ctx_create (0 = legacy default
+ *     stream).  fls_features / fls_assemble / fls_eval are ASYNCHRONOUS; fls_solve and
+ *     fls_sync are blocking.
+ *   - Errors: every call returns fls_status.  Argument errors (FLS_EINVAL) are detected on
+ *     the host before anything is enqueued.  Non-finite inputs (W, b, X, values, coefficient
+ *     fields) are detected by the kernels themselves and reported asynchronously: the next
+ *     fls_sync / fls_solve on the ctx returns FLS_ENONFINITE (the affected output is then
+ *     unspecified).  fls_last_error() returns a thread-local message for the last failure.
+ *   - Determinism: for fixed inputs every assembled entry is bit-identical regardless of the
+ *     row range [row_begin, row_end) a call produces (row sharding), the layout, lda, and the
+ *     launch configuration.
+ */
+#ifndef FLS_H_
+#define FLS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define FLS_API __attribute__((visibility("default")))
+#else
+#define FLS_API
+#endif
+
+#define FLS_API_VERSION 1
+#define FLS_MAX_DIM 8      /* spatial / space-time dimension d <= 8 */
+#define FLS_MAX_TERMS 64   /* terms per operator */
+#define FLS_MAX_FIELDS 4   /* coefficient fields per block */
+
+typedef enum {
+    FLS_OK = 0,
+    FLS_EINVAL = 1,        /* bad argument (null pointer, size, dim / alpha mismatch, lda) */
+    FLS_ENOMEM = 2,        /* device allocation failed */
+    FLS_ECUDA = 3,         /* CUDA runtime error */
+    FLS_ECUSOLVER = 4,     /* cuSOLVER / cuBLAS error */
+    FLS_ENCCL = 5,         /* reserved for the collective layer */
+    FLS_ENONFINITE = 6,    /* NaN / Inf in an input (reported by fls_sync / fls_solve) */
+    FLS_ERANK = 7,         /* exactly zero diagonal in R with no ridge */
+    FLS_EUNSUPPORTED = 8   /* valid request this build does not implement */
+} fls_status;
+
+/* thread-local message describing the last non-FLS_OK return of this thread */
+FLS_API const char *fls_last_error(void);
+FLS_API const char *fls_status_string(fls_status s);
+FLS_API int fls_api_version(void);
+
+/* ---------------------------------------------------------------------------------------- */
+/* context                                                                                  */
+/* ---------------------------------------------------------------------------------------- */
+typedef struct fls_ctx fls_ctx;
+
+/* device: CUDA ordinal; cuda_stream: a cudaStream_t (borrowed, not destroyed), or NULL for
+ * the legacy default stream.  *out receives the ctx.  Errors: FLS_EINVAL (out NULL, bad
+ * device), FLS_ECUDA. */
+FLS_API fls_status fls_ctx_create(int device, void *cuda_stream, fls_ctx **out);
+/* frees the ctx workspace and library handles; NULL is a no-op. */
+FLS_API fls_status fls_ctx_destroy(fls_ctx *ctx);
+/* re-point the ctx at another stream (borrowed). */
+FLS_API fls_status fls_ctx_set_stream(fls_ctx *ctx, void *cuda_stream);
+/* block until the ctx stream is idle; returns FLS_ENONFINITE (and clears the flag) if a
+ * kernel saw a non-finite input since the last check, FLS_ECUDA on an asynchronous fault. */
+FLS_API fls_status fls_sync(fls_ctx *ctx);
+/* measurement hook: with enable != 0 every assembly-kernel launch of fls_assemble is bracketed
+ * by CUDA events on the ctx stream (the prefactor kernel is not included).  timing_read
+ * synchronises the stream, returns the summed kernel milliseconds and the launch count since
+ * the last enable / read (host outputs), and restarts the count. */
+FLS_API fls_status fls_ctx_timing(fls_ctx *ctx, int32_t enable);
+FLS_API fls_status fls_ctx_timing_read(fls_ctx *ctx, double *ms_total, int64_t *n_launches);
+
+/* ---------------------------------------------------------------------------------------- */
+/* operators as data: L = sum_t c_t(x) D^{alpha_t}   (P:L92 multi-index; "linear    */
+/* PDE L[u] = f"; P:L402-403 variable coefficients)                                         */
+/* ---------------------------------------------------------------------------------------- */
+typedef struct {
+    int32_t alpha[FLS_MAX_DIM];  /* derivative orders per axis; entries >= dim must be 0 */
+    double coef;                 /* constant coefficient c_t */
+    int32_t field;               /* -1: constant; g in [0, n_fields): c_t(x_i) = coef *
+                                    coef_fields[i * n_fields + g] */
+} fls_term;
+
+typedef struct {
+    int32_t dim;                 /* must equal the basis dim */
+    int32_t n_terms;             /* 1 .. FLS_MAX_TERMS */
+    const fls_term *terms;       /* host array of n_terms */
+} fls_operator;
+
+/* one row block of Eq. 3: its rows are  weight * L_blk[phi_j](x_i),  rhs  weight * values_i.
+ * Dirichlet BC / IC blocks use the identity operator (one term, alpha = 0, coef = 1). */
+typedef struct {
+    const double *X;             /* device, n_points x dim, row-major */
+    int64_t n_points;            /* >= 0; 0 = empty block */
+    const fls_operator *op;      /* host */
+    const double *coef_fields;   /* device, n_points x n_fields row-major, or NULL if n_fields=0 */
+    int32_t n_fields;            /* 0 .. FLS_MAX_FIELDS */
+    double weight;               /* 1 for PDE rows, lambda for BC / IC rows */
+    const double *values;        /* device, n_points (f, g or h), or NULL: rhs rows = 0 */
+} fls_block;
+
+/* ---------------------------------------------------------------------------------------- */
+/* Alg. 1 line 1: W_j ~ N(0, sigma^2 I_dim), b_j ~ U[0, 2 pi).              */
+/* Counter-based and bit-reproducible: Philox4x64-10 keyed (seed, stream), raw output n is  */
+/* word n%4 of the block at counter (n/4 + 1, 0, 0, 0); stream 1 feeds W through Box-Muller */
+/* on uniform pairs (u = (raw >> 11) 2^-53; r = sqrt(-2 log(1-u1)), th = 2 pi u2; normal   */
+/* 2m = r cos th, 2m+1 = r sin th; W[j][k] = sigma * normal[j*dim + k]); stream 2 feeds    */
+/* b_j = 2 pi u_j.  (DESIGN.md §3 R1 -- the paper names no generator.)                     */
+/*   W: device, n_features x dim row-major (written).  b: device, n_features (written).    */
+/*   Errors: FLS_EINVAL for dim not in 1..FLS_MAX_DIM, n_features < 1, sigma <= 0 or not   */
+/*   finite, NULL outputs.                                                                  */
+/* ---------------------------------------------------------------------------------------- */
+FLS_API fls_status fls_features(fls_ctx *ctx, int32_t dim, int64_t n_features, double sigma,
+                        uint64_t seed, double *W, double *b);
+
+#define FLS_COL_MAJOR 0   /* A[j * lda + i]: rows contiguous (what fls_solve consumes) */
+#define FLS_ROW_MAJOR 1   /* A[i * lda + j]: features contiguous */
+
+/* ---------------------------------------------------------------------------------------- */
+/* Alg. 1 lines 3-5, Eq. 3 with Eq. 2:                    */
+/*   A_ij = w_blk * s * sum_t c_t(x_i) (prod_k W_jk^alpha_tk) Phi_{|alpha_t| mod 4}(z_ij),   */
+/*   z_ij = W_j . x_i + b_j,   s = 1/sqrt(n_features) if normalize else 1,                  */
+/*   rhs_i = w_blk * values_i.                                                               */
+/* The blocks are stacked in order (global row g runs over block 0's points, then block 1's */
+/* ...).  This call writes the global rows [row_begin, row_end) -- one rank's shard -- to    */
+/* local row (g - row_begin) of A, and of rhs if rhs != NULL.                               */
+/*   W, b: device (fls_features layout).  dim: 1..FLS_MAX_DIM.  n_features >= 1.             */
+/*   blocks: host array of n_blocks (>= 1) descriptors.                                      */
+/*   0 <= row_begin <= row_end <= total rows.  row_begin == row_end is a no-op (FLS_OK).     */
+/*   A: device; FLS_COL_MAJOR needs lda >= row_end - row_begin, FLS_ROW_MAJOR lda >=         */
+/*   n_features.  Fastest when A is 16-byte aligned and lda is even (vector stores).        */
+/*   rhs: device, row_end - row_begin doubles, or NULL.  For the solver's [A | b] layout pass */
+/*   rhs = A + n_features * lda (column-major).                                              */
+/*   Errors (host, before any launch): FLS_EINVAL for NULL pointers, sizes, layout, lda,     */
+/*   op->dim != dim, alpha entries < 0 or set beyond dim, field >= n_fields, too many terms. */
+/*   Non-finite inputs: FLS_ENONFINITE at the next fls_sync.                                 */
+/* ---------------------------------------------------------------------------------------- */
+FLS_API fls_status fls_assemble(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
+                        int64_t n_features, int32_t normalize, const fls_block *blocks,
+                        int32_t n_blocks, int64_t row_begin, int64_t row_end, double *A,
+                        int64_t lda, int32_t layout, double *rhs);
+
+/* ---------------------------------------------------------------------------------------- */
+/* Alg. 1 line 5 ("beta* = argmin ||A beta - b||^2 via QR"), with the optional       */
+/* Tikhonov term of P:L156-160:  beta = argmin ||A beta - b||^2 + mu ||beta||^2.             */
+/* Householder QR (cuSOLVER geqrf) of the column-major [A | b] (n_rows x (n_features + 1),   */
+/* b stored as column n_features), then R beta = (Q^T b)[0:n].  sqrt_mu > 0 appends the      */
+/* rows [sqrt_mu I | 0] at rows n_rows .. n_rows + n_features - 1 of the same buffer, so     */
+/* then lda >= n_rows + n_features is required.  (reading A16: sqrt_mu =          */
+/* tau ||A||_F with tau = 0 for C1-C4, 1e-10 for C5; use fls_frob2 for ||A||_F^2.)           */
+/*   Ab: device, destroyed (holds R on return).  beta: device, n_features (written).          */
+/*   resid_norm: host, optional: ||A beta - b||_2 (+ ridge part) = |R[n, n]|.                 */
+/*   Blocking.  Errors: FLS_EINVAL, FLS_ENOMEM, FLS_ECUSOLVER, FLS_ERANK (exact zero on the   */
+/*   diagonal of R with sqrt_mu = 0), FLS_ENONFINITE (pending from an earlier kernel).       */
+/* ---------------------------------------------------------------------------------------- */
+FLS_API fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int64_t n_features,
+                     double sqrt_mu, double *beta, double *resid_norm);
+
+/* TSQR building block: Householder QR of the local column-major block M (n_rows x n_cols,
+ * destroyed) and copy of its upper-trapezoidal R (min(n_rows, n_cols) x n_cols, zeros below
+ * the diagonal) into R (device, column-major, ldr >= min(n_rows, n_cols)).  Blocking. */
+FLS_API fls_status fls_qr_r(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda, int64_t n_cols,
+                    double *R, int64_t ldr);
+
+/* sum of squares of the n_rows x n_cols column-major block (for ||A||_F^2).  out: host.
+ * Blocking. */
+FLS_API fls_status fls_frob2(fls_ctx *ctx, const double *A, int64_t n_rows, int64_t lda, int64_t n_cols,
+                     double *out);
+
+/* ---------------------------------------------------------------------------------------- */
+/* Alg. 1 line 6, Eq. 1:  out_i = s * sum_j beta_j sin(W_j . x_i + b_j),    */
+/* or with op != NULL,  out_i = L[u_N](x_i) = sum_j beta_j A_ij  (the PDE residual check of   */
+/* P:L191).  A is never materialised.  op may not use coefficient fields (FLS_EINVAL).        */
+/*   X: device, n_points x dim.  out: device, n_points.  Asynchronous.                       */
+/* ---------------------------------------------------------------------------------------- */
+FLS_API fls_status fls_eval(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
+                    int64_t n_features, int32_t normalize, const double *beta,
+                    const fls_operator *op, const double *X, int64_t n_points, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLS_H_ */

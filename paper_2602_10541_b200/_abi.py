@@ -1,0 +1,100 @@
+"""ctypes declarations of the libfls C ABI (include/fls.h).  Argument marshalling only.
+
+Loading fails loudly (FlsError / OSError) when libfls.so is missing: there is no CPU
+fallback anywhere in this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB_PATH = os.path.join(HERE, "libfls.so")
+HEADER = os.path.join(ROOT, "include", "fls.h")
+
+FLS_MAX_DIM = 8
+FLS_MAX_TERMS = 64
+FLS_MAX_FIELDS = 4
+FLS_COL_MAJOR = 0
+FLS_ROW_MAJOR = 1
+
+STATUS = {0: "FLS_OK", 1: "FLS_EINVAL", 2: "FLS_ENOMEM", 3: "FLS_ECUDA", 4: "FLS_ECUSOLVER",
+          5: "FLS_ENCCL", 6: "FLS_ENONFINITE", 7: "FLS_ERANK", 8: "FLS_EUNSUPPORTED"}
+
+
+class FlsError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class fls_term(C.Structure):
+    _fields_ = [("alpha", C.c_int32 * FLS_MAX_DIM), ("coef", C.c_double), ("field", C.c_int32)]
+
+
+class fls_operator(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("n_terms", C.c_int32), ("terms", C.POINTER(fls_term))]
+
+
+class fls_block(C.Structure):
+    _fields_ = [("X", C.c_void_p), ("n_points", C.c_int64), ("op", C.POINTER(fls_operator)),
+                ("coef_fields", C.c_void_p), ("n_fields", C.c_int32), ("weight", C.c_double),
+                ("values", C.c_void_p)]
+
+
+_SIGS = {
+    "fls_last_error": (C.c_char_p, []),
+    "fls_status_string": (C.c_char_p, [C.c_int]),
+    "fls_api_version": (C.c_int, []),
+    "fls_ctx_create": (C.c_int, [C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "fls_ctx_destroy": (C.c_int, [C.c_void_p]),
+    "fls_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "fls_sync": (C.c_int, [C.c_void_p]),
+    "fls_ctx_timing": (C.c_int, [C.c_void_p, C.c_int32]),
+    "fls_ctx_timing_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    "fls_features": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_uint64,
+                               C.c_void_p, C.c_void_p]),
+    "fls_assemble": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int32,
+                               C.POINTER(fls_block), C.c_int32, C.c_int64, C.c_int64, C.c_void_p,
+                               C.c_int64, C.c_int32, C.c_void_p]),
+    "fls_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_double,
+                            C.c_void_p, C.POINTER(C.c_double)]),
+    "fls_qr_r": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                           C.c_int64]),
+    "fls_frob2": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                            C.POINTER(C.c_double)]),
+    "fls_eval": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int32,
+                           C.c_void_p, C.POINTER(fls_operator), C.c_void_p, C.c_int64, C.c_void_p]),
+}
+
+_lib = None
+
+
+def header_symbols() -> list:
+    """every function declared in include/fls.h"""
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(fls_[a-z0-9_]+)\s*\(", txt)))
+
+
+def load():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FlsError(3, f"libfls.so not built at {LIB_PATH}; run "
+                              "`python -m paper_2602_10541_b200.build` (no CPU fallback exists)")
+        lib = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def check(status: int):
+    if status != 0:
+        msg = load().fls_last_error()
+        raise FlsError(status, msg.decode() if msg else "")

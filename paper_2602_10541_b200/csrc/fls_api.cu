@@ -1,0 +1,556 @@
+// fls_api.cu -- the C ABI of libfls (include/fls.h): ctx, argument validation, mode selection,
+// launches, and the cuSOLVER least-squares solve.
+//
+// Product code.  Paper = PAPER.md (arxiv 2602.10541), cited P:L<line>.
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fls_internal.h"
+
+using namespace fls;
+
+struct fls_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  unsigned *d_err = nullptr;          // async non-finite flag
+  double *d_scratch = nullptr;        // small device scratch (min diag, frob partials)
+  double *ws = nullptr;               // per-feature prefactor records
+  size_t ws_bytes = 0;
+  cusolverDnHandle_t solver = nullptr;
+  cublasHandle_t blas = nullptr;
+  // optional per-launch timing of the assembly kernels (fls_ctx_timing)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;  // pairs (start, stop)
+  size_t ev_used = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+fls_status fail(fls_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+fls_status cuda_fail(cudaError_t e, const char *where) {
+  return fail(FLS_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define FLS_CUDA(call)                                         \
+  do {                                                         \
+    cudaError_t e_ = (call);                                   \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);        \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+fls_status ensure_ws(fls_ctx *ctx, size_t bytes) {
+  if (bytes <= ctx->ws_bytes) return FLS_OK;
+  if (ctx->ws) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->ws);
+    ctx->ws = nullptr;
+    ctx->ws_bytes = 0;
+  }
+  size_t nb = bytes < (1u << 20) ? (1u << 20) : bytes;
+  if (cudaMalloc(&ctx->ws, nb) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FLS_ENOMEM, "workspace allocation of %zu bytes failed", nb);
+  }
+  ctx->ws_bytes = nb;
+  return FLS_OK;
+}
+
+// host-side analysis of one operator: groups, parity, mode
+struct OpPlan {
+  int G = 0;
+  int pmode = PM_SIN;
+  int kmode = KM_SIN;
+  int gfield[FLS_MAX_FIELDS] = {0, 0, 0, 0};
+  int n_terms = 0;
+  TermDev terms[FLS_MAX_TERMS];
+};
+
+fls_status plan_operator(const fls_operator *op, int32_t dim, int32_t n_fields, bool allow_fields,
+                         OpPlan &pl, const char *what) {
+  if (!op) return fail(FLS_EINVAL, "%s: operator is NULL", what);
+  if (op->dim != dim)
+    return fail(FLS_EINVAL, "%s: operator dim %d != basis dim %d", what, op->dim, dim);
+  if (op->n_terms < 1 || op->n_terms > FLS_MAX_TERMS)
+    return fail(FLS_EINVAL, "%s: n_terms %d not in 1..%d", what, op->n_terms, FLS_MAX_TERMS);
+  if (!op->terms) return fail(FLS_EINVAL, "%s: terms is NULL", what);
+  bool any_s = false, any_c = false;
+  std::memset(pl.terms, 0, sizeof pl.terms);
+  pl.n_terms = op->n_terms;
+  pl.G = 0;
+  for (int t = 0; t < op->n_terms; ++t) {
+    const fls_term &T = op->terms[t];
+    int order = 0;
+    for (int k = 0; k < FLS_MAX_DIM; ++k) {
+      if (T.alpha[k] < 0 || T.alpha[k] > 64)
+        return fail(FLS_EINVAL, "%s: term %d alpha[%d] = %d out of range", what, t, k, T.alpha[k]);
+      if (k >= dim && T.alpha[k] != 0)
+        return fail(FLS_EINVAL, "%s: term %d alpha[%d] set beyond dim %d", what, t, k, dim);
+      order += T.alpha[k];
+      pl.terms[t].alpha[k] = (int8_t)T.alpha[k];
+    }
+    if (!std::isfinite(T.coef)) return fail(FLS_EINVAL, "%s: term %d coef not finite", what, t);
+    pl.terms[t].coef = T.coef;
+    int grp = 0;
+    if (T.field >= 0) {
+      if (!allow_fields) return fail(FLS_EINVAL, "%s: coefficient fields not allowed here", what);
+      if (T.field >= n_fields)
+        return fail(FLS_EINVAL, "%s: term %d field %d >= n_fields %d", what, t, T.field, n_fields);
+      int g = 0;
+      while (g < pl.G && pl.gfield[g] != T.field) ++g;
+      if (g == pl.G) pl.gfield[pl.G++] = T.field;
+      grp = g + 1;
+    } else if (T.field != -1) {
+      return fail(FLS_EINVAL, "%s: term %d field %d (use -1 for constant)", what, t, T.field);
+    }
+    pl.terms[t].group = (int8_t)grp;
+    if (order & 1) any_c = true; else any_s = true;
+  }
+  if (!any_c) { pl.pmode = PM_SIN; pl.kmode = KM_SIN; }
+  else if (!any_s) { pl.pmode = PM_COSSHIFT; pl.kmode = KM_SIN; }
+  else if (pl.G == 0) { pl.pmode = PM_FOLD; pl.kmode = KM_SIN; }
+  else { pl.pmode = PM_SINCOS; pl.kmode = KM_SINCOS; }
+  return FLS_OK;
+}
+
+fls_status check_ctx(fls_ctx *ctx) {
+  if (!ctx) return fail(FLS_EINVAL, "ctx is NULL");
+  return FLS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *fls_last_error(void) { return g_err.c_str(); }
+
+const char *fls_status_string(fls_status s) {
+  switch (s) {
+    case FLS_OK: return "FLS_OK";
+    case FLS_EINVAL: return "FLS_EINVAL";
+    case FLS_ENOMEM: return "FLS_ENOMEM";
+    case FLS_ECUDA: return "FLS_ECUDA";
+    case FLS_ECUSOLVER: return "FLS_ECUSOLVER";
+    case FLS_ENCCL: return "FLS_ENCCL";
+    case FLS_ENONFINITE: return "FLS_ENONFINITE";
+    case FLS_ERANK: return "FLS_ERANK";
+    case FLS_EUNSUPPORTED: return "FLS_EUNSUPPORTED";
+  }
+  return "FLS_?";
+}
+
+int fls_api_version(void) { return FLS_API_VERSION; }
+
+fls_status fls_ctx_create(int device, void *cuda_stream, fls_ctx **out) {
+  if (!out) return fail(FLS_EINVAL, "out is NULL");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (device < 0 || device >= n) return fail(FLS_EINVAL, "device %d not in [0, %d)", device, n);
+  DeviceGuard g(device);
+  fls_ctx *c = new fls_ctx();
+  c->device = device;
+  c->stream = (cudaStream_t)cuda_stream;
+  if ((e = cudaMalloc(&c->d_err, sizeof(unsigned))) != cudaSuccess ||
+      (e = cudaMemset(c->d_err, 0, sizeof(unsigned))) != cudaSuccess ||
+      (e = cudaMalloc(&c->d_scratch, 1024 * sizeof(double))) != cudaSuccess) {
+    fls_ctx_destroy(c);
+    return cuda_fail(e, "fls_ctx_create");
+  }
+  *out = c;
+  return FLS_OK;
+}
+
+fls_status fls_ctx_destroy(fls_ctx *ctx) {
+  if (!ctx) return FLS_OK;
+  DeviceGuard g(ctx->device);
+  if (ctx->stream || true) cudaStreamSynchronize(ctx->stream);
+  if (ctx->solver) cusolverDnDestroy(ctx->solver);
+  if (ctx->blas) cublasDestroy(ctx->blas);
+  for (cudaEvent_t ev : ctx->ev) cudaEventDestroy(ev);
+  cudaFree(ctx->ws);
+  cudaFree(ctx->d_err);
+  cudaFree(ctx->d_scratch);
+  delete ctx;
+  return FLS_OK;
+}
+
+fls_status fls_ctx_set_stream(fls_ctx *ctx, void *cuda_stream) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  ctx->stream = (cudaStream_t)cuda_stream;
+  if (ctx->solver) cusolverDnSetStream(ctx->solver, ctx->stream);
+  if (ctx->blas) cublasSetStream(ctx->blas, ctx->stream);
+  return FLS_OK;
+}
+
+fls_status fls_ctx_timing(fls_ctx *ctx, int32_t enable) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  ctx->timing = enable != 0;
+  ctx->ev_used = 0;
+  return FLS_OK;
+}
+
+fls_status fls_ctx_timing_read(fls_ctx *ctx, double *ms_total, int64_t *n_launches) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!ms_total || !n_launches) return fail(FLS_EINVAL, "NULL output");
+  DeviceGuard g(ctx->device);
+  FLS_CUDA(cudaStreamSynchronize(ctx->stream));
+  double tot = 0.0;
+  for (size_t k = 0; k + 1 < ctx->ev_used; k += 2) {
+    float ms = 0.f;
+    FLS_CUDA(cudaEventElapsedTime(&ms, ctx->ev[k], ctx->ev[k + 1]));
+    tot += ms;
+  }
+  *ms_total = tot;
+  *n_launches = (int64_t)(ctx->ev_used / 2);
+  ctx->ev_used = 0;
+  return FLS_OK;
+}
+
+fls_status fls_sync(fls_ctx *ctx) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  DeviceGuard g(ctx->device);
+  FLS_CUDA(cudaStreamSynchronize(ctx->stream));
+  unsigned h = 0;
+  FLS_CUDA(cudaMemcpyAsync(&h, ctx->d_err, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  FLS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h) {
+    FLS_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream));
+    FLS_CUDA(cudaStreamSynchronize(ctx->stream));
+    return fail(FLS_ENONFINITE, "non-finite value in an input (W, b, X, values or fields)");
+  }
+  return FLS_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+fls_status fls_features(fls_ctx *ctx, int32_t dim, int64_t n_features, double sigma,
+                        uint64_t seed, double *W, double *b) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (dim < 1 || dim > FLS_MAX_DIM) return fail(FLS_EINVAL, "dim %d not in 1..%d", dim, FLS_MAX_DIM);
+  if (n_features < 1) return fail(FLS_EINVAL, "n_features %lld < 1", (long long)n_features);
+  if (!(sigma > 0.0) || !std::isfinite(sigma)) return fail(FLS_EINVAL, "sigma must be > 0 and finite");
+  if (!W || !b) return fail(FLS_EINVAL, "W or b is NULL");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_features(dim, n_features, sigma, seed, W, b, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "features_kernel");
+  return FLS_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+fls_status fls_assemble(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
+                        int64_t n_features, int32_t normalize, const fls_block *blocks,
+                        int32_t n_blocks, int64_t row_begin, int64_t row_end, double *A,
+                        int64_t lda, int32_t layout, double *rhs) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (dim < 1 || dim > FLS_MAX_DIM) return fail(FLS_EINVAL, "dim %d not in 1..%d", dim, FLS_MAX_DIM);
+  if (n_features < 1) return fail(FLS_EINVAL, "n_features %lld < 1", (long long)n_features);
+  if (!W || !b) return fail(FLS_EINVAL, "W or b is NULL");
+  if (!blocks || n_blocks < 1) return fail(FLS_EINVAL, "need n_blocks >= 1 block descriptors");
+  if (layout != FLS_COL_MAJOR && layout != FLS_ROW_MAJOR)
+    return fail(FLS_EINVAL, "layout %d unknown", layout);
+  int64_t total = 0;
+  static thread_local OpPlan plans[64];
+  if (n_blocks > 64) return fail(FLS_EUNSUPPORTED, "more than 64 blocks");
+  for (int q = 0; q < n_blocks; ++q) {
+    const fls_block &B = blocks[q];
+    if (B.n_points < 0) return fail(FLS_EINVAL, "block %d: n_points < 0", q);
+    if (B.n_fields < 0 || B.n_fields > FLS_MAX_FIELDS)
+      return fail(FLS_EINVAL, "block %d: n_fields %d not in 0..%d", q, B.n_fields, FLS_MAX_FIELDS);
+    if (B.n_points > 0 && !B.X) return fail(FLS_EINVAL, "block %d: X is NULL", q);
+    if (B.n_points > 0 && B.n_fields > 0 && !B.coef_fields)
+      return fail(FLS_EINVAL, "block %d: coef_fields is NULL with n_fields %d", q, B.n_fields);
+    if (!std::isfinite(B.weight)) return fail(FLS_EINVAL, "block %d: weight not finite", q);
+    char what[32];
+    snprintf(what, sizeof what, "block %d", q);
+    if (fls_status s = plan_operator(B.op, dim, B.n_fields, true, plans[q], what)) return s;
+    total += B.n_points;
+  }
+  if (row_begin < 0 || row_end < row_begin || row_end > total)
+    return fail(FLS_EINVAL, "row range [%lld, %lld) not within [0, %lld]", (long long)row_begin,
+                (long long)row_end, (long long)total);
+  const int64_t n_local = row_end - row_begin;
+  if (n_local == 0) return FLS_OK;
+  if (!A) return fail(FLS_EINVAL, "A is NULL");
+  if (layout == FLS_COL_MAJOR && lda < n_local)
+    return fail(FLS_EINVAL, "lda %lld < local rows %lld", (long long)lda, (long long)n_local);
+  if (layout == FLS_ROW_MAJOR && lda < n_features)
+    return fail(FLS_EINVAL, "lda %lld < n_features %lld", (long long)lda, (long long)n_features);
+
+  DeviceGuard g(ctx->device);
+  // per-block prefactor records: stride S doubles per feature, block q at offset q * F * Smax
+  const int Smax = pf_stride(FLS_MAX_DIM, FLS_MAX_FIELDS, KM_SINCOS);
+  if (fls_status s = ensure_ws(ctx, (size_t)n_blocks * n_features * Smax * sizeof(double))) return s;
+  const double s_norm = normalize ? 1.0 / std::sqrt((double)n_features) : 1.0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0);
+
+  int64_t g0 = 0;  // first global row of block q
+  for (int q = 0; q < n_blocks; ++q) {
+    const fls_block &B = blocks[q];
+    const int64_t lo = std::max(g0, row_begin), hi = std::min(g0 + B.n_points, row_end);
+    g0 += B.n_points;
+    if (hi <= lo) continue;
+    const OpPlan &pl = plans[q];
+    PrefArgs pa;
+    std::memset(&pa, 0, sizeof pa);
+    pa.W = W;
+    pa.b = b;
+    pa.F = n_features;
+    pa.D = dim;
+    pa.n_terms = pl.n_terms;
+    pa.G = pl.G;
+    pa.pmode = pl.pmode;
+    pa.S = pf_stride(dim, pl.G, pl.kmode);
+    pa.scale = s_norm * B.weight;
+    pa.pf = ctx->ws + (size_t)q * n_features * Smax;
+    pa.err = ctx->d_err;
+    std::memcpy(pa.terms, pl.terms, sizeof pl.terms);
+    cudaError_t e = launch_prefactor(pa, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "prefactor_kernel");
+
+    AsmArgs aa;
+    std::memset(&aa, 0, sizeof aa);
+    aa.pf = pa.pf;
+    aa.F = n_features;
+    aa.X = B.X;
+    aa.fields = B.coef_fields;
+    aa.values = B.values;
+    aa.weight = B.weight;
+    aa.pt0 = lo - (g0 - B.n_points);
+    aa.lr0 = lo - row_begin;
+    aa.lr1 = hi - row_begin;
+    aa.A = A;
+    aa.lda = lda;
+    aa.rhs = rhs;
+    aa.err = ctx->d_err;
+    aa.nf = B.n_fields;
+    aa.vec = vec ? 1 : 0;
+    for (int i = 0; i < FLS_MAX_FIELDS; ++i) aa.gfield[i] = pl.gfield[i];
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->timing) {
+      if (ctx->ev_used + 2 > ctx->ev.size()) {
+        for (int k = 0; k < 2; ++k) {
+          cudaEvent_t ev;
+          FLS_CUDA(cudaEventCreate(&ev));
+          ctx->ev.push_back(ev);
+        }
+      }
+      e0 = ctx->ev[ctx->ev_used++];
+      e1 = ctx->ev[ctx->ev_used++];
+      FLS_CUDA(cudaEventRecord(e0, ctx->stream));
+    }
+    e = (layout == FLS_COL_MAJOR) ? launch_assemble_cm(dim, pl.G, pl.kmode, aa, ctx->stream)
+                                  : launch_assemble_rm(dim, pl.G, pl.kmode, aa, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "assemble kernel");
+    if (ctx->timing) FLS_CUDA(cudaEventRecord(e1, ctx->stream));
+  }
+  return FLS_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+static fls_status ensure_handles(fls_ctx *ctx) {
+  if (!ctx->solver) {
+    if (cusolverDnCreate(&ctx->solver) != CUSOLVER_STATUS_SUCCESS)
+      return fail(FLS_ECUSOLVER, "cusolverDnCreate failed");
+  }
+  if (!ctx->blas) {
+    if (cublasCreate(&ctx->blas) != CUBLAS_STATUS_SUCCESS)
+      return fail(FLS_ECUSOLVER, "cublasCreate failed");
+  }
+  cusolverDnSetStream(ctx->solver, ctx->stream);
+  cublasSetStream(ctx->blas, ctx->stream);
+  return FLS_OK;
+}
+
+// Householder QR of an m x n column-major block in place (R in the upper trapezoid)
+static fls_status geqrf_inplace(fls_ctx *ctx, double *M, int64_t m, int64_t lda, int64_t n) {
+  if (m > INT32_MAX || n > INT32_MAX || lda > INT32_MAX)
+    return fail(FLS_EUNSUPPORTED, "geqrf: dimensions exceed int32 (m=%lld n=%lld lda=%lld)",
+                (long long)m, (long long)n, (long long)lda);
+  int lwork = 0;
+  if (cusolverDnDgeqrf_bufferSize(ctx->solver, (int)m, (int)n, M, (int)lda, &lwork) !=
+      CUSOLVER_STATUS_SUCCESS)
+    return fail(FLS_ECUSOLVER, "cusolverDnDgeqrf_bufferSize failed");
+  const int64_t k = m < n ? m : n;
+  double *work = nullptr;
+  size_t bytes = ((size_t)lwork + (size_t)k + 2) * sizeof(double);
+  if (cudaMallocAsync((void **)&work, bytes, ctx->stream) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FLS_ENOMEM, "geqrf workspace of %zu bytes", bytes);
+  }
+  double *tau = work + lwork;
+  int *info = reinterpret_cast<int *>(tau + k);
+  cusolverStatus_t st = cusolverDnDgeqrf(ctx->solver, (int)m, (int)n, M, (int)lda, tau, work,
+                                         lwork, info);
+  int h_info = 0;
+  cudaMemcpyAsync(&h_info, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+  cudaFreeAsync(work, ctx->stream);
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "geqrf");
+  if (st != CUSOLVER_STATUS_SUCCESS || h_info != 0)
+    return fail(FLS_ECUSOLVER, "cusolverDnDgeqrf status %d info %d", (int)st, h_info);
+  return FLS_OK;
+}
+
+fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int64_t n_features,
+                     double sqrt_mu, double *beta, double *resid_norm) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!Ab || !beta) return fail(FLS_EINVAL, "Ab or beta is NULL");
+  if (n_features < 1) return fail(FLS_EINVAL, "n_features < 1");
+  if (!(sqrt_mu >= 0.0) || !std::isfinite(sqrt_mu)) return fail(FLS_EINVAL, "sqrt_mu must be >= 0");
+  const int64_t m = n_rows + (sqrt_mu > 0.0 ? n_features : 0);
+  if (n_rows < 0 || lda < m)
+    return fail(FLS_EINVAL, "lda %lld < rows %lld (ridge rows included)", (long long)lda,
+                (long long)m);
+  if (m < n_features)
+    return fail(FLS_EINVAL, "underdetermined: %lld rows < %lld features without ridge",
+                (long long)m, (long long)n_features);
+  DeviceGuard g(ctx->device);
+  if (fls_status s = fls_sync(ctx)) return s;  // surface pending async errors first
+  if (fls_status s = ensure_handles(ctx)) return s;
+  if (sqrt_mu > 0.0) {
+    cudaError_t e = launch_ridge_fill(Ab, lda, n_rows, n_features, sqrt_mu, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "ridge_fill");
+  }
+  const int64_t n = n_features + 1;
+  if (fls_status s = geqrf_inplace(ctx, Ab, m, lda, n)) return s;
+  // zero diagonal?
+  cudaError_t e = launch_min_abs_diag(Ab, lda, n_features, ctx->d_scratch, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "min_abs_diag");
+  double dmin = 0.0, rnn = 0.0;
+  FLS_CUDA(cudaMemcpyAsync(&dmin, ctx->d_scratch, sizeof dmin, cudaMemcpyDeviceToHost, ctx->stream));
+  if (m > n_features)
+    FLS_CUDA(cudaMemcpyAsync(&rnn, Ab + n_features * lda + n_features, sizeof rnn,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  FLS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (dmin == 0.0) return fail(FLS_ERANK, "R has an exactly zero diagonal entry (rank deficient)");
+  // beta = R^{-1} (Q^T b)[0:n]
+  FLS_CUDA(cudaMemcpyAsync(beta, Ab + n_features * lda, n_features * sizeof(double),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+  if (n_features > INT32_MAX) return fail(FLS_EUNSUPPORTED, "n_features exceeds int32");
+  if (cublasDtrsv(ctx->blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
+                  (int)n_features, Ab, (int)lda, beta, 1) != CUBLAS_STATUS_SUCCESS)
+    return fail(FLS_ECUSOLVER, "cublasDtrsv failed");
+  FLS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (resid_norm) *resid_norm = std::fabs(rnn);
+  return FLS_OK;
+}
+
+fls_status fls_qr_r(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda, int64_t n_cols,
+                    double *R, int64_t ldr) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!M || !R) return fail(FLS_EINVAL, "M or R is NULL");
+  if (n_rows < 1 || n_cols < 1 || lda < n_rows)
+    return fail(FLS_EINVAL, "bad sizes n_rows %lld n_cols %lld lda %lld", (long long)n_rows,
+                (long long)n_cols, (long long)lda);
+  const int64_t k = n_rows < n_cols ? n_rows : n_cols;
+  if (ldr < k) return fail(FLS_EINVAL, "ldr %lld < %lld", (long long)ldr, (long long)k);
+  DeviceGuard g(ctx->device);
+  if (fls_status s = fls_sync(ctx)) return s;
+  if (fls_status s = ensure_handles(ctx)) return s;
+  if (fls_status s = geqrf_inplace(ctx, M, n_rows, lda, n_cols)) return s;
+  cudaError_t e = launch_copy_upper(M, lda, k, n_cols, R, ldr, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "copy_upper");
+  FLS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return FLS_OK;
+}
+
+fls_status fls_frob2(fls_ctx *ctx, const double *A, int64_t n_rows, int64_t lda, int64_t n_cols,
+                     double *out) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!A || !out) return fail(FLS_EINVAL, "A or out is NULL");
+  if (n_rows < 0 || n_cols < 0 || lda < n_rows) return fail(FLS_EINVAL, "bad sizes");
+  DeviceGuard g(ctx->device);
+  const int nblk = 592;  // 4 x 148 SMs, fixed -> deterministic summation order
+  cudaError_t e = launch_frob2(A, lda, n_rows, n_cols, ctx->d_scratch + 8, nblk, ctx->d_scratch,
+                               ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "frob2");
+  FLS_CUDA(cudaMemcpyAsync(out, ctx->d_scratch, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  FLS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return FLS_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+fls_status fls_eval(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
+                    int64_t n_features, int32_t normalize, const double *beta,
+                    const fls_operator *op, const double *X, int64_t n_points, double *out) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (dim < 1 || dim > FLS_MAX_DIM) return fail(FLS_EINVAL, "dim %d not in 1..%d", dim, FLS_MAX_DIM);
+  if (n_features < 1) return fail(FLS_EINVAL, "n_features < 1");
+  if (!W || !b || !beta) return fail(FLS_EINVAL, "W, b or beta is NULL");
+  if (n_points < 0) return fail(FLS_EINVAL, "n_points < 0");
+  if (n_points > 0 && (!X || !out)) return fail(FLS_EINVAL, "X or out is NULL");
+  fls_term ident;
+  std::memset(&ident, 0, sizeof ident);
+  ident.coef = 1.0;
+  ident.field = -1;
+  fls_operator idop{dim, 1, &ident};
+  OpPlan pl;
+  if (fls_status s = plan_operator(op ? op : &idop, dim, 0, false, pl, "eval operator")) return s;
+  if (n_points == 0) return FLS_OK;
+  DeviceGuard g(ctx->device);
+  const int S = pf_stride(dim, 0, KM_SINCOS);
+  // eval records live after the largest assemble layout we may have (separate region)
+  const int Smax = pf_stride(FLS_MAX_DIM, FLS_MAX_FIELDS, KM_SINCOS);
+  if (fls_status s = ensure_ws(ctx, (size_t)n_features * Smax * sizeof(double))) return s;
+  PrefArgs pa;
+  std::memset(&pa, 0, sizeof pa);
+  pa.W = W;
+  pa.b = b;
+  pa.F = n_features;
+  pa.D = dim;
+  pa.n_terms = pl.n_terms;
+  pa.G = 0;
+  pa.pmode = PM_SINCOS;
+  pa.S = S;
+  pa.scale = normalize ? 1.0 / std::sqrt((double)n_features) : 1.0;
+  pa.pf = ctx->ws;
+  pa.err = ctx->d_err;
+  std::memcpy(pa.terms, pl.terms, sizeof pl.terms);
+  cudaError_t e = launch_prefactor(pa, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "prefactor_kernel");
+  EvalArgs ea;
+  ea.pf = pa.pf;
+  ea.S = S;
+  ea.F = n_features;
+  ea.beta = beta;
+  ea.X = X;
+  ea.n = n_points;
+  ea.out = out;
+  ea.err = ctx->d_err;
+  e = launch_eval(dim, ea, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "eval_kernel");
+  return FLS_OK;
+}
+
+}  // extern "C"

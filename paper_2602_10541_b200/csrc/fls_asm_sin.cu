@@ -1,0 +1,46 @@
+// fls_asm_sin.cu -- instantiations of the column-major assembly kernel, KM_SIN family
+// (split from the other family so the two compile in parallel).
+#include "fls_assemble.cuh"
+
+namespace fls {
+
+template <int D, int G>
+static cudaError_t go_sin(const AsmArgs &a, cudaStream_t st) {
+  constexpr int S = pf_stride(D, G, KM_SIN);
+  const size_t smem = (size_t)kFC * S * sizeof(double);
+  const int64_t span = a.lr1 - (a.lr0 & ~int64_t(1));
+  const dim3 grid((unsigned)((span + kRowsCTA - 1) / kRowsCTA), (unsigned)((a.F + kFC - 1) / kFC));
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(assemble_cm_kernel<D, G, KM_SIN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  assemble_cm_kernel<D, G, KM_SIN><<<grid, kNT, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assemble_cm_sin(int D, int G, const AsmArgs &a, cudaStream_t st) {
+#define FLS_G(d)                              \
+  switch (G) {                                \
+    case 0: return go_sin<d, 0>(a, st);     \
+    case 1: return go_sin<d, 1>(a, st);     \
+    case 2: return go_sin<d, 2>(a, st);     \
+    case 3: return go_sin<d, 3>(a, st);     \
+    case 4: return go_sin<d, 4>(a, st);     \
+    default: return cudaErrorInvalidValue;    \
+  }
+  switch (D) {
+    case 1: FLS_G(1)
+    case 2: FLS_G(2)
+    case 3: FLS_G(3)
+    case 4: FLS_G(4)
+    case 5: FLS_G(5)
+    case 6: FLS_G(6)
+    case 7: FLS_G(7)
+    case 8: FLS_G(8)
+    default: return cudaErrorInvalidValue;
+  }
+#undef FLS_G
+}
+
+}  // namespace fls

@@ -1,0 +1,74 @@
+// fls_device.cuh -- device-side building blocks shared by the libfls kernels.
+//
+// Product code (CUDA path).  Nothing here is shared with oracle/ (DESIGN.md §2).
+//
+// Half-turn trigonometry.  The kernels carry the phase in half turns,
+//     h = z / pi = sum_k (W_jk / pi) x_ik + b_j / pi,
+// with W / pi and b / pi prescaled once per feature (prefactor kernel), so the phase costs d
+// DFMA and no multiply by 1/pi.  Range reduction to f = h - n, n = rint(h), |f| <= 1/2, uses
+// the 1.5 * 2^52 magic constant (2 DADD + 1 DADD, no F2I / I2F conversions), and
+//     sin(z) = (-1)^n sin(pi f),   cos(z) = (-1)^n cos(pi f),
+// with (-1)^n applied by an integer XOR on the sign bit.  sin(pi f) = f p(f^2) (7 coefficients,
+// max abs error 3.97e-14) and cos(pi f) = q(f^2) (8 coefficients, 1.08e-14) are minimax fits
+// produced by tools/fit_sinpoly.py.  Budget per sin: 3 DADD + 1 DMUL + 6 DFMA + 1 DMUL.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fls {
+
+constexpr double kPi = 3.141592653589793238462643383279502884;
+constexpr double kInvPi = 0.318309886183790671537767526745028724;
+constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: x + kMagic rounds x to an integer
+
+// sin(pi f) = f * p(f^2), |f| <= 1/2 -- tools/fit_sinpoly.py 7 sin
+__device__ __forceinline__ double sinpi_core(double f, double u) {
+  double p = 0x1.d3d9ca396c5b5p-12;
+  p = fma(p, u, -0x1.e289957d36087p-8);
+  p = fma(p, u, 0x1.5076b5c39bedfp-4);
+  p = fma(p, u, -0x1.32d2c80461e85p-1);
+  p = fma(p, u, 0x1.466bc666fa76ep+1);
+  p = fma(p, u, -0x1.4abbce622b70dp+2);
+  p = fma(p, u, 0x1.921fb544422b9p+1);
+  return f * p;
+}
+
+// cos(pi f) = q(f^2), |f| <= 1/2 -- tools/fit_sinpoly.py 8 cos
+__device__ __forceinline__ double cospi_core(double u) {
+  double q = -0x1.a75f6839218cdp-14;
+  q = fma(q, u, 0x1.f97f5b4f53910p-10);
+  q = fma(q, u, -0x1.a6d11187be151p-6);
+  q = fma(q, u, 0x1.e1f504256b638p-3);
+  q = fma(q, u, -0x1.55d3c7e0ba51dp+0);
+  q = fma(q, u, 0x1.03c1f081b29f6p+2);
+  q = fma(q, u, -0x1.3bd3cc9be45b0p+2);
+  q = fma(q, u, 1.0);
+  return q;
+}
+
+// h (phase in half turns) -> f in [-1/2, 1/2] and the sign word (n odd -> 0x80000000).
+// Valid for |h| < 2^51; accuracy of the caller's h is ~ulp(|h|).
+__device__ __forceinline__ double halfturn(double h, int &sgn) {
+  const double t = __dadd_rn(h, kMagic);
+  sgn = __double2loint(t) << 31;
+  const double n = __dsub_rn(t, kMagic);
+  return __dsub_rn(h, n);
+}
+
+__device__ __forceinline__ double flipsign(double x, int sgn) {
+  return __hiloint2double(__double2hiint(x) ^ sgn, __double2loint(x));
+}
+
+// sin(pi h) for any |h| < 2^51
+__device__ __forceinline__ double sin_halfturns(double h) {
+  int sgn;
+  const double f = halfturn(h, sgn);
+  return sinpi_core(flipsign(f, sgn), f * f);
+}
+
+__device__ __forceinline__ bool finite(double v) {
+  // exponent field all ones <=> Inf / NaN
+  return (__double2hiint(v) & 0x7ff00000) != 0x7ff00000;
+}
+
+}  // namespace fls

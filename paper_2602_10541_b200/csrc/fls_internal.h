@@ -1,0 +1,99 @@
+// fls_internal.h -- host-side internals of libfls (ctx, errors, kernel launch interfaces).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fls.h"
+
+namespace fls {
+
+// per-feature parameter layouts produced by the prefactor kernel
+enum PrefMode : int32_t {
+  PM_SIN = 0,      // A = (P_0 + sum_g c_g P_g) sin z
+  PM_COSSHIFT = 1, // all terms odd: cos z = sin(z + pi/2) -> b' += 1/2, P_g = Pc_g
+  PM_FOLD = 2,     // constant coefficients, mixed parity: Ps sin z + Pc cos z = rho sin(z + psi)
+  PM_SINCOS = 3    // general: (Ps_0 + sum c_g Ps_g) sin z + (Pc_0 + sum c_g Pc_g) cos z
+};
+
+// kernel families
+enum KMode : int32_t { KM_SIN = 0, KM_SINCOS = 1 };
+
+constexpr int kNT = 256;           // threads per CTA, column-major assembly
+constexpr int kRowsCTA = 4 * kNT;  // 4 rows per thread (two 16-byte row pairs)
+constexpr int kFC = 128;           // features per CTA tile
+constexpr int kRmRows = 64;        // rows per CTA, row-major assembly
+constexpr int kRmFeat = 64;        // features per CTA (2 per lane), row-major assembly
+
+struct TermDev {
+  double coef;
+  int8_t alpha[FLS_MAX_DIM];
+  int8_t group;  // 0 = constant coefficient, 1..G = compacted field groups
+  int8_t pad[7];
+};
+
+struct PrefArgs {
+  const double *W;
+  const double *b;
+  int64_t F;
+  int32_t D;
+  int32_t n_terms;
+  int32_t G;      // number of field groups
+  int32_t pmode;  // PrefMode
+  int32_t S;      // doubles per feature in pf
+  double scale;   // s * weight
+  double *pf;
+  unsigned *err;
+  TermDev terms[FLS_MAX_TERMS];
+};
+
+struct AsmArgs {
+  const double *pf;
+  int64_t F;
+  const double *X;
+  const double *fields;
+  const double *values;
+  double weight;
+  int64_t pt0;  // point index of local row lr0
+  int64_t lr0, lr1;
+  double *A;
+  int64_t lda;
+  double *rhs;
+  unsigned *err;
+  int32_t nf;                    // n_fields of the block (row stride of fields)
+  int32_t vec;                   // 16-byte vector stores allowed
+  int32_t gfield[FLS_MAX_FIELDS];// field id of group g+1
+};
+
+struct EvalArgs {
+  const double *pf;  // PM_SINCOS layout, G = 0: [W'_0..W'_{D-1}, b', Ps, Pc] (+pad)
+  int32_t S;
+  int64_t F;
+  const double *beta;
+  const double *X;
+  int64_t n;
+  double *out;
+  unsigned *err;
+};
+
+// layout helper shared by host and kernels
+__host__ __device__ constexpr int pf_stride(int D, int G, int kmode) {
+  return (D + 1 + (G + 1) * (kmode == KM_SINCOS ? 2 : 1) + 1) & ~1;
+}
+
+// launchers (fls_kernels.cu / fls_assemble_*.cu)
+cudaError_t launch_features(int32_t dim, int64_t F, double sigma, uint64_t seed, double *W,
+                            double *b, cudaStream_t st);
+cudaError_t launch_prefactor(const PrefArgs &a, cudaStream_t st);
+cudaError_t launch_assemble_cm(int D, int G, int kmode, const AsmArgs &a, cudaStream_t st);
+cudaError_t launch_assemble_rm(int D, int G, int kmode, const AsmArgs &a, cudaStream_t st);
+cudaError_t launch_eval(int D, const EvalArgs &a, cudaStream_t st);
+cudaError_t launch_ridge_fill(double *Ab, int64_t lda, int64_t row0, int64_t F, double sqrt_mu,
+                              cudaStream_t st);
+cudaError_t launch_copy_upper(const double *M, int64_t lda, int64_t k, int64_t n, double *R,
+                              int64_t ldr, cudaStream_t st);
+cudaError_t launch_min_abs_diag(const double *M, int64_t lda, int64_t n, double *out,
+                                cudaStream_t st);
+cudaError_t launch_frob2(const double *A, int64_t lda, int64_t m, int64_t n, double *partials,
+                         int nblk, double *out, cudaStream_t st);
+
+}  // namespace fls

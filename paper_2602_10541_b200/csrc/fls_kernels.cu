@@ -1,0 +1,306 @@
+// fls_kernels.cu -- features, prefactor fold, eval and solve-helper kernels of libfls.
+//
+// Product code.  Paper = PAPER.md (arxiv 2602.10541), cited P:L<line>.
+#include <math.h>
+
+#include "fls_device.cuh"
+#include "fls_internal.h"
+
+namespace fls {
+
+// ------------------------------------------------------------------------------------------
+// a1 features (Alg. 1 line 1).  Philox4x64-10, one block of 4 x 64-bit words
+// per thread (header fls.h documents the stream layout).
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void philox4x64(uint64_t c[4], uint64_t k0, uint64_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t M0 = 0xD2E7470EE14C6C93ULL, M1 = 0xCA5A826395121157ULL;
+    const uint64_t hi0 = __umul64hi(M0, c[0]), lo0 = M0 * c[0];
+    const uint64_t hi1 = __umul64hi(M1, c[2]), lo1 = M1 * c[2];
+    const uint64_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += 0x9E3779B97F4A7C15ULL;
+    k1 += 0xBB67AE8584CAA73BULL;
+  }
+}
+
+__device__ __forceinline__ double u01(uint64_t r) {
+  return (double)(r >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// thread t owns Philox block t: raw words 4t..4t+3 of stream 1 -> normals 4t..4t+3
+// (Box-Muller pairs (4t, 4t+1) and (4t+2, 4t+3)); of stream 2 -> b_{4t..4t+3}.
+__global__ void features_kernel(int32_t D, int64_t F, double sigma, uint64_t seed, double *W,
+                                double *b) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n_norm = F * D;
+  const double two_pi = 6.283185307179586476925286766559;
+  if (4 * t < n_norm) {
+    uint64_t c[4] = {(uint64_t)t + 1, 0, 0, 0};
+    philox4x64(c, seed, 1);
+#pragma unroll
+    for (int pr = 0; pr < 2; ++pr) {
+      const int64_t m0 = 4 * t + 2 * pr;
+      if (m0 >= n_norm) break;
+      const double u1 = u01(c[2 * pr]), u2 = u01(c[2 * pr + 1]);
+      const double rad = sqrt(-2.0 * log(1.0 - u1));
+      const double th = two_pi * u2;
+      double sn, cs;
+      sincos(th, &sn, &cs);
+      W[m0] = sigma * (rad * cs);
+      if (m0 + 1 < n_norm) W[m0 + 1] = sigma * (rad * sn);
+    }
+  }
+  if (4 * t < F) {
+    uint64_t c[4] = {(uint64_t)t + 1, 0, 0, 0};
+    philox4x64(c, seed, 2);
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+      if (4 * t + w < F) b[4 * t + w] = two_pi * u01(c[w]);
+  }
+}
+
+cudaError_t launch_features(int32_t dim, int64_t F, double sigma, uint64_t seed, double *W,
+                            double *b, cudaStream_t st) {
+  const int64_t n_norm = F * dim;
+  const int64_t blocks4 = (((n_norm > F ? n_norm : F) + 3) / 4 + 255) / 256;
+  features_kernel<<<(unsigned)blocks4, 256, 0, st>>>(dim, F, sigma, seed, W, b);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// a2 prefactor fold (Eq. 2; Cor. 1 P:L102; App. F angle addition P:L733).
+// For each feature j and coefficient group g:
+//   Ps_gj = s w sum_{t in g, |a_t| even} c_t (+1,-1 for |a_t| mod 4 = 0,2) prod_k W_jk^a_tk
+//   Pc_gj = s w sum_{t in g, |a_t| odd } c_t (+1,-1 for |a_t| mod 4 = 1,3) prod_k W_jk^a_tk
+// and the per-feature record [W_j / pi, b'_j / pi, P...] the assembly kernel reads.
+// ------------------------------------------------------------------------------------------
+__global__ void prefactor_kernel(const PrefArgs a) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.F) return;
+  double w[FLS_MAX_DIM];
+  bool ok = true;
+  for (int k = 0; k < a.D; ++k) {
+    w[k] = a.W[j * a.D + k];
+    ok &= finite(w[k]);
+  }
+  double bj = a.b[j];
+  ok &= finite(bj);
+  if (!ok) atomicOr(a.err, 1u);
+  double Ps[FLS_MAX_FIELDS + 1], Pc[FLS_MAX_FIELDS + 1];
+  for (int g = 0; g <= FLS_MAX_FIELDS; ++g) Ps[g] = Pc[g] = 0.0;
+  for (int t = 0; t < a.n_terms; ++t) {
+    const TermDev &T = a.terms[t];
+    double m = T.coef;
+    int order = 0;
+    for (int k = 0; k < a.D; ++k)
+      for (int e = 0; e < T.alpha[k]; ++e) {
+        m *= w[k];
+        ++order;
+      }
+    const int p = order & 3;  // Phi_{|alpha| mod 4}: sin, cos, -sin, -cos
+    if (p & 2) m = -m;
+    if (p & 1)
+      Pc[T.group] += m;
+    else
+      Ps[T.group] += m;
+  }
+  double *out = a.pf + j * a.S;
+  for (int k = 0; k < a.D; ++k) out[k] = w[k] * kInvPi;
+  double bp = bj;
+  int o = a.D + 1;
+  switch (a.pmode) {
+    case PM_SIN:
+      for (int g = 0; g <= a.G; ++g) out[o++] = a.scale * Ps[g];
+      out[a.D] = bp * kInvPi;
+      break;
+    case PM_COSSHIFT:  // cos z = sin(z + pi/2)  (App. F quarter-wave shift)
+      for (int g = 0; g <= a.G; ++g) out[o++] = a.scale * Pc[g];
+      out[a.D] = bp * kInvPi + 0.5;
+      break;
+    case PM_FOLD: {    // Ps sin z + Pc cos z = rho sin(z + psi)
+      const double ps = a.scale * Ps[0], pc = a.scale * Pc[0];
+      const double rho = hypot(ps, pc);
+      const double psi = atan2(pc, ps);
+      out[o++] = rho;
+      out[a.D] = (bp + psi) * kInvPi;
+      break;
+    }
+    default:           // PM_SINCOS
+      for (int g = 0; g <= a.G; ++g) {
+        out[o++] = a.scale * Ps[g];
+        out[o++] = a.scale * Pc[g];
+      }
+      out[a.D] = bp * kInvPi;
+      break;
+  }
+  for (; o < a.S; ++o) out[o] = 0.0;
+}
+
+cudaError_t launch_prefactor(const PrefArgs &a, cudaStream_t st) {
+  const unsigned nb = (unsigned)((a.F + 127) / 128);
+  prefactor_kernel<<<nb, 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// a10 eval (Alg. 1 line 6):  out_i = sum_j beta_j (Ps_j sin z_ij + Pc_j cos z_ij),
+// with Ps = s, Pc = 0 for u_N itself (identity operator) -- A is never materialised.
+// One warp per 4 rows; lanes stride over features; fixed-order warp reduction.
+// ------------------------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256) eval_kernel(const EvalArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = ((int64_t)blockIdx.x * 8 + warp) * 4;
+  double x[4][D];
+  bool bad = false;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int64_t r = r0 + q;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      x[q][k] = r < a.n ? a.X[r * D + k] : 0.0;
+      bad |= !finite(x[q][k]);
+    }
+  }
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t j = lane; j < a.F; j += 32) {
+    const double *p = a.pf + j * a.S;
+    double w[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) w[k] = p[k];
+    const double bp = p[D], ps = p[D + 1], pc = p[D + 2];
+    const double bt = a.beta[j];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double h = bp;
+#pragma unroll
+      for (int k = 0; k < D; ++k) h = fma(w[k], x[q][k], h);
+      int sgn;
+      const double f = halfturn(h, sgn);
+      const double u = f * f;
+      const double s = sinpi_core(f, u), c = cospi_core(u);
+      acc[q] = fma(bt, flipsign(fma(ps, s, pc * c), sgn), acc[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (r0 + q < a.n) a.out[r0 + q] = acc[q];
+  }
+  if (bad) atomicOr(a.err, 1u);
+}
+
+cudaError_t launch_eval(int D, const EvalArgs &a, cudaStream_t st) {
+  const unsigned nb = (unsigned)((a.n + 31) / 32);
+  switch (D) {
+#define FLS_EV(d) \
+  case d: eval_kernel<d><<<nb, 256, 0, st>>>(a); break;
+    FLS_EV(1) FLS_EV(2) FLS_EV(3) FLS_EV(4) FLS_EV(5) FLS_EV(6) FLS_EV(7) FLS_EV(8)
+#undef FLS_EV
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// solve helpers
+// ------------------------------------------------------------------------------------------
+// rows [row0, row0 + F) of columns 0..F of the column-major [A | b]: [sqrt_mu I | 0]
+__global__ void ridge_fill_kernel(double *Ab, int64_t lda, int64_t row0, int64_t F, double sq) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = F * (F + 1);
+  if (idx >= n) return;
+  const int64_t col = idx / F, i = idx % F;
+  Ab[col * lda + row0 + i] = (col == i) ? sq : 0.0;
+}
+
+cudaError_t launch_ridge_fill(double *Ab, int64_t lda, int64_t row0, int64_t F, double sqrt_mu,
+                              cudaStream_t st) {
+  const int64_t n = F * (F + 1);
+  ridge_fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Ab, lda, row0, F, sqrt_mu);
+  return cudaGetLastError();
+}
+
+// R (k x n, column-major, ldr) = upper trapezoid of M's first k rows
+__global__ void copy_upper_kernel(const double *M, int64_t lda, int64_t k, int64_t n, double *R,
+                                  int64_t ldr) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= k * n) return;
+  const int64_t col = idx / k, i = idx % k;
+  R[col * ldr + i] = (i <= col) ? M[col * lda + i] : 0.0;
+}
+
+cudaError_t launch_copy_upper(const double *M, int64_t lda, int64_t k, int64_t n, double *R,
+                              int64_t ldr, cudaStream_t st) {
+  const int64_t tot = k * n;
+  if (tot == 0) return cudaSuccess;
+  copy_upper_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(M, lda, k, n, R, ldr);
+  return cudaGetLastError();
+}
+
+__global__ void min_abs_diag_kernel(const double *M, int64_t lda, int64_t n, double *out) {
+  __shared__ double sm[256];
+  double m = INFINITY;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmin(m, fabs(M[i * lda + i]));
+  sm[threadIdx.x] = m;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sm[threadIdx.x] = fmin(sm[threadIdx.x], sm[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sm[0];
+}
+
+cudaError_t launch_min_abs_diag(const double *M, int64_t lda, int64_t n, double *out,
+                                cudaStream_t st) {
+  min_abs_diag_kernel<<<1, 256, 0, st>>>(M, lda, n, out);
+  return cudaGetLastError();
+}
+
+// deterministic two-pass sum of squares: fixed grid, fixed per-block order
+__global__ void frob2_partial_kernel(const double *A, int64_t lda, int64_t m, int64_t n,
+                                     double *partials) {
+  __shared__ double sm[256];
+  double acc = 0.0;
+  const int64_t tot = m * n;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < tot;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = idx / m, i = idx % m;
+    const double v = A[col * lda + i];
+    acc = fma(v, v, acc);
+  }
+  sm[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sm[threadIdx.x] += sm[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = sm[0];
+}
+
+__global__ void frob2_final_kernel(const double *partials, int nblk, double *out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < nblk; ++i) s += partials[i];
+    *out = s;
+  }
+}
+
+cudaError_t launch_frob2(const double *A, int64_t lda, int64_t m, int64_t n, double *partials,
+                         int nblk, double *out, cudaStream_t st) {
+  frob2_partial_kernel<<<nblk, 256, 0, st>>>(A, lda, m, n, partials);
+  frob2_final_kernel<<<1, 32, 0, st>>>(partials, nblk, out);
+  return cudaGetLastError();
+}
+
+}  // namespace fls

@@ -1,0 +1,242 @@
+"""Thin Python binding of libfls with the C ABI's names (include/fls.h).
+
+Argument marshalling only: torch CUDA tensors in, device pointers + sizes out to the C ABI;
+every step of the path runs in libfls kernels (or cuSOLVER/cuBLAS inside fls_solve).  There
+is no CPU fallback -- calling anything here without a CUDA device and a built libfls.so
+raises.
+
+    ctx = Context()                                   # borrows torch's current stream
+    W, b = fls_features(ctx, dim, F, sigma, seed)
+    A, rhs = fls_assemble(ctx, W, b, blocks)         # [A | rhs] column-major, lda padded
+    beta, res = fls_solve(ctx, Ab, n_rows, lda, F)   # destroys Ab
+    u = fls_eval(ctx, W, b, beta, X)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from typing import List, Optional, Sequence, Tuple
+
+import torch
+
+from . import _abi
+from ._abi import FLS_COL_MAJOR, FLS_ROW_MAJOR, FlsError, check
+
+Term = Tuple[Sequence[int], float, int]   # (alpha, coef, field)
+
+__all__ = ["Context", "Block", "fls_features", "fls_assemble", "fls_solve", "fls_qr_r",
+           "fls_frob2", "fls_eval", "fls_sync", "fls_ctx_timing", "fls_ctx_timing_read", "FlsError", "FLS_COL_MAJOR", "FLS_ROW_MAJOR",
+           "round_up"]
+
+
+def round_up(n: int, m: int) -> int:
+    return ((n + m - 1) // m) * m
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _dev_f64(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != torch.float64:
+        raise TypeError(f"{name} must be float64")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+class Context:
+    """fls_ctx on a device, borrowing a CUDA stream (default: torch's current stream)."""
+
+    def __init__(self, device: Optional[int] = None, stream: Optional[torch.cuda.Stream] = None):
+        lib = _abi.load()
+        if not torch.cuda.is_available():
+            raise FlsError(3, "no CUDA device: libfls has no CPU path")
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        h = C.c_void_p()
+        check(lib.fls_ctx_create(self.device, C.c_void_p(self.stream.cuda_stream), C.byref(h)))
+        self.handle = h
+
+    def set_stream(self, stream: torch.cuda.Stream):
+        self.stream = stream
+        check(_abi.load().fls_ctx_set_stream(self.handle, C.c_void_p(stream.cuda_stream)))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _abi.load().fls_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def fls_sync(ctx: Context):
+    check(_abi.load().fls_sync(ctx.handle))
+
+
+def fls_ctx_timing(ctx: Context, enable: bool = True):
+    check(_abi.load().fls_ctx_timing(ctx.handle, int(bool(enable))))
+
+
+def fls_ctx_timing_read(ctx: Context):
+    """(summed assembly-kernel ms, launches) since the last enable / read"""
+    ms = C.c_double(0.0)
+    n = C.c_int64(0)
+    check(_abi.load().fls_ctx_timing_read(ctx.handle, C.byref(ms), C.byref(n)))
+    return ms.value, n.value
+
+
+class _Op:
+    def __init__(self, dim: int, terms: Sequence[Term]):
+        n = len(terms)
+        self.arr = (_abi.fls_term * max(n, 1))()
+        for t, (alpha, coef, field) in enumerate(terms):
+            for k, v in enumerate(alpha):
+                self.arr[t].alpha[k] = int(v)
+            self.arr[t].coef = float(coef)
+            self.arr[t].field = int(field)
+        self.op = _abi.fls_operator(int(dim), n, C.cast(self.arr, C.POINTER(_abi.fls_term)))
+
+
+@dataclasses.dataclass
+class Block:
+    """one row block of Eq. 3 (device tensors)"""
+    X: torch.Tensor                      # (n, d) float64 CUDA
+    terms: List[Term]
+    weight: float = 1.0
+    values: Optional[torch.Tensor] = None
+    fields: Optional[torch.Tensor] = None   # (n, G)
+
+    @property
+    def n(self) -> int:
+        return int(self.X.shape[0])
+
+
+def fls_features(ctx: Context, dim: int, n_features: int, sigma: float, seed: int,
+                 W: Optional[torch.Tensor] = None, b: Optional[torch.Tensor] = None):
+    dev = torch.device("cuda", ctx.device)
+    W = torch.empty((n_features, dim), dtype=torch.float64, device=dev) if W is None else W
+    b = torch.empty((n_features,), dtype=torch.float64, device=dev) if b is None else b
+    check(_abi.load().fls_features(ctx.handle, int(dim), int(n_features), float(sigma),
+                                   C.c_uint64(int(seed) & (2**64 - 1)), _ptr(W), _ptr(b)))
+    return W, b
+
+
+class BlockSet:
+    """marshalled fls_block array (keeps the ctypes structs alive); reusable across calls"""
+
+    def __init__(self, blocks: Sequence[Block], dim: int):
+        self.blocks = list(blocks)
+        self.ops = []
+        self.arr = (_abi.fls_block * len(self.blocks))()
+        for q, blk in enumerate(self.blocks):
+            _dev_f64(blk.X, "X")
+            op = _Op(dim, blk.terms)
+            self.ops.append(op)
+            B = self.arr[q]
+            B.X = blk.X.data_ptr()
+            B.n_points = blk.n
+            B.op = C.pointer(op.op)
+            if blk.fields is not None:
+                _dev_f64(blk.fields, "fields")
+                B.coef_fields = blk.fields.data_ptr()
+                B.n_fields = int(blk.fields.shape[1])
+            else:
+                B.coef_fields = None
+                B.n_fields = 0
+            B.weight = float(blk.weight)
+            if blk.values is not None:
+                _dev_f64(blk.values, "values")
+            B.values = blk.values.data_ptr() if blk.values is not None else None
+        self.total = sum(b.n for b in self.blocks)
+
+
+def fls_assemble(ctx: Context, W: torch.Tensor, b: torch.Tensor, blocks, *,
+                 normalize: bool = True, row_begin: int = 0, row_end: Optional[int] = None,
+                 A: Optional[torch.Tensor] = None, lda: Optional[int] = None,
+                 layout: int = FLS_COL_MAJOR, rhs: Optional[torch.Tensor] = None,
+                 with_rhs: bool = True, extra_rows: int = 0):
+    """Assemble global rows [row_begin, row_end) of [A | rhs].
+
+    Column-major default: returns (Ab, lda) where Ab is a flat float64 tensor of
+    (F + 1) * lda doubles; column j at Ab[j*lda : j*lda + n_local]; rhs in column F.
+    extra_rows reserves rows after the local block (e.g. ridge rows for fls_solve).
+    Row-major: returns (A (n_local, lda) with lda >= F, rhs (n_local,))."""
+    _dev_f64(W, "W")
+    _dev_f64(b, "b")
+    F, dim = int(W.shape[0]), int(W.shape[1])
+    bs = blocks if isinstance(blocks, BlockSet) else BlockSet(blocks, dim)
+    row_end = bs.total if row_end is None else int(row_end)
+    n_local = row_end - int(row_begin)
+    dev = W.device
+    if layout == FLS_COL_MAJOR:
+        if lda is None:
+            lda = round_up(max(n_local + extra_rows, 1), 4)
+        if A is None:
+            A = torch.empty(((F + 1) * lda,), dtype=torch.float64, device=dev)
+        if with_rhs and rhs is None:
+            rhs = A[F * lda:]
+    else:
+        if lda is None:
+            lda = round_up(F, 2)
+        if A is None:
+            A = torch.empty((max(n_local, 0), lda), dtype=torch.float64, device=dev)
+        if with_rhs and rhs is None:
+            rhs = torch.empty((max(n_local, 0),), dtype=torch.float64, device=dev)
+    check(_abi.load().fls_assemble(ctx.handle, _ptr(W), _ptr(b), dim, F, int(bool(normalize)),
+                                   bs.arr, len(bs.blocks), int(row_begin), row_end, _ptr(A),
+                                   int(lda), int(layout), _ptr(rhs) if with_rhs else None))
+    if layout == FLS_COL_MAJOR:
+        return A, lda
+    return A, rhs
+
+
+def fls_solve(ctx: Context, Ab: torch.Tensor, n_rows: int, lda: int, n_features: int,
+              sqrt_mu: float = 0.0, beta: Optional[torch.Tensor] = None):
+    """beta = argmin ||A beta - b||^2 + mu ||beta||^2 on the column-major [A | b] (destroyed)."""
+    _dev_f64(Ab, "Ab")
+    if beta is None:
+        beta = torch.empty((n_features,), dtype=torch.float64, device=Ab.device)
+    res = C.c_double(0.0)
+    check(_abi.load().fls_solve(ctx.handle, _ptr(Ab), int(n_rows), int(lda), int(n_features),
+                                float(sqrt_mu), _ptr(beta), C.byref(res)))
+    return beta, res.value
+
+
+def fls_qr_r(ctx: Context, M: torch.Tensor, n_rows: int, lda: int, n_cols: int,
+             R: Optional[torch.Tensor] = None, ldr: Optional[int] = None):
+    k = min(n_rows, n_cols)
+    ldr = k if ldr is None else ldr
+    if R is None:
+        R = torch.empty((n_cols * ldr,), dtype=torch.float64, device=M.device)
+    check(_abi.load().fls_qr_r(ctx.handle, _ptr(M), int(n_rows), int(lda), int(n_cols), _ptr(R),
+                               int(ldr)))
+    return R, ldr
+
+
+def fls_frob2(ctx: Context, A: torch.Tensor, n_rows: int, lda: int, n_cols: int) -> float:
+    out = C.c_double(0.0)
+    check(_abi.load().fls_frob2(ctx.handle, _ptr(A), int(n_rows), int(lda), int(n_cols),
+                                C.byref(out)))
+    return out.value
+
+
+def fls_eval(ctx: Context, W: torch.Tensor, b: torch.Tensor, beta: torch.Tensor, X: torch.Tensor,
+             terms: Optional[Sequence[Term]] = None, normalize: bool = True,
+             out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    for t, nm in ((W, "W"), (b, "b"), (beta, "beta"), (X, "X")):
+        _dev_f64(t, nm)
+    F, dim = int(W.shape[0]), int(W.shape[1])
+    n = int(X.shape[0])
+    if out is None:
+        out = torch.empty((n,), dtype=torch.float64, device=X.device)
+    op = _Op(dim, terms) if terms is not None else None
+    check(_abi.load().fls_eval(ctx.handle, _ptr(W), _ptr(b), dim, F, int(bool(normalize)),
+                               _ptr(beta), C.pointer(op.op) if op else None, _ptr(X), n, _ptr(out)))
+    return out

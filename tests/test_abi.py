@@ -1,0 +1,70 @@
+"""C-ABI library: loads, exports every symbol include/fls.h declares, and host-side argument
+validation that needs no device (CPU, -m "not gpu").  No compute calls here."""
+import ctypes as C
+import os
+import subprocess
+
+import pytest
+
+from paper_2602_10541_b200 import _abi
+from paper_2602_10541_b200.build import LIB, build
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build()
+    return _abi.load()
+
+
+def test_library_exports_every_header_symbol(lib):
+    syms = _abi.header_symbols()
+    assert {"fls_features", "fls_assemble", "fls_solve", "fls_eval"} <= set(syms)
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    for s in syms:
+        assert hasattr(lib, s)
+    # no stray C++ symbols leak (visibility hidden)
+    assert all(e.startswith("fls_") for e in exported), sorted(e for e in exported if not e.startswith("fls_"))
+
+
+def test_api_version_and_status_strings(lib):
+    assert lib.fls_api_version() == 1
+    for k, v in _abi.STATUS.items():
+        assert lib.fls_status_string(k).decode() == v
+
+
+def test_null_ctx_is_einval_without_device(lib):
+    assert lib.fls_features(None, 3, 10, 1.0, 0, None, None) == 1
+    assert "ctx" in lib.fls_last_error().decode()
+    assert lib.fls_assemble(None, None, None, 3, 10, 1, None, 0, 0, 0, None, 0, 0, None) == 1
+    assert lib.fls_solve(None, None, 0, 0, 0, 0.0, None, None) == 1
+    assert lib.fls_eval(None, None, None, 1, 1, 1, None, None, None, 0, None) == 1
+    assert lib.fls_sync(None) == 1
+    assert lib.fls_ctx_destroy(None) == 0
+    h = C.c_void_p()
+    assert lib.fls_ctx_create(0, None, None) == 1
+
+
+def test_ctx_create_without_gpu_fails_loudly(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    h = C.c_void_p()
+    st = lib.fls_ctx_create(0, None, C.byref(h))
+    assert st in (1, 3) and not h.value
+
+
+def test_product_package_never_imports_oracle():
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pkg = os.path.join(root, "paper_2602_10541_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "oracle.c" not in txt and "liboracle" not in txt, f
+    # and the oracle never includes the product headers
+    orc = open(os.path.join(root, "oracle", "oracle.c")).read()
+    assert "fls.h" not in orc and "fls_device" not in orc

@@ -1,0 +1,282 @@
+"""GPU parity: libfls (through the C ABI) against the CPU oracle, element by element.
+
+Entry metric: |A_gpu - A_orc| <= 1e-12 * S_ij with
+S_ij = w s sum_t |c_t(x_i)| |prod_k W_jk^alpha_tk|.  rhs entries are a single product on both
+sides and must be bit-exact.  Fitted u at 10,000 held-out points: relative L2 <= 1e-6.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as wl
+from gpu_common import ENTRY_TOL, U_TOL, dev_blocks, rows_from_colmajor, scaled_err
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2602_10541_b200 import fls
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return fls.Context()
+
+
+def _parity_feats(p):
+    W, b = p.parity_features()
+    return W, b, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda()
+
+
+# ------------------------------------------------------------------------------------- a1
+@pytest.mark.parametrize("dim,F,sigma,seed", [(1, 500, 10.0, 0), (3, 8192, 3.0, 0),
+                                              (5, 4001, 2.0, 7), (2, 1, 5.0, 2**64 - 1)])
+def test_features_match_oracle(ctx, dim, F, sigma, seed):
+    Wd, bd = fls.fls_features(ctx, dim, F, sigma, seed)
+    fls.fls_sync(ctx)
+    Wo, bo = oracle.features(dim, F, sigma, seed)
+    assert np.array_equal(bd.cpu().numpy(), bo)                 # one correctly rounded product
+    Wg = Wd.cpu().numpy()
+    ulp = np.spacing(np.abs(Wo))
+    assert np.all(np.abs(Wg - Wo) <= 8 * ulp + 1e-300), np.max(np.abs(Wg - Wo) / ulp)
+    Wd2, bd2 = fls.fls_features(ctx, dim, F, sigma, seed)
+    assert torch.equal(Wd, Wd2) and torch.equal(bd, bd2)
+
+
+# ------------------------------------------------------------------------------------- a2-a8
+@pytest.mark.parametrize("name", wl.CONFIG_NAMES)
+def test_assemble_parity_mini(ctx, name):
+    p = wl.make_problem(name, "mini")
+    W, b, Wd, bd = _parity_feats(p)
+    F = p.n_features
+    Ab, lda = fls.fls_assemble(ctx, Wd, bd, dev_blocks(p))
+    fls.fls_sync(ctx)
+    Ao, ro, S = oracle.assemble(W, b, p.blocks)
+    Ag, rg = rows_from_colmajor(Ab, lda, F, np.arange(p.n_rows))
+    emax, e999 = scaled_err(Ag, Ao, S)
+    assert emax <= ENTRY_TOL, (emax, e999)
+    assert np.array_equal(rg, ro)
+
+
+@pytest.mark.parametrize("name", ["c3_poisson5d", "c4_heat2d", "c5_biharm3d"])
+def test_assemble_parity_full_size_sampled_rows(ctx, name):
+    """BASELINE.json full sizes in the bench's launch configuration, oracle on sampled rows."""
+    p = wl.make_problem(name, "full")
+    F, R = p.n_features, p.n_rows
+    need = (F + 1) * wl_round4(R) * 8
+    free, _ = torch.cuda.mem_get_info()
+    if need + (2 << 30) > free:
+        pytest.skip(f"needs {need / 1e9:.1f} GB, {free / 1e9:.1f} GB free")
+    W, b, Wd, bd = _parity_feats(p)
+    Ab, lda = fls.fls_assemble(ctx, Wd, bd, dev_blocks(p))
+    fls.fls_sync(ctx)
+    rows = wl.sample_rows(R, 8, 256 if R > 100_000 else 61)
+    Ag, rg = rows_from_colmajor(Ab, lda, F, rows)
+    del Ab
+    torch.cuda.empty_cache()
+    Ao, ro, S = oracle.assemble(W, b, p.blocks, rows=rows)
+    emax, e999 = scaled_err(Ag, Ao, S)
+    assert emax <= ENTRY_TOL, (emax, e999)
+    assert np.array_equal(rg, ro)
+
+
+def wl_round4(n):
+    return ((n + 3) // 4) * 4
+
+
+# ------------------------------------------------------------------------------------- layouts, shards
+def test_row_major_and_shards_bit_identical(ctx):
+    p = wl.make_problem("c4_heat2d", "mini")
+    _, _, Wd, bd = _parity_feats(p)
+    F, R = p.n_features, p.n_rows
+    blocks = fls.BlockSet(dev_blocks(p), 3)
+    Ab, lda = fls.fls_assemble(ctx, Wd, bd, blocks)
+    full = Ab[: (F + 1) * lda].view(F + 1, lda)[:, :R].T.contiguous()   # (R, F+1)
+    Arm, rrm = fls.fls_assemble(ctx, Wd, bd, blocks, layout=fls.FLS_ROW_MAJOR)
+    assert torch.equal(Arm[:, :F], full[:, :F]) and torch.equal(rrm, full[:, F])
+    for P in (2, 3, 8):
+        for r in range(P):
+            a, e = wl.shard_range(R, r, P)
+            Ash, ldl = fls.fls_assemble(ctx, Wd, bd, blocks, row_begin=a, row_end=e)
+            sh = Ash[: (F + 1) * ldl].view(F + 1, ldl)[:, : e - a].T
+            assert torch.equal(sh, full[a:e]), (P, r)
+    fls.fls_sync(ctx)
+
+
+def test_unaligned_lda_and_pointer_scalar_path(ctx):
+    p = wl.make_problem("c2_poisson2d", "mini")
+    _, _, Wd, bd = _parity_feats(p)
+    F, R = p.n_features, p.n_rows
+    blocks = fls.BlockSet(dev_blocks(p), 2)
+    Ab, lda = fls.fls_assemble(ctx, Wd, bd, blocks)
+    ref = Ab[: (F + 1) * lda].view(F + 1, lda)[:, :R]
+    lda2 = R + 1                                    # odd lda -> scalar stores
+    buf = torch.full(((F + 1) * lda2 + 1,), float("nan"), dtype=torch.float64, device="cuda")
+    A2 = buf[1:]                                    # 8-byte (not 16-byte) aligned
+    fls.fls_assemble(ctx, Wd, bd, blocks, A=A2, lda=lda2)
+    got = A2[: (F + 1) * lda2].view(F + 1, lda2)[:, :R]
+    assert torch.equal(got, ref)
+    assert torch.isnan(A2[lda2 - 1])                # padding row untouched
+
+
+def test_empty_and_ragged_blocks(ctx):
+    d, F = 3, 131
+    g = np.random.default_rng(0)
+    W = g.normal(0, 2, (F, d))
+    b = g.uniform(0, 2 * math.pi, F)
+    X1 = g.random((3, d))
+    X2 = g.random((1025, d))
+    Wd, bd = torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda()
+
+    class B:
+        def __init__(s, X, terms, w):
+            s.X, s.terms, s.weight, s.values, s.fields = X, terms, w, np.ones(len(X)), None
+    lap = wl.op_laplacian(d, -1.0)
+    host = [B(np.zeros((0, d)), lap, 1.0), B(X1, lap, 1.0), B(X2, wl.op_identity(d), 7.0)]
+    dev = [fls.Block(torch.from_numpy(np.ascontiguousarray(h.X)).cuda(), h.terms, h.weight,
+                     torch.from_numpy(h.values).cuda()) for h in host]
+    Ab, lda = fls.fls_assemble(ctx, Wd, bd, dev)
+    fls.fls_sync(ctx)
+    Ao, ro, S = oracle.assemble(W, b, host)
+    Ag, rg = rows_from_colmajor(Ab, lda, F, np.arange(1028))
+    assert scaled_err(Ag, Ao, S)[0] <= ENTRY_TOL and np.array_equal(rg, ro)
+    # empty range is a no-op
+    fls.fls_assemble(ctx, Wd, bd, dev, row_begin=5, row_end=5)
+
+
+# ------------------------------------------------------------------------------------- operator modes
+def _mode_case(ctx, terms, fields=None, d=3, F=203, n=777, seed=3):
+    g = np.random.default_rng(seed)
+    W = g.normal(0, 2.5, (F, d))
+    b = g.uniform(0, 2 * math.pi, F)
+    X = g.random((n, d))
+
+    class B:
+        pass
+    h = B()
+    h.X, h.terms, h.weight, h.values, h.fields = X, terms, 3.0, g.normal(size=n), fields
+    dv = fls.Block(torch.from_numpy(X).cuda(), terms, 3.0, torch.from_numpy(h.values).cuda(),
+                   torch.from_numpy(fields).cuda() if fields is not None else None)
+    Ab, lda = fls.fls_assemble(ctx, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(), [dv])
+    fls.fls_sync(ctx)
+    Ao, ro, S = oracle.assemble(W, b, [h])
+    Ag, rg = rows_from_colmajor(Ab, lda, F, np.arange(n))
+    emax, _ = scaled_err(Ag, Ao, S)
+    assert emax <= ENTRY_TOL, emax
+    assert np.array_equal(rg, ro)
+
+
+def test_mode_cos_only_shift(ctx):
+    _mode_case(ctx, wl.op_advection([0.5, -1.0, 2.0]))               # all odd orders
+
+
+def test_mode_fold_mixed_constant(ctx):
+    _mode_case(ctx, wl.op_partial(3, 2, 1) + wl.op_laplacian(3, -0.1, [0, 1])
+               + [((1, 1, 1), 0.3, -1), ((0, 0, 0), 5.0, -1)])
+
+
+def test_mode_sincos_with_fields(ctx):
+    g = np.random.default_rng(1)
+    fields = np.ascontiguousarray(g.normal(size=(777, 3)))
+    terms = (wl.op_laplacian(3, 1.0) + [((1, 0, 0), 2.0, 0), ((0, 0, 0), -1.0, 2),
+                                        ((0, 3, 0), 0.5, 1)])
+    _mode_case(ctx, terms, fields)
+
+
+def test_mode_sin_two_fields_high_order(ctx):
+    g = np.random.default_rng(2)
+    fields = np.ascontiguousarray(g.normal(size=(777, 2)))
+    terms = wl.op_biharmonic(3) + [((0, 0, 0), 16.0, 0), ((2, 0, 0), 1.5, 1), ((0, 0, 6), 1e-3, -1)]
+    _mode_case(ctx, terms, fields)
+
+
+@pytest.mark.parametrize("d", [1, 2, 4, 6, 8])
+def test_all_dims(ctx, d):
+    _mode_case(ctx, wl.op_laplacian(d, -1.0) + wl.op_identity(d, 2.0), d=d, F=150, n=300, seed=d)
+
+
+# ------------------------------------------------------------------------------------- errors
+def test_error_paths(ctx):
+    from paper_2602_10541_b200._abi import FlsError
+    p = wl.make_problem("c1_poisson1d", "mini")
+    _, _, Wd, bd = _parity_feats(p)
+    blocks = dev_blocks(p)
+    with pytest.raises(FlsError, match="EINVAL"):
+        fls.fls_assemble(ctx, Wd, bd, blocks, row_begin=0, row_end=p.n_rows + 1)
+    with pytest.raises(FlsError, match="EINVAL"):
+        fls.fls_assemble(ctx, Wd, bd, blocks, lda=10)
+    bad = [fls.Block(blocks[0].X, [((1, 1), 1.0, -1)], 1.0, blocks[0].values)]
+    with pytest.raises(FlsError, match="EINVAL"):                      # alpha beyond dim
+        fls.fls_assemble(ctx, Wd, bd, bad)
+    bad = [fls.Block(blocks[0].X, [((0,), 1.0, 0)], 1.0, blocks[0].values)]
+    with pytest.raises(FlsError, match="EINVAL"):                      # field without fields
+        fls.fls_assemble(ctx, Wd, bd, bad)
+    with pytest.raises(FlsError, match="EINVAL"):
+        fls.fls_features(ctx, 0, 10, 1.0, 0)
+    with pytest.raises(FlsError, match="EINVAL"):
+        fls.fls_features(ctx, 2, 10, -1.0, 0)
+    # non-finite input is reported asynchronously at the next sync
+    Xn = blocks[0].X.clone()
+    Xn[5, 0] = float("nan")
+    nb = [fls.Block(Xn, blocks[0].terms, 1.0, blocks[0].values)]
+    fls.fls_assemble(ctx, Wd, bd, nb)
+    with pytest.raises(FlsError, match="ENONFINITE"):
+        fls.fls_sync(ctx)
+    fls.fls_sync(ctx)                                                  # flag cleared
+    # rank deficiency: a zero column without ridge
+    M = torch.zeros((3 * 8,), dtype=torch.float64, device="cuda")
+    M.view(3, 8)[0, :] = 1.0
+    M.view(3, 8)[2, :] = 1.0
+    with pytest.raises(FlsError, match="ERANK"):
+        fls.fls_solve(ctx, M, 8, 8, 2)
+
+
+# ------------------------------------------------------------------------------------- solve + eval
+@pytest.mark.parametrize("name,size", [("c1_poisson1d", "full"), ("c2_poisson2d", "full"),
+                                       ("c3_poisson5d", "mini"), ("c4_heat2d", "mini"),
+                                       ("c5_biharm3d", "mini")])
+def test_solve_and_eval_parity(ctx, name, size):
+    p = wl.make_problem(name, size)
+    W, b, Wd, bd = _parity_feats(p)
+    F, R = p.n_features, p.n_rows
+    ridge = p.ridge_rel > 0
+    Ab, lda = fls.fls_assemble(ctx, Wd, bd, dev_blocks(p), extra_rows=F if ridge else 0)
+    sq = 0.0
+    if ridge:
+        sq = p.ridge_rel * math.sqrt(fls.fls_frob2(ctx, Ab, R, lda, F))
+    beta, res = fls.fls_solve(ctx, Ab, R, lda, F, sq)
+    Xt = p.test_points(10_000)
+    u_gpu = fls.fls_eval(ctx, Wd, bd, beta, torch.from_numpy(Xt).cuda()).cpu().numpy()
+    # oracle chain
+    Ao, ro, _ = oracle.assemble(W, b, p.blocks, want_scale=False)
+    beta_o, res_o, _ = oracle.lstsq(Ao, ro, ridge_rel=p.ridge_rel)
+    u_orc = oracle.evaluate(W, b, beta_o, Xt)
+    rel = np.linalg.norm(u_gpu - u_orc) / np.linalg.norm(u_orc)
+    assert rel <= U_TOL, rel
+    # eval parity alone (same beta on both sides)
+    u_gpu2 = fls.fls_eval(ctx, Wd, bd, torch.from_numpy(beta_o).cuda(),
+                          torch.from_numpy(Xt).cuda()).cpu().numpy()
+    scale = np.abs(beta_o).sum() / math.sqrt(F)
+    assert np.abs(u_gpu2 - u_orc).max() <= 1e-12 * max(scale, 1.0)
+
+
+def test_eval_with_operator_matches_assembled_rows(ctx):
+    p = wl.make_problem("c4_heat2d", "mini")
+    W, b, Wd, bd = _parity_feats(p)
+    F = p.n_features
+    beta = torch.from_numpy(np.random.default_rng(0).normal(size=F)).cuda()
+    X = torch.from_numpy(p.test_points(999)).cuda()
+    terms = p.blocks[0].terms
+    Lu = fls.fls_eval(ctx, Wd, bd, beta, X, terms=terms).cpu().numpy()
+
+    class B:
+        pass
+    h = B()
+    h.X, h.terms, h.weight, h.values, h.fields = X.cpu().numpy(), terms, 1.0, None, None
+    Ao, _, S = oracle.assemble(W, b, [h])
+    ref = Ao @ beta.cpu().numpy()
+    assert np.abs(Lu - ref).max() <= 1e-12 * (S @ np.abs(beta.cpu().numpy())).max()
