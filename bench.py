@@ -161,6 +161,8 @@ def main():
     ap.add_argument("--workload", default="c5_biharm3d")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
     ap.add_argument("--ref-rows", type=int, default=64)
+    ap.add_argument("--rows", type=int, default=None,
+                    help="override the interior row count (profiling a reduced copy of the workload)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -177,7 +179,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    p = wl.make_problem(args.workload, "full")
+    p = wl.make_problem(args.workload, "full", **({"n_int": args.rows} if args.rows else {}))
     F, R, d = p.n_features, p.n_rows, p.dim
     a, e = wl.shard_range(R, rank, world)
     n_local = e - a

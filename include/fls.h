@@ -175,6 +175,23 @@ FLS_API fls_status fls_assemble(fls_ctx *ctx, const double *W, const double *b, 
                         int64_t lda, int32_t layout, double *rhs);
 
 /* ---------------------------------------------------------------------------------------- */
+/* fls_assemble with HOST buffers (the end-to-end path of a caller whose data lives in host  */
+/* memory).  Same arguments and semantics as fls_assemble with FLS_COL_MAJOR, except that    */
+/* W, b, every block's X / coef_fields / values, A and rhs are HOST pointers (pinned memory   */
+/* gives full PCIe bandwidth; pageable works, slower).  The call copies W, b and the points   */
+/* of [row_begin, row_end) to ctx-owned device staging, assembles in row chunks of at most    */
+/* chunk_rows rows (0 = about 2 GiB per chunk) into two device buffers, and copies each chunk */
+/* into A / rhs (cudaMemcpy2DAsync on a second stream) while the next chunk computes.        */
+/* Blocking: on return A and rhs hold the result.  The ctx keeps the staging for reuse.       */
+/*   Errors: as fls_assemble; FLS_ENOMEM if the staging does not fit.                        */
+/* ---------------------------------------------------------------------------------------- */
+FLS_API fls_status fls_assemble_host(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
+                                     int64_t n_features, int32_t normalize,
+                                     const fls_block *blocks, int32_t n_blocks,
+                                     int64_t row_begin, int64_t row_end, double *A, int64_t lda,
+                                     double *rhs, int64_t chunk_rows);
+
+/* ---------------------------------------------------------------------------------------- */
 /* Alg. 1 line 5 ("beta* = argmin ||A beta - b||^2 via QR"), with the optional       */
 /* Tikhonov term of P:L156-160:  beta = argmin ||A beta - b||^2 + mu ||beta||^2.             */
 /* Householder QR (cuSOLVER geqrf) of the column-major [A | b] (n_rows x (n_features + 1),   */

@@ -60,6 +60,9 @@ _SIGS = {
     "fls_assemble": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int32,
                                C.POINTER(fls_block), C.c_int32, C.c_int64, C.c_int64, C.c_void_p,
                                C.c_int64, C.c_int32, C.c_void_p]),
+    "fls_assemble_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64,
+                                    C.c_int32, C.POINTER(fls_block), C.c_int32, C.c_int64,
+                                    C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]),
     "fls_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_double,
                             C.c_void_p, C.POINTER(C.c_double)]),
     "fls_qr_r": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,

@@ -72,9 +72,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+MB_SRC = os.path.join(CSRC, "bench", "microbench.cu")
+MB_LIB = os.path.join(HERE, "libfls_microbench.so")
+
+
+def build_microbench(force: bool = False) -> str:
+    """roofline probes (not part of the product ABI)"""
+    deps = [MB_SRC, os.path.join(CSRC, "fls_device.cuh")]
+    if not force and os.path.exists(MB_LIB) and all(os.path.getmtime(d) <= os.path.getmtime(MB_LIB) for d in deps):
+        return MB_LIB
+    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", MB_LIB, MB_SRC]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for microbench:\n{r.stderr}")
+    return MB_LIB
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     a = ap.parse_args()
     print(build(a.force, a.verbose))
+    print(build_microbench(a.force))

@@ -1,0 +1,270 @@
+// microbench.cu -- roofline denominators for the assembly path, built into
+// a separate libfls_microbench.so (not part of the product ABI).
+//
+//   mb_store_bw     store-only HBM bandwidth with the assembly kernel's exact store pattern
+//                   (16-byte st.global.cs, 512 contiguous bytes per warp instruction)
+//   mb_dfma_rate    register-only DFMA throughput (8 independent chains per thread)
+//   mb_entry_rate   register-only throughput of the assembly kernel's per-entry arithmetic
+//                   (d = 3 phase, half-turn reduction, degree-13 sin, one coefficient field)
+//                   = the FP64-pipe ceiling of the C5 kernel with no memory traffic at all
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../fls_device.cuh"
+
+using namespace fls;
+
+extern "C" {
+
+__global__ void __launch_bounds__(256) store_kernel(double *A, int64_t n2, double v) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double2 *p = reinterpret_cast<double2 *>(A);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += stride)
+    __stcs(p + i, make_double2(v, v + 1.0));
+}
+
+__global__ void __launch_bounds__(256) dfma_kernel(double *out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.678) out[threadIdx.x] = s;  // never true; keeps the chains alive
+}
+
+// per thread: 4 rows in registers (as the assembly kernel), loop over `nfeat` synthetic
+// features; accumulate instead of storing
+__global__ void __launch_bounds__(256) entry_kernel(double *out, int nfeat, double w0, double w1,
+                                                    double w2) {
+  const double x[4][3] = {{0.1 + threadIdx.x * 1e-4, 0.2, 0.3}, {0.4, 0.5 + blockIdx.x * 1e-6, 0.6},
+                          {0.7, 0.8, 0.9}, {0.15, 0.25, 0.35}};
+  const double c[4] = {1.1, 1.2, 1.3, 1.4};
+  double acc[4] = {0, 0, 0, 0};
+  double wa = w0, wb = w1, wc = w2, bp = 0.1, P0 = 2.0, P1 = 3.0;
+  for (int j = 0; j < nfeat; ++j) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double h = fma(wc, x[q][2], fma(wb, x[q][1], fma(wa, x[q][0], bp)));
+      int sgn;
+      const double f = halfturn(h, sgn);
+      const double P = fma(c[q], P1, P0);
+      acc[q] += P * sinpi_core(flipsign(f, sgn), f * f);
+    }
+    wa += 1e-3;  // integer-free per-feature change (models the smem record load)
+    bp += 2e-3;
+  }
+  const double s = acc[0] + acc[1] + acc[2] + acc[3];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+// the assembly kernel's exact tile/store pattern with no arithmetic: 1024-row x 128-column
+// tiles, 4 rows per thread as two 16-byte pairs, one column per iteration
+__global__ void __launch_bounds__(256) tile_store_kernel(double *A, int64_t lda, int ncols, double v) {
+  double *colp = A + (int64_t)blockIdx.y * 128 * lda + (int64_t)blockIdx.x * 1024 + 2 * threadIdx.x;
+  const int nc = min(128, ncols - (int)blockIdx.y * 128);
+  for (int j = 0; j < nc; ++j, colp += lda) {
+    __stcs(reinterpret_cast<double2 *>(colp), make_double2(v, v + j));
+    __stcs(reinterpret_cast<double2 *>(colp + 512), make_double2(v + 1.0, v - j));
+  }
+}
+
+// contiguous streaming: each CTA writes one contiguous 256 KiB chunk
+__global__ void __launch_bounds__(256) chunk_store_kernel(double *A, double v) {
+  double2 *p = reinterpret_cast<double2 *>(A) + (int64_t)blockIdx.x * 16384 + threadIdx.x;
+#pragma unroll 4
+  for (int k = 0; k < 64; ++k) __stcs(p + k * 256, make_double2(v, v + k));
+}
+
+static float time_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+// returns 0 on success; *gbs = bytes / s / 1e9 over `reps` launches (after one warm-up)
+__attribute__((visibility("default"))) int mb_store_bw(double *A, int64_t n_doubles, int reps,
+                                                       double *gbs) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = sms * 8;
+  store_kernel<<<grid, 256>>>(A, n_doubles / 2, 1.0);
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) store_kernel<<<grid, 256>>>(A, n_doubles / 2, 1.0 + r);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  *gbs = (double)n_doubles * 8.0 * reps / (time_ms(e0, e1) / 1e3) / 1e9;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return (int)cudaGetLastError();
+}
+
+__attribute__((visibility("default"))) int mb_dfma_rate(double *scratch, int iters, double *dfma_per_s) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = sms * 8;
+  dfma_kernel<<<grid, 256>>>(scratch, 1000, 0.999, 1e-3);
+  cudaEventRecord(e0);
+  dfma_kernel<<<grid, 256>>>(scratch, iters, 0.999, 1e-3);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  *dfma_per_s = (double)grid * 256 * iters * 8 / (time_ms(e0, e1) / 1e3);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return (int)cudaGetLastError();
+}
+
+__attribute__((visibility("default"))) int mb_entry_rate(double *scratch, int nfeat, double *entries_per_s) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = sms * 8;
+  entry_kernel<<<grid, 256>>>(scratch, 100, 1.0, 2.0, 3.0);
+  cudaEventRecord(e0);
+  entry_kernel<<<grid, 256>>>(scratch, nfeat, 1.0, 2.0, 3.0);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  *entries_per_s = (double)grid * 256 * 4 * nfeat / (time_ms(e0, e1) / 1e3);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return (int)cudaGetLastError();
+}
+
+// rows must be a multiple of 1024, cols of 128; A holds cols * lda doubles
+__attribute__((visibility("default"))) int mb_tile_store_bw(double *A, int64_t rows, int64_t lda,
+                                                            int cols, int reps, double *gbs) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  dim3 grid((unsigned)(rows / 1024), (unsigned)((cols + 127) / 128));
+  tile_store_kernel<<<grid, 256>>>(A, lda, cols, 1.0);
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) tile_store_kernel<<<grid, 256>>>(A, lda, cols, 2.0 + r);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  *gbs = (double)rows * cols * 8.0 * reps / (time_ms(e0, e1) / 1e3) / 1e9;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return (int)cudaGetLastError();
+}
+
+// n_doubles must be a multiple of 32768
+__attribute__((visibility("default"))) int mb_chunk_store_bw(double *A, int64_t n_doubles, int reps,
+                                                             double *gbs) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const unsigned grid = (unsigned)(n_doubles / 32768);
+  chunk_store_kernel<<<grid, 256>>>(A, 1.0);
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) chunk_store_kernel<<<grid, 256>>>(A, 2.0 + r);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  *gbs = (double)n_doubles * 8.0 * reps / (time_ms(e0, e1) / 1e3) / 1e9;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return (int)cudaGetLastError();
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// per-op FP64 throughput: 8 independent chains per thread of one op kind
+template <int OP>
+__global__ void __launch_bounds__(256) op_kernel(double *out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k + 0.25;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (OP == 0) x[k] = __dadd_rn(x[k], a);
+      if (OP == 1) x[k] = __dmul_rn(x[k], a);
+      if (OP == 2) x[k] = fma(x[k], a, b);
+      if (OP == 3) x[k] = rint(x[k]) + a;          // FRND + DADD
+      if (OP == 4) x[k] = (double)(__double2int_rn(x[k]) + 1);   // F2I + I2F
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+// entry kernel variant: rint (FRND) + integer parity instead of the magic-constant rounding
+__device__ __forceinline__ double halfturn_frnd(double h, int &sgn) {
+  const double n = rint(h);
+  // parity of n from the integer bits of n (n exact, |n| < 2^31): low bit of the converted int
+  // computed on the integer pipe from the mantissa
+  const int hi = __double2hiint(n), lo = __double2loint(n);
+  const int e = ((hi >> 20) & 0x7ff) - 1023;          // n = 1.m * 2^e, e in [0, 30] when n != 0
+  // units bit of n sits at mantissa bit (52 - e): in lo for e >= 21, in hi for e < 21
+  const int bit = (e < 0) ? 0 : (e == 0 ? 1 : (e <= 20 ? (hi >> (20 - e)) & 1 : (lo >> (52 - e)) & 1));
+  sgn = bit << 31;
+  return __dsub_rn(h, n);
+}
+
+__global__ void __launch_bounds__(256) entry2_kernel(double *out, int nfeat, double w0, double w1,
+                                                     double w2) {
+  const double x[4][3] = {{0.1 + threadIdx.x * 1e-4, 0.2, 0.3}, {0.4, 0.5 + blockIdx.x * 1e-6, 0.6},
+                          {0.7, 0.8, 0.9}, {0.15, 0.25, 0.35}};
+  const double c[4] = {1.1, 1.2, 1.3, 1.4};
+  double acc[4] = {0, 0, 0, 0};
+  double wa = w0, wb = w1, wc = w2, bp = 0.1, P0 = 2.0, P1 = 3.0;
+  for (int j = 0; j < nfeat; ++j) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double h = fma(wc, x[q][2], fma(wb, x[q][1], fma(wa, x[q][0], bp)));
+      int sgn;
+      const double f = halfturn_frnd(h, sgn);
+      const double P = fma(c[q], P1, P0);
+      acc[q] += P * sinpi_core(flipsign(f, sgn), f * f);
+    }
+    wa += 1e-3;
+    bp += 2e-3;
+  }
+  const double s = acc[0] + acc[1] + acc[2] + acc[3];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+extern "C" __attribute__((visibility("default"))) int mb_op_rate(int op, double *scratch, int iters,
+                                                                 double *ops_per_s) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = sms * 8;
+  auto go = [&](int it) {
+    switch (op) {
+      case 0: op_kernel<0><<<grid, 256>>>(scratch, it, 1e-9, 1e-3); break;
+      case 1: op_kernel<1><<<grid, 256>>>(scratch, it, 0.9999999, 1e-3); break;
+      case 2: op_kernel<2><<<grid, 256>>>(scratch, it, 0.9999999, 1e-3); break;
+      case 3: op_kernel<3><<<grid, 256>>>(scratch, it, 0.25, 1e-3); break;
+      case 4: op_kernel<4><<<grid, 256>>>(scratch, it, 0.25, 1e-3); break;
+      case 5: entry2_kernel<<<grid, 256>>>(scratch, it, 1.0, 2.0, 3.0); break;
+    }
+  };
+  go(100);
+  cudaEventRecord(e0);
+  go(iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  const double per = (op == 5) ? 4.0 : 8.0;
+  *ops_per_s = (double)grid * 256 * iters * per / (time_ms(e0, e1) / 1e3);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return (int)cudaGetLastError();
+}

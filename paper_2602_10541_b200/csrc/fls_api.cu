@@ -30,6 +30,11 @@ struct fls_ctx {
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // pairs (start, stop)
   size_t ev_used = 0;
+  // host-buffer path (fls_assemble_host): copy stream, events, device staging
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t hev[4] = {nullptr, nullptr, nullptr, nullptr};
+  double *hin = nullptr, *hout = nullptr;
+  size_t hin_bytes = 0, hout_bytes = 0;
 };
 
 namespace {
@@ -199,6 +204,14 @@ fls_status fls_ctx_destroy(fls_ctx *ctx) {
   if (ctx->solver) cusolverDnDestroy(ctx->solver);
   if (ctx->blas) cublasDestroy(ctx->blas);
   for (cudaEvent_t ev : ctx->ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : ctx->hev)
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+  }
+  cudaFree(ctx->hin);
+  cudaFree(ctx->hout);
   cudaFree(ctx->ws);
   cudaFree(ctx->d_err);
   cudaFree(ctx->d_scratch);
@@ -267,21 +280,31 @@ fls_status fls_features(fls_ctx *ctx, int32_t dim, int64_t n_features, double si
   return FLS_OK;
 }
 
+}  // extern "C"
+
 // ---------------------------------------------------------------------------------------------
-fls_status fls_assemble(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
-                        int64_t n_features, int32_t normalize, const fls_block *blocks,
-                        int32_t n_blocks, int64_t row_begin, int64_t row_end, double *A,
-                        int64_t lda, int32_t layout, double *rhs) {
-  if (fls_status s = check_ctx(ctx)) return s;
+// assembly: validation shared by the device and host entry points
+namespace {
+
+struct AsmPlan {
+  int32_t n_blocks = 0;
+  int64_t total = 0;
+  OpPlan plans[64];
+};
+
+fls_status validate_assemble(int32_t dim, int64_t n_features, const double *W, const double *b,
+                             const fls_block *blocks, int32_t n_blocks, int64_t row_begin,
+                             int64_t row_end, const double *A, int64_t lda, int32_t layout,
+                             AsmPlan &ap) {
   if (dim < 1 || dim > FLS_MAX_DIM) return fail(FLS_EINVAL, "dim %d not in 1..%d", dim, FLS_MAX_DIM);
   if (n_features < 1) return fail(FLS_EINVAL, "n_features %lld < 1", (long long)n_features);
   if (!W || !b) return fail(FLS_EINVAL, "W or b is NULL");
   if (!blocks || n_blocks < 1) return fail(FLS_EINVAL, "need n_blocks >= 1 block descriptors");
+  if (n_blocks > 64) return fail(FLS_EUNSUPPORTED, "more than 64 blocks");
   if (layout != FLS_COL_MAJOR && layout != FLS_ROW_MAJOR)
     return fail(FLS_EINVAL, "layout %d unknown", layout);
-  int64_t total = 0;
-  static thread_local OpPlan plans[64];
-  if (n_blocks > 64) return fail(FLS_EUNSUPPORTED, "more than 64 blocks");
+  ap.n_blocks = n_blocks;
+  ap.total = 0;
   for (int q = 0; q < n_blocks; ++q) {
     const fls_block &B = blocks[q];
     if (B.n_points < 0) return fail(FLS_EINVAL, "block %d: n_points < 0", q);
@@ -293,12 +316,12 @@ fls_status fls_assemble(fls_ctx *ctx, const double *W, const double *b, int32_t 
     if (!std::isfinite(B.weight)) return fail(FLS_EINVAL, "block %d: weight not finite", q);
     char what[32];
     snprintf(what, sizeof what, "block %d", q);
-    if (fls_status s = plan_operator(B.op, dim, B.n_fields, true, plans[q], what)) return s;
-    total += B.n_points;
+    if (fls_status s = plan_operator(B.op, dim, B.n_fields, true, ap.plans[q], what)) return s;
+    ap.total += B.n_points;
   }
-  if (row_begin < 0 || row_end < row_begin || row_end > total)
+  if (row_begin < 0 || row_end < row_begin || row_end > ap.total)
     return fail(FLS_EINVAL, "row range [%lld, %lld) not within [0, %lld]", (long long)row_begin,
-                (long long)row_end, (long long)total);
+                (long long)row_end, (long long)ap.total);
   const int64_t n_local = row_end - row_begin;
   if (n_local == 0) return FLS_OK;
   if (!A) return fail(FLS_EINVAL, "A is NULL");
@@ -306,47 +329,69 @@ fls_status fls_assemble(fls_ctx *ctx, const double *W, const double *b, int32_t 
     return fail(FLS_EINVAL, "lda %lld < local rows %lld", (long long)lda, (long long)n_local);
   if (layout == FLS_ROW_MAJOR && lda < n_features)
     return fail(FLS_EINVAL, "lda %lld < n_features %lld", (long long)lda, (long long)n_features);
+  return FLS_OK;
+}
 
-  DeviceGuard g(ctx->device);
-  // per-block prefactor records: stride S doubles per feature, block q at offset q * F * Smax
-  const int Smax = pf_stride(FLS_MAX_DIM, FLS_MAX_FIELDS, KM_SINCOS);
-  if (fls_status s = ensure_ws(ctx, (size_t)n_blocks * n_features * Smax * sizeof(double))) return s;
-  const double s_norm = normalize ? 1.0 / std::sqrt((double)n_features) : 1.0;
-  const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0);
+constexpr int kSmax = pf_stride(FLS_MAX_DIM, FLS_MAX_FIELDS, KM_SINCOS);
 
-  int64_t g0 = 0;  // first global row of block q
-  for (int q = 0; q < n_blocks; ++q) {
+// a2: one prefactor launch per block that has rows in [row_begin, row_end)
+fls_status launch_prefactors(fls_ctx *ctx, const AsmPlan &ap, const double *W, const double *b,
+                             int32_t dim, int64_t F, int32_t normalize, const fls_block *blocks,
+                             int64_t row_begin, int64_t row_end, cudaStream_t st) {
+  if (fls_status s = ensure_ws(ctx, (size_t)ap.n_blocks * F * kSmax * sizeof(double))) return s;
+  const double s_norm = normalize ? 1.0 / std::sqrt((double)F) : 1.0;
+  int64_t g0 = 0;
+  for (int q = 0; q < ap.n_blocks; ++q) {
     const fls_block &B = blocks[q];
     const int64_t lo = std::max(g0, row_begin), hi = std::min(g0 + B.n_points, row_end);
     g0 += B.n_points;
     if (hi <= lo) continue;
-    const OpPlan &pl = plans[q];
+    const OpPlan &pl = ap.plans[q];
     PrefArgs pa;
     std::memset(&pa, 0, sizeof pa);
     pa.W = W;
     pa.b = b;
-    pa.F = n_features;
+    pa.F = F;
     pa.D = dim;
     pa.n_terms = pl.n_terms;
     pa.G = pl.G;
     pa.pmode = pl.pmode;
     pa.S = pf_stride(dim, pl.G, pl.kmode);
     pa.scale = s_norm * B.weight;
-    pa.pf = ctx->ws + (size_t)q * n_features * Smax;
+    pa.pf = ctx->ws + (size_t)q * F * kSmax;
     pa.err = ctx->d_err;
     std::memcpy(pa.terms, pl.terms, sizeof pl.terms);
-    cudaError_t e = launch_prefactor(pa, ctx->stream);
+    cudaError_t e = launch_prefactor(pa, st);
     if (e != cudaSuccess) return cuda_fail(e, "prefactor_kernel");
+  }
+  return FLS_OK;
+}
 
+// a3-a8: assembly launches for global rows [row_begin, row_end) into local rows of A / rhs.
+// blocks[q]'s X / fields / values pointers refer to point index pt_base[q] (0 for the caller's
+// own arrays; the slice start for staged copies).
+fls_status assemble_range(fls_ctx *ctx, const AsmPlan &ap, int32_t dim, int64_t F,
+                          const fls_block *blocks, const int64_t *pt_base, int64_t row_begin,
+                          int64_t row_end, double *A, int64_t lda, int32_t layout, double *rhs,
+                          cudaStream_t st) {
+  const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0);
+  int64_t g0 = 0;  // first global row of block q
+  for (int q = 0; q < ap.n_blocks; ++q) {
+    const fls_block &B = blocks[q];
+    const int64_t lo = std::max(g0, row_begin), hi = std::min(g0 + B.n_points, row_end);
+    const int64_t blk_start = g0;
+    g0 += B.n_points;
+    if (hi <= lo) continue;
+    const OpPlan &pl = ap.plans[q];
     AsmArgs aa;
     std::memset(&aa, 0, sizeof aa);
-    aa.pf = pa.pf;
-    aa.F = n_features;
+    aa.pf = ctx->ws + (size_t)q * F * kSmax;
+    aa.F = F;
     aa.X = B.X;
     aa.fields = B.coef_fields;
     aa.values = B.values;
     aa.weight = B.weight;
-    aa.pt0 = lo - (g0 - B.n_points);
+    aa.pt0 = (lo - blk_start) - (pt_base ? pt_base[q] : 0);
     aa.lr0 = lo - row_begin;
     aa.lr1 = hi - row_begin;
     aa.A = A;
@@ -367,15 +412,153 @@ fls_status fls_assemble(fls_ctx *ctx, const double *W, const double *b, int32_t 
       }
       e0 = ctx->ev[ctx->ev_used++];
       e1 = ctx->ev[ctx->ev_used++];
-      FLS_CUDA(cudaEventRecord(e0, ctx->stream));
+      FLS_CUDA(cudaEventRecord(e0, st));
     }
-    e = (layout == FLS_COL_MAJOR) ? launch_assemble_cm(dim, pl.G, pl.kmode, aa, ctx->stream)
-                                  : launch_assemble_rm(dim, pl.G, pl.kmode, aa, ctx->stream);
+    cudaError_t e = (layout == FLS_COL_MAJOR) ? launch_assemble_cm(dim, pl.G, pl.kmode, aa, st)
+                                              : launch_assemble_rm(dim, pl.G, pl.kmode, aa, st);
     if (e != cudaSuccess) return cuda_fail(e, "assemble kernel");
-    if (ctx->timing) FLS_CUDA(cudaEventRecord(e1, ctx->stream));
+    if (ctx->timing) FLS_CUDA(cudaEventRecord(e1, st));
   }
   return FLS_OK;
 }
+
+fls_status ensure_dev(double *&p, size_t &cap, size_t bytes, cudaStream_t st) {
+  if (bytes <= cap) return FLS_OK;
+  if (p) {
+    cudaStreamSynchronize(st);
+    cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FLS_ENOMEM, "staging allocation of %zu bytes failed", bytes);
+  }
+  cap = bytes;
+  return FLS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+fls_status fls_assemble(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
+                        int64_t n_features, int32_t normalize, const fls_block *blocks,
+                        int32_t n_blocks, int64_t row_begin, int64_t row_end, double *A,
+                        int64_t lda, int32_t layout, double *rhs) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  static thread_local AsmPlan ap;
+  if (fls_status s = validate_assemble(dim, n_features, W, b, blocks, n_blocks, row_begin, row_end,
+                                       A, lda, layout, ap))
+    return s;
+  if (row_end == row_begin) return FLS_OK;
+  DeviceGuard g(ctx->device);
+  if (fls_status s = launch_prefactors(ctx, ap, W, b, dim, n_features, normalize, blocks,
+                                       row_begin, row_end, ctx->stream))
+    return s;
+  return assemble_range(ctx, ap, dim, n_features, blocks, nullptr, row_begin, row_end, A, lda,
+                        layout, rhs, ctx->stream);
+}
+
+fls_status fls_assemble_host(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
+                             int64_t n_features, int32_t normalize, const fls_block *blocks,
+                             int32_t n_blocks, int64_t row_begin, int64_t row_end, double *A,
+                             int64_t lda, double *rhs, int64_t chunk_rows) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  static thread_local AsmPlan ap;
+  if (fls_status s = validate_assemble(dim, n_features, W, b, blocks, n_blocks, row_begin, row_end,
+                                       A, lda, FLS_COL_MAJOR, ap))
+    return s;
+  if (row_end == row_begin) return FLS_OK;
+  if (chunk_rows < 0) return fail(FLS_EINVAL, "chunk_rows < 0");
+  const int64_t F = n_features;
+  if (chunk_rows == 0) {  // ~2 GiB per staging buffer
+    chunk_rows = ((int64_t)1 << 31) / (8 * (F + 1));
+    chunk_rows = std::max<int64_t>(1024, chunk_rows / 1024 * 1024);
+  }
+  const int64_t n_local = row_end - row_begin;
+  chunk_rows = std::min(chunk_rows, n_local);
+  const int64_t ldc = (chunk_rows + 3) / 4 * 4;
+  DeviceGuard g(ctx->device);
+  cudaStream_t cs = ctx->stream;
+  if (!ctx->copy_stream) FLS_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  cudaStream_t xs = ctx->copy_stream;
+  for (int k = 0; k < 4; ++k)
+    if (!ctx->hev[k]) FLS_CUDA(cudaEventCreateWithFlags(&ctx->hev[k], cudaEventDisableTiming));
+
+  // 1. stage inputs: W, b and each block's slice of points / fields / values for the range
+  size_t in_doubles = (size_t)F * dim + F;
+  int64_t g0 = 0;
+  int64_t lo_pt[64], n_pt[64];
+  for (int q = 0; q < ap.n_blocks; ++q) {
+    const fls_block &B = blocks[q];
+    const int64_t lo = std::max(g0, row_begin), hi = std::min(g0 + B.n_points, row_end);
+    lo_pt[q] = std::max<int64_t>(0, lo - g0);
+    n_pt[q] = std::max<int64_t>(0, hi - lo);
+    g0 += B.n_points;
+    in_doubles += (size_t)n_pt[q] * (dim + B.n_fields + (B.values ? 1 : 0));
+  }
+  if (fls_status s = ensure_dev(ctx->hin, ctx->hin_bytes, in_doubles * sizeof(double), cs)) return s;
+  if (fls_status s = ensure_dev(ctx->hout, ctx->hout_bytes, 2 * (size_t)ldc * (F + 1) * sizeof(double), cs))
+    return s;
+  double *Wd = ctx->hin, *bd = Wd + F * dim, *cur = bd + F;
+  FLS_CUDA(cudaMemcpyAsync(Wd, W, sizeof(double) * F * dim, cudaMemcpyHostToDevice, cs));
+  FLS_CUDA(cudaMemcpyAsync(bd, b, sizeof(double) * F, cudaMemcpyHostToDevice, cs));
+  fls_block dblk[64];
+  int64_t base[64];
+  for (int q = 0; q < ap.n_blocks; ++q) {
+    const fls_block &B = blocks[q];
+    dblk[q] = B;
+    base[q] = lo_pt[q];
+    if (n_pt[q] == 0) continue;
+    dblk[q].X = cur;
+    FLS_CUDA(cudaMemcpyAsync(cur, B.X + lo_pt[q] * dim, sizeof(double) * n_pt[q] * dim,
+                             cudaMemcpyHostToDevice, cs));
+    cur += n_pt[q] * dim;
+    if (B.n_fields > 0) {
+      dblk[q].coef_fields = cur;
+      FLS_CUDA(cudaMemcpyAsync(cur, B.coef_fields + lo_pt[q] * B.n_fields,
+                               sizeof(double) * n_pt[q] * B.n_fields, cudaMemcpyHostToDevice, cs));
+      cur += n_pt[q] * B.n_fields;
+    }
+    if (B.values) {
+      dblk[q].values = cur;
+      FLS_CUDA(cudaMemcpyAsync(cur, B.values + lo_pt[q], sizeof(double) * n_pt[q],
+                               cudaMemcpyHostToDevice, cs));
+      cur += n_pt[q];
+    }
+  }
+  // 2. prefactors once, then chunks: compute on cs into buffer k%2, copy out on xs
+  if (fls_status s = launch_prefactors(ctx, ap, Wd, bd, dim, F, normalize, dblk, row_begin,
+                                       row_end, cs))
+    return s;
+  const int64_t n_chunks = (n_local + chunk_rows - 1) / chunk_rows;
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    const int slot = (int)(c & 1);
+    double *buf = ctx->hout + (size_t)slot * ldc * (F + 1);
+    const int64_t r0 = row_begin + c * chunk_rows, r1 = std::min(row_end, r0 + chunk_rows);
+    if (c >= 2) FLS_CUDA(cudaStreamWaitEvent(cs, ctx->hev[2 + slot], 0));  // buffer drained
+    if (fls_status s = assemble_range(ctx, ap, dim, F, dblk, base, r0, r1, buf, ldc, FLS_COL_MAJOR,
+                                      rhs ? buf + F * ldc : nullptr, cs))
+      return s;
+    FLS_CUDA(cudaEventRecord(ctx->hev[slot], cs));
+    FLS_CUDA(cudaStreamWaitEvent(xs, ctx->hev[slot], 0));
+    const int64_t nr = r1 - r0, off = r0 - row_begin;
+    FLS_CUDA(cudaMemcpy2DAsync(A + off, sizeof(double) * lda, buf, sizeof(double) * ldc,
+                               sizeof(double) * nr, F, cudaMemcpyDeviceToHost, xs));
+    if (rhs)
+      FLS_CUDA(cudaMemcpyAsync(rhs + off, buf + F * ldc, sizeof(double) * nr,
+                               cudaMemcpyDeviceToHost, xs));
+    FLS_CUDA(cudaEventRecord(ctx->hev[2 + slot], xs));
+  }
+  FLS_CUDA(cudaStreamSynchronize(xs));
+  FLS_CUDA(cudaStreamSynchronize(cs));
+  return FLS_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
 
 // ---------------------------------------------------------------------------------------------
 static fls_status ensure_handles(fls_ctx *ctx) {

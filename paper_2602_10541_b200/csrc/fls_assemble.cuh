@@ -3,16 +3,19 @@
 //   A_ij = sum_g c_g(x_i) (Ps_gj sin z_ij + Pc_gj cos z_ij),   z_ij = W_j . x_i + b_j
 //
 // (Eq. 2 folded per feature by the prefactor kernel; Eq. 3 row blocks).
-// HBM-write-bound (8 B per entry) with the FP64 pipe as co-bound (d + 12 DFMA-class ops per
-// entry in the sin-only family).
+// HBM-write-bound (8 B per entry) with the FP64 pipe as co-bound (d + 12 FP64 ops per entry
+// in the sin-only family, + 1 per coefficient field).
 //
 // Column-major layout A[j * lda + i] (what cuSOLVER geqrf consumes):
-//   CTA = 256 threads, tile = 1024 rows x 128 features.  Thread t owns the row pairs
-//   (2t, 2t+1) and (512 + 2t, 512 + 2t + 1) of the tile -- its x_i stay in registers for the
-//   whole tile -- so every store instruction of a warp writes 64 consecutive rows = 512
-//   contiguous bytes of one column, as one 16-byte st.global.cs per lane (streaming: the
-//   output is never re-read by this kernel).  The tile's 128 per-feature records
-//   [W_j/pi, b'_j/pi, P_j...] sit in shared memory and are read as warp-wide broadcasts.
+//   CTA = 256 threads owning a 1024-row tile.  Thread t keeps the x_i (and coefficient
+//   fields) of 4 rows -- the row pairs (2t, 2t+1) and (512 + 2t, 512 + 2t + 1) -- in
+//   registers while the CTA walks a GROUP of 128-feature chunks (grid.y = feature groups, so
+//   X is read from HBM once per group, not once per chunk).  Per chunk the 128 per-feature
+//   records [W_j/pi, b'_j/pi, P_j...] are staged in shared memory and read as warp-uniform
+//   LDS.128 broadcasts.  Every store instruction of a warp writes 64 consecutive rows = 512
+//   contiguous bytes of one column as one 16-byte st.global.cs per lane (streaming).
+//   Two features per loop iteration (8 independent entries per thread) for FP64-pipe ILP;
+//   full tiles run a predicate-free loop, ragged tiles a masked one.
 #pragma once
 #include "fls_device.cuh"
 #include "fls_internal.h"
@@ -20,27 +23,57 @@
 namespace fls {
 
 template <int D, int G, int KM>
+struct EntryMath {
+  static constexpr int S = pf_stride(D, G, KM);
+
+  __device__ __forceinline__ static void record(const double *p, double (&rec)[S]) {
+#pragma unroll
+    for (int s2 = 0; s2 < S / 2; ++s2) {
+      const double2 v = reinterpret_cast<const double2 *>(p)[s2];
+      rec[2 * s2] = v.x;
+      rec[2 * s2 + 1] = v.y;
+    }
+  }
+
+  // one entry from the feature record and the row's registers
+  __device__ __forceinline__ static double entry(const double (&rec)[S], const double (&x)[D],
+                                                 const double (&c)[G > 0 ? G : 1]) {
+    double h = rec[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) h = fma(rec[k], x[k], h);
+    int sgn;
+    const double f = halfturn(h, sgn);
+    const double u = f * f;
+    if constexpr (KM == KM_SIN) {
+      double P = rec[D + 1];
+#pragma unroll
+      for (int g = 0; g < G; ++g) P = fma(c[g], rec[D + 2 + g], P);
+      return flipsign(P * sinpi_core(f, u), sgn);
+    } else {
+      double Ps = rec[D + 1], Pc = rec[D + 2];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        Ps = fma(c[g], rec[D + 3 + 2 * g], Ps);
+        Pc = fma(c[g], rec[D + 4 + 2 * g], Pc);
+      }
+      return flipsign(fma(Ps, sinpi_core(f, u), Pc * cospi_core(u)), sgn);
+    }
+  }
+};
+
+template <int D, int G, int KM>
 __global__ void __launch_bounds__(kNT) assemble_cm_kernel(const AsmArgs a) {
-  constexpr int NP = (G + 1) * (KM == KM_SINCOS ? 2 : 1);
-  constexpr int S = pf_stride(D, G, KM);
+  using M = EntryMath<D, G, KM>;
+  constexpr int S = M::S;
+  constexpr int GG = G > 0 ? G : 1;
   static_assert(S % 2 == 0, "pf stride must be even for 16-byte smem reads");
   extern __shared__ __align__(16) double sp[];
-
-  const int64_t j0 = (int64_t)blockIdx.y * kFC;
-  const int64_t nfe64 = a.F - j0;
-  const int nfe = nfe64 < kFC ? (int)nfe64 : kFC;
-  {
-    const double2 *src = reinterpret_cast<const double2 *>(a.pf + j0 * S);
-    double2 *dst = reinterpret_cast<double2 *>(sp);
-    const int n2 = nfe * (S / 2);
-    for (int t = threadIdx.x; t < n2; t += kNT) dst[t] = __ldg(src + t);
-  }
 
   // local rows (A-relative) of this thread: rbase + {0, 1, 2*kNT, 2*kNT + 1}; rbase is even.
   // The block's points map to local rows [lr0, lr1): point i = pt0 + (r - lr0).
   const int64_t rbase = (a.lr0 & ~int64_t(1)) + (int64_t)blockIdx.x * kRowsCTA + 2 * threadIdx.x;
   double x[4][D];
-  double c[4][G > 0 ? G : 1];
+  double c[4][GG];
   bool in[4];
   bool bad = false;
 #pragma unroll
@@ -54,7 +87,7 @@ __global__ void __launch_bounds__(kNT) assemble_cm_kernel(const AsmArgs a) {
       bad |= !finite(x[q][k]);
     }
 #pragma unroll
-    for (int g = 0; g < (G > 0 ? G : 1); ++g) {
+    for (int g = 0; g < GG; ++g) {
       c[q][g] = (G > 0 && in[q]) ? __ldg(a.fields + i * a.nf + a.gfield[g]) : 0.0;
       bad |= !finite(c[q][g]);
     }
@@ -65,56 +98,67 @@ __global__ void __launch_bounds__(kNT) assemble_cm_kernel(const AsmArgs a) {
     }
   }
   if (bad) atomicOr(a.err, 1u);
-  __syncthreads();
-
   const bool full = a.vec && in[0] && in[1] && in[2] && in[3];
-  double *colp = a.A + j0 * a.lda + rbase;
-  for (int jj = 0; jj < nfe; ++jj, colp += a.lda) {
-    const double *p = sp + jj * S;
-    double rec[S];
-#pragma unroll
-    for (int s2 = 0; s2 < S / 2; ++s2) {
-      const double2 v = reinterpret_cast<const double2 *>(p)[s2];
-      rec[2 * s2] = v.x;
-      rec[2 * s2 + 1] = v.y;
+
+  // feature chunks of this CTA's group
+  const int64_t n_chunks = (a.F + kFC - 1) / kFC;
+  const int64_t cpg = (n_chunks + gridDim.y - 1) / gridDim.y;
+  const int64_t c0 = (int64_t)blockIdx.y * cpg;
+  const int64_t c1 = c0 + cpg < n_chunks ? c0 + cpg : n_chunks;
+  for (int64_t ch = c0; ch < c1; ++ch) {
+    const int64_t j0 = ch * kFC;
+    const int nfe = (a.F - j0) < kFC ? (int)(a.F - j0) : kFC;
+    __syncthreads();  // previous chunk's records no longer in use
+    {
+      const double2 *src = reinterpret_cast<const double2 *>(a.pf + j0 * S);
+      double2 *dst = reinterpret_cast<double2 *>(sp);
+      const int n2 = nfe * (S / 2);
+      for (int t = threadIdx.x; t < n2; t += kNT) dst[t] = __ldg(src + t);
     }
-    double out[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      double h = rec[D];
-#pragma unroll
-      for (int k = 0; k < D; ++k) h = fma(rec[k], x[q][k], h);
-      int sgn;
-      const double f = halfturn(h, sgn);
-      const double u = f * f;
-      if constexpr (KM == KM_SIN) {
-        double P = rec[D + 1];
-#pragma unroll
-        for (int g = 0; g < G; ++g) P = fma(c[q][g], rec[D + 2 + g], P);
-        out[q] = P * sinpi_core(flipsign(f, sgn), u);
-      } else {
-        double Ps = rec[D + 1], Pc = rec[D + 2];
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          Ps = fma(c[q][g], rec[D + 3 + 2 * g], Ps);
-          Pc = fma(c[q][g], rec[D + 4 + 2 * g], Pc);
-        }
-        out[q] = flipsign(fma(Ps, sinpi_core(f, u), Pc * cospi_core(u)), sgn);
-      }
-    }
-    (void)NP;
+    __syncthreads();
+    double *colp = a.A + j0 * a.lda + rbase;
     if (full) {
-      __stcs(reinterpret_cast<double2 *>(colp), make_double2(out[0], out[1]));
-      __stcs(reinterpret_cast<double2 *>(colp + 2 * kNT), make_double2(out[2], out[3]));
-    } else {
+      int jj = 0;
+      for (; jj + 2 <= nfe; jj += 2, colp += 2 * a.lda) {
+        double r0[S], r1[S];
+        M::record(sp + jj * S, r0);
+        M::record(sp + (jj + 1) * S, r1);
+        double o0[4], o1[4];
 #pragma unroll
-      for (int pr = 0; pr < 2; ++pr) {
-        double *dst = colp + pr * (2 * kNT);
-        if (a.vec && in[2 * pr] && in[2 * pr + 1]) {
-          __stcs(reinterpret_cast<double2 *>(dst), make_double2(out[2 * pr], out[2 * pr + 1]));
-        } else {
-          if (in[2 * pr]) __stcs(dst, out[2 * pr]);
-          if (in[2 * pr + 1]) __stcs(dst + 1, out[2 * pr + 1]);
+        for (int q = 0; q < 4; ++q) {
+          o0[q] = M::entry(r0, x[q], c[q]);
+          o1[q] = M::entry(r1, x[q], c[q]);
+        }
+        __stcs(reinterpret_cast<double2 *>(colp), make_double2(o0[0], o0[1]));
+        __stcs(reinterpret_cast<double2 *>(colp + 2 * kNT), make_double2(o0[2], o0[3]));
+        __stcs(reinterpret_cast<double2 *>(colp + a.lda), make_double2(o1[0], o1[1]));
+        __stcs(reinterpret_cast<double2 *>(colp + a.lda + 2 * kNT), make_double2(o1[2], o1[3]));
+      }
+      if (jj < nfe) {
+        double r0[S];
+        M::record(sp + jj * S, r0);
+        double o0[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) o0[q] = M::entry(r0, x[q], c[q]);
+        __stcs(reinterpret_cast<double2 *>(colp), make_double2(o0[0], o0[1]));
+        __stcs(reinterpret_cast<double2 *>(colp + 2 * kNT), make_double2(o0[2], o0[3]));
+      }
+    } else {
+      for (int jj = 0; jj < nfe; ++jj, colp += a.lda) {
+        double r0[S];
+        M::record(sp + jj * S, r0);
+        double o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) o[q] = M::entry(r0, x[q], c[q]);
+#pragma unroll
+        for (int pr = 0; pr < 2; ++pr) {
+          double *dst = colp + pr * (2 * kNT);
+          if (a.vec && in[2 * pr] && in[2 * pr + 1]) {
+            __stcs(reinterpret_cast<double2 *>(dst), make_double2(o[2 * pr], o[2 * pr + 1]));
+          } else {
+            if (in[2 * pr]) __stcs(dst, o[2 * pr]);
+            if (in[2 * pr + 1]) __stcs(dst + 1, o[2 * pr + 1]);
+          }
         }
       }
     }

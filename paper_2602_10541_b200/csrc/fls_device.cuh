@@ -21,28 +21,39 @@ constexpr double kPi = 3.141592653589793238462643383279502884;
 constexpr double kInvPi = 0.318309886183790671537767526745028724;
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: x + kMagic rounds x to an integer
 
+// Coefficients live in constant memory so DFMA reads them as c[bank][offset] operands
+// (no per-iteration materialisation of 64-bit immediates).
 // sin(pi f) = f * p(f^2), |f| <= 1/2 -- tools/fit_sinpoly.py 7 sin
+static __constant__ double kSinC[7] = {0x1.921fb544422b9p+1, -0x1.4abbce622b70dp+2,
+                                       0x1.466bc666fa76ep+1, -0x1.32d2c80461e85p-1,
+                                       0x1.5076b5c39bedfp-4, -0x1.e289957d36087p-8,
+                                       0x1.d3d9ca396c5b5p-12};
+// cos(pi f) = q(f^2), |f| <= 1/2 -- tools/fit_sinpoly.py 8 cos
+static __constant__ double kCosC[8] = {1.0, -0x1.3bd3cc9be45b0p+2, 0x1.03c1f081b29f6p+2,
+                                       -0x1.55d3c7e0ba51dp+0, 0x1.e1f504256b638p-3,
+                                       -0x1.a6d11187be151p-6, 0x1.f97f5b4f53910p-10,
+                                       -0x1.a75f6839218cdp-14};
+
 __device__ __forceinline__ double sinpi_core(double f, double u) {
-  double p = 0x1.d3d9ca396c5b5p-12;
-  p = fma(p, u, -0x1.e289957d36087p-8);
-  p = fma(p, u, 0x1.5076b5c39bedfp-4);
-  p = fma(p, u, -0x1.32d2c80461e85p-1);
-  p = fma(p, u, 0x1.466bc666fa76ep+1);
-  p = fma(p, u, -0x1.4abbce622b70dp+2);
-  p = fma(p, u, 0x1.921fb544422b9p+1);
+  double p = kSinC[6];
+  p = fma(p, u, kSinC[5]);
+  p = fma(p, u, kSinC[4]);
+  p = fma(p, u, kSinC[3]);
+  p = fma(p, u, kSinC[2]);
+  p = fma(p, u, kSinC[1]);
+  p = fma(p, u, kSinC[0]);
   return f * p;
 }
 
-// cos(pi f) = q(f^2), |f| <= 1/2 -- tools/fit_sinpoly.py 8 cos
 __device__ __forceinline__ double cospi_core(double u) {
-  double q = -0x1.a75f6839218cdp-14;
-  q = fma(q, u, 0x1.f97f5b4f53910p-10);
-  q = fma(q, u, -0x1.a6d11187be151p-6);
-  q = fma(q, u, 0x1.e1f504256b638p-3);
-  q = fma(q, u, -0x1.55d3c7e0ba51dp+0);
-  q = fma(q, u, 0x1.03c1f081b29f6p+2);
-  q = fma(q, u, -0x1.3bd3cc9be45b0p+2);
-  q = fma(q, u, 1.0);
+  double q = kCosC[7];
+  q = fma(q, u, kCosC[6]);
+  q = fma(q, u, kCosC[5]);
+  q = fma(q, u, kCosC[4]);
+  q = fma(q, u, kCosC[3]);
+  q = fma(q, u, kCosC[2]);
+  q = fma(q, u, kCosC[1]);
+  q = fma(q, u, kCosC[0]);
   return q;
 }
 

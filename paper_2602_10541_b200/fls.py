@@ -25,7 +25,8 @@ from ._abi import FLS_COL_MAJOR, FLS_ROW_MAJOR, FlsError, check
 Term = Tuple[Sequence[int], float, int]   # (alpha, coef, field)
 
 __all__ = ["Context", "Block", "fls_features", "fls_assemble", "fls_solve", "fls_qr_r",
-           "fls_frob2", "fls_eval", "fls_sync", "fls_ctx_timing", "fls_ctx_timing_read", "FlsError", "FLS_COL_MAJOR", "FLS_ROW_MAJOR",
+           "fls_frob2", "fls_eval", "fls_sync", "fls_ctx_timing", "fls_ctx_timing_read",
+           "fls_assemble_host", "HostBlockSet", "BlockSet", "FlsError", "FLS_COL_MAJOR", "FLS_ROW_MAJOR",
            "round_up"]
 
 
@@ -194,6 +195,53 @@ def fls_assemble(ctx: Context, W: torch.Tensor, b: torch.Tensor, blocks, *,
                                    int(lda), int(layout), _ptr(rhs) if with_rhs else None))
     if layout == FLS_COL_MAJOR:
         return A, lda
+    return A, rhs
+
+
+def _host_ptr(a):
+    if a is None:
+        return None
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda or a.dtype != torch.float64 or not a.is_contiguous():
+            raise TypeError("host path needs contiguous float64 CPU tensors / arrays")
+        return a.data_ptr()
+    if a.dtype.name != "float64" or not a.flags.c_contiguous:
+        raise TypeError("host path needs contiguous float64 CPU tensors / arrays")
+    return a.ctypes.data
+
+
+class HostBlockSet:
+    """fls_block array over HOST memory (numpy arrays or CPU tensors; pinned is fastest)"""
+
+    def __init__(self, blocks, dim: int):
+        self.blocks = list(blocks)
+        self.ops = []
+        self.arr = (_abi.fls_block * len(self.blocks))()
+        for q, blk in enumerate(self.blocks):
+            op = _Op(dim, blk.terms)
+            self.ops.append(op)
+            B = self.arr[q]
+            B.X = _host_ptr(blk.X)
+            B.n_points = int(blk.X.shape[0])
+            B.op = C.pointer(op.op)
+            B.coef_fields = _host_ptr(blk.fields) if blk.fields is not None else None
+            B.n_fields = int(blk.fields.shape[1]) if blk.fields is not None else 0
+            B.weight = float(blk.weight)
+            B.values = _host_ptr(blk.values) if blk.values is not None else None
+        self.total = sum(int(b.X.shape[0]) for b in self.blocks)
+
+
+def fls_assemble_host(ctx: Context, W, b, blocks, A, lda: int, rhs=None, *, normalize: bool = True,
+                      row_begin: int = 0, row_end: Optional[int] = None, chunk_rows: int = 0):
+    """Host-buffer assembly (C ABI fls_assemble_host): W, b, the blocks' arrays, A (flat,
+    column-major, >= F * lda doubles) and rhs live in host memory.  Blocking."""
+    F, dim = int(W.shape[0]), int(W.shape[1])
+    bs = blocks if isinstance(blocks, HostBlockSet) else HostBlockSet(blocks, dim)
+    row_end = bs.total if row_end is None else int(row_end)
+    check(_abi.load().fls_assemble_host(ctx.handle, _host_ptr(W), _host_ptr(b), dim, F,
+                                        int(bool(normalize)), bs.arr, len(bs.blocks),
+                                        int(row_begin), row_end, _host_ptr(A), int(lda),
+                                        _host_ptr(rhs), int(chunk_rows)))
     return A, rhs
 
 
