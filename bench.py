@@ -82,17 +82,19 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        sm, mx, reasons = [], 0.0, set()
+        sm, mx, reasons, pw = [], 0.0, set(), []
         for r in self.rows:
             try:
                 sm.append(float(r[1]))
                 mx = max(mx, float(r[2]))
+                pw.append(float(r[3]))
             except ValueError:
                 continue
             for k, nm in enumerate(names):
                 if r[5 + k].lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "sm_min_mhz": min(sm) if sm else None, "power_w_max": max(pw) if pw else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
@@ -152,15 +154,84 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def e2e_measure(args, p, ctx, W, b, a, e, world, local):
+    """The same metric through the C ABI with HOST buffers (fls_assemble_host): every step copies
+    this rank's inputs (points, fields, values, W, b) from pinned host memory and every entry of
+    [A | b] back to pinned host memory.  The host output is a pinned ring of `ring` rows that
+    each call overwrites (a streaming consumer's view; 137 GB would not fit the host)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2602_10541_b200 import fls
+
+    F, d = p.n_features, p.dim
+    W_h = W.cpu().pin_memory()
+    b_h = b.cpu().pin_memory()
+
+    class HB:
+        pass
+    hblocks = []
+    in_bytes_points = 0
+    offs = p.block_offsets()
+    for blk, o in zip(p.blocks, offs):
+        h = HB()
+        h.X = torch.from_numpy(blk.X).pin_memory()
+        h.terms = blk.terms
+        h.weight = blk.weight
+        h.values = torch.from_numpy(blk.values).pin_memory()
+        h.fields = torch.from_numpy(blk.fields).pin_memory() if blk.fields is not None else None
+        hblocks.append(h)
+        lo, hi = max(a, o), min(e, o + blk.n)
+        if hi > lo:
+            per = d + 1 + (blk.fields.shape[1] if blk.fields is not None else 0)
+            in_bytes_points += 8 * (hi - lo) * per
+    hset = fls.HostBlockSet(hblocks, d)
+    n_local = e - a
+    ring = min(n_local, args.e2e_ring_rows)
+    A_h = torch.empty((F + 1) * ring, dtype=torch.float64).pin_memory()
+    n_calls = (n_local + ring - 1) // ring
+
+    def step():
+        for c in range(n_calls):
+            r0 = a + c * ring
+            r1 = min(e, r0 + ring)
+            fls.fls_assemble_host(ctx, W_h, b_h, hset, A_h, ring, A_h[F * ring:], row_begin=r0,
+                                  row_end=r1)
+
+    step()                                   # warm-up (staging allocation, first touch)
+    times = []
+    for _ in range(args.e2e_steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    t = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    s_step = float(t.item())
+    h2d = in_bytes_points + n_calls * 8 * (F * d + F)
+    d2h = 8 * n_local * (F + 1)
+    return {"value": p.n_rows * F / s_step, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "s_per_step": s_step, "steps": args.e2e_steps,
+            "api": "fls_assemble_host (C ABI, host buffers)",
+            "d2h_gbs": d2h / s_step / 1e9,
+            "note": f"pinned host ring of {ring} rows x {F + 1} columns, {n_calls} calls per step"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fls", choices=["fls", "reference"])
     ap.add_argument("--workload", default="c5_biharm3d")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
     ap.add_argument("--ref-rows", type=int, default=64)
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-ring-rows", type=int, default=262144)
     ap.add_argument("--rows", type=int, default=None,
                     help="override the interior row count (profiling a reduced copy of the workload)")
     args = ap.parse_args()
@@ -242,13 +313,14 @@ def main():
     # roofline of the dominant kernel (assembly): algorithmic bytes = 8 B x entries per launch
     hbm_peak, peak_kind = _peaks()
     k_avg_ms = k_ms / max(k_launches, 1)
-    bytes_per_launch = 8.0 * n_local * F / max(len(blocks), 1)
-    achieved = bytes_per_launch / (k_avg_ms / 1e3) / 1e9
+    # algorithmic bytes of all assembly launches of one step / their summed time per step
+    k_ms_step = k_ms / args.steps
+    achieved = 8.0 * n_local * F / (k_ms_step / 1e3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf) and args.rows is None and world == 1:
         try:
-            traffic = json.load(open(tf)).get(args.workload)
+            traffic = json.load(open(tf)).get(args.workload, {}).get("traffic_bytes_per_launch")
         except Exception:
             traffic = None
     line = {
@@ -267,6 +339,11 @@ def main():
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
     }
+    # ---------------------------------------------------------------- end to end (host buffers)
+    del Ab
+    torch.cuda.empty_cache()
+    if not args.no_e2e:
+        line["e2e"] = e2e_measure(args, p, ctx, W, b, a, e, world, local)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(p)
     if rank == 0:

@@ -1,0 +1,104 @@
+"""Multi-GPU plumbing: row sharding of the stacked system and the TSQR least-squares solve.
+
+Assembly needs no collective: rank r owns global rows
+[floor(r R / P), floor((r+1) R / P)) and every rank regenerates W, b from the seed.
+The solve has one real exchange step (TSQR, "QR or SVD"; Tikhonov form P:L158):
+
+    local:  [A_r | b_r] = Q_r R_r                      (fls_qr_r, cuSOLVER geqrf on each GPU)
+    gather: R_0 .. R_{P-1} -> root                      (torch.distributed / NCCL over NVLink)
+    root:   [R_0; ...; R_{P-1}; sqrt(mu) I | 0] = Q R   (fls_solve: geqrf + trsv)
+    bcast:  beta
+
+`ridge_rel` = tau of DESIGN.md reading A16: sqrt(mu) = tau ||A||_F with ||A||_F^2 summed over
+ranks (all_reduce).  Every arithmetic step runs in libfls / cuSOLVER; this module only moves
+tensors.  The local-QR / solve / norm callables are injectable so the host-side combine logic
+can be tested on CPU with gloo (tests/test_dist_gloo.py).
+"""
+from __future__ import annotations
+
+import math
+from typing import Callable, Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n_rows: int, rank: int, world: int) -> Tuple[int, int]:
+    return (rank * n_rows) // world, ((rank + 1) * n_rows) // world
+
+
+class _FlsOps:
+    """default arithmetic: libfls on the current device"""
+
+    def __init__(self, ctx):
+        from . import fls
+        self.fls = fls
+        self.ctx = ctx
+
+    def frob2(self, Ab, n_rows, lda, F):
+        return self.fls.fls_frob2(self.ctx, Ab, n_rows, lda, F)
+
+    def qr_r(self, Ab, n_rows, lda, ncols):
+        R, ldr = self.fls.fls_qr_r(self.ctx, Ab, n_rows, lda, ncols)
+        return R, ldr
+
+    def solve(self, M, n_rows, lda, F, sqrt_mu):
+        return self.fls.fls_solve(self.ctx, M, n_rows, lda, F, sqrt_mu)
+
+
+def tsqr_solve(Ab: torch.Tensor, n_local: int, lda: int, F: int, *, ridge_rel: float = 0.0,
+               ctx=None, ops=None, group=None, root: int = 0) -> Tuple[torch.Tensor, float]:
+    """beta = argmin ||A beta - b||^2 + mu ||beta||^2 for [A | b] row-sharded over the ranks.
+
+    Ab: this rank's column-major [A_r | b_r] (flat, (F+1) * lda, destroyed).
+    Returns (beta replicated on every rank, residual norm on root / 0.0 elsewhere)."""
+    ops = ops if ops is not None else _FlsOps(ctx)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    dev = Ab.device
+    nc = F + 1
+    sqrt_mu = 0.0
+    if ridge_rel > 0.0:
+        fro2 = torch.tensor([ops.frob2(Ab, n_local, lda, F) if n_local > 0 else 0.0],
+                            dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(fro2, op=dist.ReduceOp.SUM, group=group)
+        sqrt_mu = ridge_rel * math.sqrt(float(fro2.item()))
+    if world == 1:
+        if ridge_rel > 0.0 and lda < n_local + F:
+            raise ValueError("ridge needs lda >= n_local + F (reserve extra_rows=F)")
+        beta, res = ops.solve(Ab, n_local, lda, F, sqrt_mu)
+        return beta, res
+
+    # local R factor, padded to kmax rows (zero rows change nothing)
+    k = min(n_local, nc)
+    if k > 0:
+        R, ldr = ops.qr_r(Ab, n_local, lda, nc)
+        Rl = R[: nc * ldr].view(nc, ldr)[:, :k]           # (nc, k): column j = R[0:k, j]
+    else:
+        Rl = torch.zeros((nc, 0), dtype=torch.float64, device=dev)
+    ks = torch.tensor([k], dtype=torch.int64, device=dev)
+    all_k = [torch.zeros_like(ks) for _ in range(world)]
+    dist.all_gather(all_k, ks, group=group)
+    all_k = [int(t.item()) for t in all_k]
+    kmax = max(all_k)
+    send = torch.zeros((nc, kmax), dtype=torch.float64, device=dev)
+    send[:, :k] = Rl
+    gathered = [torch.empty_like(send) for _ in range(world)] if rank == root else None
+    dist.gather(send, gathered, dst=root, group=group)
+    beta = torch.empty((F,), dtype=torch.float64, device=dev)
+    res = 0.0
+    if rank == root:
+        K = sum(all_k)
+        ldm = K + (F if sqrt_mu > 0.0 else 0)
+        ldm = ((ldm + 3) // 4) * 4
+        M = torch.zeros((nc * ldm,), dtype=torch.float64, device=dev)
+        Mv = M.view(nc, ldm)
+        off = 0
+        for r in range(world):
+            Mv[:, off:off + all_k[r]] = gathered[r][:, :all_k[r]]
+            off += all_k[r]
+        b_root, res = ops.solve(M, K, ldm, F, sqrt_mu)
+        beta.copy_(b_root)
+    dist.broadcast(beta, src=root, group=group)
+    return beta, res

@@ -280,3 +280,23 @@ def test_eval_with_operator_matches_assembled_rows(ctx):
     Ao, _, S = oracle.assemble(W, b, [h])
     ref = Ao @ beta.cpu().numpy()
     assert np.abs(Lu - ref).max() <= 1e-12 * (S @ np.abs(beta.cpu().numpy())).max()
+
+
+# ------------------------------------------------------------------------------------- host path
+@pytest.mark.parametrize("chunk", [0, 1000, 4096])
+def test_assemble_host_matches_device(ctx, chunk):
+    """fls_assemble_host (host buffers, chunked, two streams) == fls_assemble, bitwise."""
+    p = wl.make_problem("c4_heat2d", "mini")
+    W, b, Wd, bd = _parity_feats(p)
+    F, R = p.n_features, p.n_rows
+    Ab, lda = fls.fls_assemble(ctx, Wd, bd, dev_blocks(p))
+    ref = Ab[: (F + 1) * lda].view(F + 1, lda)[:, :R].cpu().numpy()
+    for (r0, r1) in [(0, R), (17, R - 5)]:
+        n = r1 - r0
+        ldh = n + 3
+        A_h = np.full((F + 1) * ldh, np.nan)
+        fls.fls_assemble_host(ctx, W, b, p.blocks, A_h, ldh, A_h[F * ldh:], row_begin=r0,
+                              row_end=r1, chunk_rows=chunk)
+        got = A_h.reshape(F + 1, ldh)[:, :n]
+        assert np.array_equal(got, ref[:, r0:r1])
+        assert np.isnan(A_h.reshape(F + 1, ldh)[:F, n:]).all()     # padding untouched
