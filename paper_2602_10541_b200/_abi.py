@@ -11,7 +11,8 @@ import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "libfls.so")
+# FLS_LIB selects a tuning-variant build (tools/variant_sweep.sh); default = the product build
+LIB_PATH = os.environ.get("FLS_LIB") or os.path.join(HERE, "libfls.so")
 HEADER = os.path.join(ROOT, "include", "fls.h")
 
 FLS_MAX_DIM = 8

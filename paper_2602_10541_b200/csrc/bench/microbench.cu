@@ -239,6 +239,68 @@ __global__ void __launch_bounds__(256) entry2_kernel(double *out, int nfeat, dou
   if (s == 12345.678) out[threadIdx.x] = s;
 }
 
+// FP64 tensor path: mma.sync m8n8k4 f64 (DMMA); MODE 0 = DMMA only, 1 = DMMA + DFMA chains
+// interleaved (does the tensor path run beside the FP64 ALU pipe?), 2 = the DFMA chains alone
+template <int MODE>
+__global__ void __launch_bounds__(256) dmma_kernel(double *out, int iters, double a, double b) {
+  double acc[4][2];
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) acc[k][0] = acc[k][1] = threadIdx.x * 1e-3 + k;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k + 0.5;
+  const double av = a + threadIdx.x * 1e-9, bv = b;
+  for (int i = 0; i < iters; ++i) {
+    if (MODE <= 1) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        asm volatile(
+            "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+            : "+d"(acc[k][0]), "+d"(acc[k][1])
+            : "d"(av), "d"(bv));
+    }
+    if (MODE >= 1) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) s += acc[k][0] + acc[k][1];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+// returns DMMA instructions/s (warp-level) and DFMA/s for the selected mode
+extern "C" __attribute__((visibility("default"))) int mb_dmma_rate(int mode, double *scratch,
+                                                                   int iters, double *dmma_per_s,
+                                                                   double *dfma_per_s) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = sms * 8;
+  auto go = [&](int it) {
+    if (mode == 0) dmma_kernel<0><<<grid, 256>>>(scratch, it, 0.999, 1e-3);
+    if (mode == 1) dmma_kernel<1><<<grid, 256>>>(scratch, it, 0.999, 1e-3);
+    if (mode == 2) dmma_kernel<2><<<grid, 256>>>(scratch, it, 0.999, 1e-3);
+  };
+  go(100);
+  cudaEventRecord(e0);
+  go(iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  const double s = time_ms(e0, e1) / 1e3;
+  const double warps = (double)grid * 8;
+  *dmma_per_s = (mode <= 1) ? warps * iters * 4 / s : 0.0;
+  *dfma_per_s = (mode >= 1) ? (double)grid * 256 * iters * 8 / s : 0.0;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return (int)cudaGetLastError();
+}
+
 extern "C" __attribute__((visibility("default"))) int mb_op_rate(int op, double *scratch, int iters,
                                                                  double *ops_per_s) {
   cudaEvent_t e0, e1;

@@ -7,18 +7,22 @@
 // in the sin-only family, + 1 per coefficient field).
 //
 // Column-major layout A[j * lda + i] (what cuSOLVER geqrf consumes):
-//   CTA = 256 threads owning a 1024-row tile.  Thread t keeps the x_i (and coefficient
-//   fields) of 4 rows -- the row pairs (2t, 2t+1) and (512 + 2t, 512 + 2t + 1) -- in
-//   registers while the CTA walks a GROUP of 128-feature chunks (grid.y = feature groups, so
-//   X is read from HBM once per group, not once per chunk).  Per chunk the 128 per-feature
-//   records [W_j/pi, b'_j/pi, P_j...] are staged in shared memory and read as warp-uniform
-//   LDS.128 broadcasts.  Every store instruction of a warp writes 64 consecutive rows = 512
+//   CTA = kNT threads owning a kRowsCTA-row tile.  Thread t keeps the x_i (and coefficient
+//   fields) of 2*kPairs rows -- the row pairs (p*2*kNT + 2t, +1), p < kPairs -- in registers
+//   while the CTA walks a GROUP of kFC-feature chunks (grid.y = feature groups, so X is read
+//   from HBM once per group, not once per chunk).  Per chunk the per-feature records
+//   [W_j/pi, b'_j/pi, P_j...] are staged in shared memory and read as warp-uniform LDS.128
+//   broadcasts.  Every store instruction of a warp writes 64 consecutive rows = 512
 //   contiguous bytes of one column as one 16-byte st.global.cs per lane (streaming).
-//   Two features per loop iteration (8 independent entries per thread) for FP64-pipe ILP;
-//   full tiles run a predicate-free loop, ragged tiles a masked one.
+//   kFUnroll features per loop iteration (2*kPairs*kFUnroll independent entries per thread)
+//   for FP64-pipe ILP; full tiles run a predicate-free loop, ragged tiles a masked one.
 #pragma once
 #include "fls_device.cuh"
 #include "fls_internal.h"
+
+#ifndef FLS_MINB
+#define FLS_MINB 4   // 4 CTAs x 256 threads per SM -> <= 64 registers
+#endif
 
 namespace fls {
 
@@ -61,25 +65,35 @@ struct EntryMath {
   }
 };
 
+// resident CTAs per SM the register budget is sized for: the small sin-only kernels (all
+// BASELINE configs) fit 64 registers (4 CTAs); wide ones (many dims / fields, sin+cos) get 128
 template <int D, int G, int KM>
-__global__ void __launch_bounds__(kNT) assemble_cm_kernel(const AsmArgs a) {
+constexpr int asm_min_blocks() {
+  return (KM == KM_SIN && D + G <= 5) ? FLS_MINB : 2;
+}
+
+template <int D, int G, int KM>
+__global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_kernel(const AsmArgs a) {
   using M = EntryMath<D, G, KM>;
   constexpr int S = M::S;
   constexpr int GG = G > 0 ? G : 1;
+  constexpr int NQ = 2 * kPairs;  // rows per thread
   static_assert(S % 2 == 0, "pf stride must be even for 16-byte smem reads");
   extern __shared__ __align__(16) double sp[];
 
-  // local rows (A-relative) of this thread: rbase + {0, 1, 2*kNT, 2*kNT + 1}; rbase is even.
+  // local rows (A-relative) of this thread: rbase + p*2*kNT + {0, 1}; rbase is even.
   // The block's points map to local rows [lr0, lr1): point i = pt0 + (r - lr0).
   const int64_t rbase = (a.lr0 & ~int64_t(1)) + (int64_t)blockIdx.x * kRowsCTA + 2 * threadIdx.x;
-  double x[4][D];
-  double c[4][GG];
-  bool in[4];
+  double x[NQ][D];
+  double c[NQ][GG];
+  bool in[NQ];
   bool bad = false;
+  bool full = a.vec;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < NQ; ++q) {
     const int64_t r = rbase + (q >> 1) * (2 * kNT) + (q & 1);
     in[q] = (r >= a.lr0) && (r < a.lr1);
+    full = full && in[q];
     const int64_t i = a.pt0 + (r - a.lr0);
 #pragma unroll
     for (int k = 0; k < D; ++k) {
@@ -98,7 +112,6 @@ __global__ void __launch_bounds__(kNT) assemble_cm_kernel(const AsmArgs a) {
     }
   }
   if (bad) atomicOr(a.err, 1u);
-  const bool full = a.vec && in[0] && in[1] && in[2] && in[3];
 
   // feature chunks of this CTA's group
   const int64_t n_chunks = (a.F + kFC - 1) / kFC;
@@ -119,39 +132,41 @@ __global__ void __launch_bounds__(kNT) assemble_cm_kernel(const AsmArgs a) {
     double *colp = a.A + j0 * a.lda + rbase;
     if (full) {
       int jj = 0;
-      for (; jj + 2 <= nfe; jj += 2, colp += 2 * a.lda) {
-        double r0[S], r1[S];
-        M::record(sp + jj * S, r0);
-        M::record(sp + (jj + 1) * S, r1);
-        double o0[4], o1[4];
+      for (; jj + kFUnroll <= nfe; jj += kFUnroll, colp += kFUnroll * a.lda) {
+        double o[kFUnroll][NQ];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          o0[q] = M::entry(r0, x[q], c[q]);
-          o1[q] = M::entry(r1, x[q], c[q]);
+        for (int u = 0; u < kFUnroll; ++u) {
+          double rec[S];
+          M::record(sp + (jj + u) * S, rec);
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) o[u][q] = M::entry(rec, x[q], c[q]);
         }
-        __stcs(reinterpret_cast<double2 *>(colp), make_double2(o0[0], o0[1]));
-        __stcs(reinterpret_cast<double2 *>(colp + 2 * kNT), make_double2(o0[2], o0[3]));
-        __stcs(reinterpret_cast<double2 *>(colp + a.lda), make_double2(o1[0], o1[1]));
-        __stcs(reinterpret_cast<double2 *>(colp + a.lda + 2 * kNT), make_double2(o1[2], o1[3]));
-      }
-      if (jj < nfe) {
-        double r0[S];
-        M::record(sp + jj * S, r0);
-        double o0[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) o0[q] = M::entry(r0, x[q], c[q]);
-        __stcs(reinterpret_cast<double2 *>(colp), make_double2(o0[0], o0[1]));
-        __stcs(reinterpret_cast<double2 *>(colp + 2 * kNT), make_double2(o0[2], o0[3]));
+        for (int u = 0; u < kFUnroll; ++u)
+#pragma unroll
+          for (int pr = 0; pr < kPairs; ++pr)
+            __stcs(reinterpret_cast<double2 *>(colp + u * a.lda + pr * (2 * kNT)),
+                   make_double2(o[u][2 * pr], o[u][2 * pr + 1]));
+      }
+      for (; jj < nfe; ++jj, colp += a.lda) {
+        double rec[S];
+        M::record(sp + jj * S, rec);
+        double o[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) o[q] = M::entry(rec, x[q], c[q]);
+#pragma unroll
+        for (int pr = 0; pr < kPairs; ++pr)
+          __stcs(reinterpret_cast<double2 *>(colp + pr * (2 * kNT)), make_double2(o[2 * pr], o[2 * pr + 1]));
       }
     } else {
       for (int jj = 0; jj < nfe; ++jj, colp += a.lda) {
-        double r0[S];
-        M::record(sp + jj * S, r0);
-        double o[4];
+        double rec[S];
+        M::record(sp + jj * S, rec);
+        double o[NQ];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) o[q] = M::entry(r0, x[q], c[q]);
+        for (int q = 0; q < NQ; ++q) o[q] = M::entry(rec, x[q], c[q]);
 #pragma unroll
-        for (int pr = 0; pr < 2; ++pr) {
+        for (int pr = 0; pr < kPairs; ++pr) {
           double *dst = colp + pr * (2 * kNT);
           if (a.vec && in[2 * pr] && in[2 * pr + 1]) {
             __stcs(reinterpret_cast<double2 *>(dst), make_double2(o[2 * pr], o[2 * pr + 1]));

@@ -18,9 +18,21 @@ enum PrefMode : int32_t {
 // kernel families
 enum KMode : int32_t { KM_SIN = 0, KM_SINCOS = 1 };
 
-constexpr int kNT = 256;           // threads per CTA, column-major assembly
-constexpr int kRowsCTA = 4 * kNT;  // 4 rows per thread (two 16-byte row pairs)
-constexpr int kFC = 128;           // features per CTA tile
+// column-major assembly tiling (compile-time; -D overrides are for tuning sweeps only)
+#ifndef FLS_PAIRS
+#define FLS_PAIRS 2
+#endif
+#ifndef FLS_FUNROLL
+#define FLS_FUNROLL 2
+#endif
+#ifndef FLS_NT
+#define FLS_NT 256
+#endif
+constexpr int kNT = FLS_NT;                 // threads per CTA
+constexpr int kPairs = FLS_PAIRS;           // 16-byte row pairs per thread
+constexpr int kFUnroll = FLS_FUNROLL;       // features per loop iteration
+constexpr int kRowsCTA = 2 * kPairs * kNT;  // rows per CTA tile
+constexpr int kFC = 128;                    // features per shared-memory chunk
 constexpr int kRmRows = 64;        // rows per CTA, row-major assembly
 constexpr int kRmFeat = 64;        // features per CTA (2 per lane), row-major assembly
 

@@ -50,6 +50,15 @@ def main():
                             C.byref(res))
         torch.cuda.synchronize()
         out[f"op_{name}_per_s"] = res.value
+    lib.mb_dmma_rate.restype = C.c_int
+    r2 = C.c_double()
+    for mode, name in enumerate(["dmma_only", "dmma_plus_dfma", "dfma_only"]):
+        st = lib.mb_dmma_rate(mode, C.c_void_p(scratch.data_ptr()), 200_000, C.byref(res), C.byref(r2))
+        torch.cuda.synchronize()
+        # one m8n8k4 DMMA = 8*8*4 = 256 FMAs
+        out[f"{name}_dmma_fma_per_s"] = res.value * 256
+        out[f"{name}_dfma_per_s"] = r2.value
+        out[f"{name}_status"] = st
     mhz = out["dfma_per_s_clocks"]["sm_mhz"]
     if mhz:
         out["dfma_per_clk_per_sm"] = out["dfma_per_s"] / (mhz * 1e6) / torch.cuda.get_device_properties(0).multi_processor_count
