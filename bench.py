@@ -220,6 +220,77 @@ def e2e_measure(args, p, ctx, W, b, a, e, world, local):
             "note": f"pinned host ring of {ring} rows x {F + 1} columns, {n_calls} calls per step"}
 
 
+def solve_measure(args, world, rank, local):
+    """End-to-end solve (BASELINE metric "end-to-end solve ms"), per phase, Algorithm 1 lines
+    1-6: features + assembly + least squares (QR; TSQR over the ranks) + eval at 10,000
+    held-out points.  C5 solves its first 262,144 rows (J:configs[5]) with the tau = 1e-10
+    ridge (reading A16); other workloads solve all rows."""
+    import torch
+    import workloads as wl
+    from paper_2602_10541_b200 import dist as fdist
+    from paper_2602_10541_b200 import fls
+
+    kw = {"n_int": 262_144} if args.workload == "c5_biharm3d" else {}
+    p = wl.make_problem(args.workload, "full", **kw)
+    F, R, d = p.n_features, p.n_rows, p.dim
+    a, e = wl.shard_range(R, rank, world)
+    n_local = e - a
+    offs = p.block_offsets()
+    blocks = []
+    for blk, o in zip(p.blocks, offs):
+        lo, hi = max(a, o), min(e, o + blk.n)
+        if hi <= lo:
+            continue
+        sl = slice(lo - o, hi - o)
+        blocks.append(fls.Block(torch.from_numpy(np.ascontiguousarray(blk.X[sl])).cuda(), blk.terms,
+                                blk.weight, torch.from_numpy(np.ascontiguousarray(blk.values[sl])).cuda(),
+                                torch.from_numpy(np.ascontiguousarray(blk.fields[sl])).cuda()
+                                if blk.fields is not None else None))
+    bset = fls.BlockSet(blocks, d)
+    ctx = fls.Context(local)
+    Xt = torch.from_numpy(p.test_points(10_000)).cuda()
+    extra = F if (p.ridge_rel > 0 and world == 1) else 0
+    lda = fls.round_up(n_local + extra, 4)
+    Ab = torch.empty(((F + 1) * lda,), dtype=torch.float64, device="cuda")
+    st = ctx.stream
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+
+    def run():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        ev[0].record(st)
+        W, b = fls.fls_features(ctx, d, F, p.sigma, p.seed)
+        ev[1].record(st)
+        fls.fls_assemble(ctx, W, b, bset, row_begin=0, row_end=n_local, A=Ab, lda=lda)
+        ev[2].record(st)
+        beta, res = fdist.tsqr_solve(Ab, n_local, lda, F, ridge_rel=p.ridge_rel, ctx=ctx)
+        ev[3].record(st)
+        u = fls.fls_eval(ctx, W, b, beta, Xt)
+        ev[4].record(st)
+        torch.cuda.synchronize()
+        return u, res
+
+    run()                                   # warm-up (cuSOLVER workspace, handles)
+    u, res = run()
+    ph = [ev[k].elapsed_time(ev[k + 1]) for k in range(4)]
+    t = torch.tensor(ph, dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ph = [float(v) for v in t.tolist()]
+    us = p.u_star(Xt.cpu().numpy())
+    uh = u.cpu().numpy()
+    ctx.close()
+    out = {"ms": sum(ph), "features_ms": ph[0], "assemble_ms": ph[1], "lstsq_ms": ph[2],
+           "eval_ms": ph[3], "rows": R, "features": F, "ridge_rel": p.ridge_rel,
+           "method": "Householder QR (cuSOLVER geqrf) + trsv" + (" / TSQR over ranks" if world > 1 else ""),
+           "qr_flops": 2.0 * (R + extra) * (F + 1) ** 2 - 2.0 / 3.0 * (F + 1) ** 3,
+           "resid_norm": res}
+    if args.workload != "c5_biharm3d":   # C5 has no BC rows: u* is not the LS solution (A12)
+        out["rel_l2_vs_u_star"] = float(np.linalg.norm(uh - us) / np.linalg.norm(us))
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -230,6 +301,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
     ap.add_argument("--ref-rows", type=int, default=64)
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
+    ap.add_argument("--no-solve", action="store_true", help="skip the end-to-end solve leg")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-ring-rows", type=int, default=262144)
     ap.add_argument("--rows", type=int, default=None,
@@ -344,6 +416,8 @@ def main():
     torch.cuda.empty_cache()
     if not args.no_e2e:
         line["e2e"] = e2e_measure(args, p, ctx, W, b, a, e, world, local)
+    if not args.no_solve and args.rows is None:
+        line["solve"] = solve_measure(args, world, rank, local)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(p)
     if rank == 0:
