@@ -63,6 +63,7 @@ extern "C" {
 #define FLS_MAX_DIM 8      /* spatial / space-time dimension d <= 8 */
 #define FLS_MAX_TERMS 64   /* terms per operator */
 #define FLS_MAX_FIELDS 4   /* coefficient fields per block */
+#define FLS_MAX_FEAT_BLOCKS 16 /* bandwidth blocks of a multi-block basis */
 
 typedef enum {
     FLS_OK = 0,
@@ -147,6 +148,16 @@ typedef struct {
 FLS_API fls_status fls_features(fls_ctx *ctx, int32_t dim, int64_t n_features, double sigma,
                         uint64_t seed, double *W, double *b);
 
+/* Multi-block basis ("B blocks at potentially different bandwidths sigma_b,
+ * concatenating all features"): block q holds block_features[q] consecutive features drawn
+ * with sigmas[q]; the same Philox streams as fls_features, with W[j][k] =
+ * sigma_{block(j)} * normal[j*dim + k] (n_blocks = 1 is exactly fls_features).
+ *   block_features, sigmas: host arrays of n_blocks (1..FLS_MAX_FEAT_BLOCKS), each >= 1 / > 0.
+ *   W: device, (sum block_features) x dim.  b: device, sum block_features. */
+FLS_API fls_status fls_features_blocks(fls_ctx *ctx, int32_t dim, int32_t n_blocks,
+                                       const int64_t *block_features, const double *sigmas,
+                                       uint64_t seed, double *W, double *b);
+
 #define FLS_COL_MAJOR 0   /* A[j * lda + i]: rows contiguous (what fls_solve consumes) */
 #define FLS_ROW_MAJOR 1   /* A[i * lda + j]: features contiguous */
 
@@ -207,7 +218,26 @@ FLS_API fls_status fls_assemble_host(fls_ctx *ctx, const double *W, const double
 FLS_API fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int64_t n_features,
                      double sqrt_mu, double *beta, double *resid_norm);
 
-/* TSQR building block: Householder QR of the local column-major block M (n_rows x n_cols,
+/* ---------------------------------------------------------------------------------------- */
+/* Cached / prefactored solves (App. I "Matrix caching": factor A once, then     */
+/* every new right-hand side costs a cached apply; inverse problems P:L395-397).             */
+/* fls_qr_factor copies the column-major A (n_rows x n_features, lda) into ctx-independent   */
+/* device storage owned by the returned handle, appends [sqrt_mu I] rows when sqrt_mu > 0,   */
+/* and runs Householder QR (geqrf).  fls_qr_solve then computes, for each of nrhs columns of  */
+/* B (n_rows x nrhs, ldb; the ridge rows' rhs are 0), beta = R^-1 (Q^T [b; 0])[0:n_features] */
+/* (ormqr + trsm) into Beta (n_features x nrhs, ldbeta).  All device pointers; blocking.      */
+/* The handle is immutable after factoring and may be used from any ctx on the same device.  */
+/*   Errors: FLS_EINVAL (sizes, NULL), FLS_ENOMEM, FLS_ECUSOLVER, FLS_ERANK (zero diagonal,   */
+/*   sqrt_mu = 0; reported by fls_qr_factor).                                                 */
+/* ---------------------------------------------------------------------------------------- */
+typedef struct fls_qr fls_qr;
+FLS_API fls_status fls_qr_factor(fls_ctx *ctx, const double *A, int64_t n_rows, int64_t lda,
+                                 int64_t n_features, double sqrt_mu, fls_qr **out);
+FLS_API fls_status fls_qr_solve(fls_ctx *ctx, const fls_qr *qr, const double *B, int64_t ldb,
+                                int64_t nrhs, double *Beta, int64_t ldbeta);
+FLS_API fls_status fls_qr_destroy(fls_qr *qr);
+
+/* TSQR building block:Householder QR of the local column-major block M (n_rows x n_cols,
  * destroyed) and copy of its upper-trapezoidal R (min(n_rows, n_cols) x n_cols, zeros below
  * the diagonal) into R (device, column-major, ldr >= min(n_rows, n_cols)).  Blocking. */
 FLS_API fls_status fls_qr_r(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda, int64_t n_cols,

@@ -50,7 +50,9 @@ def lib():
         L.orc_philox4x64.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_raw_stream.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, C.c_void_p]
         L.orc_features.argtypes = [C.c_int, C.c_int64, C.c_double, C.c_uint64, C.c_void_p, C.c_void_p]
-        L.orc_diff.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_features_blocks.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64,
+                                          C.c_void_p, C.c_void_p]
+        L.orc_diff.argtypes =[C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_assemble.argtypes = [C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
                                    C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_lstsq.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_double,
@@ -91,6 +93,16 @@ def features(dim: int, n_features: int, sigma: float, seed: int):
     W = np.zeros((n_features, dim))
     b = np.zeros(n_features)
     lib().orc_features(dim, n_features, sigma, seed, _p(W), _p(b))
+    return W, b
+
+
+def features_blocks(dim: int, counts: Sequence[int], sigmas: Sequence[float], seed: int):
+    F = int(sum(counts))
+    W = np.zeros((F, dim))
+    b = np.zeros(F)
+    c = np.array(counts, dtype=np.int64)
+    s = np.array(sigmas, dtype=np.float64)
+    lib().orc_features_blocks(dim, len(counts), _p(c), _p(s), seed, _p(W), _p(b))
     return W, b
 
 

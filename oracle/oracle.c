@@ -104,6 +104,36 @@ int orc_features(int dim, int64_t n_features, double sigma, uint64_t seed, doubl
     return 0;
 }
 
+/*
+ * Multi-block basis ("B blocks at potentially different bandwidths sigma_b,
+ * concatenating all features"): the same streams as orc_features; feature j of block q
+ * (counts[0] + ... + counts[q-1] <= j < ... + counts[q]) gets W_j = sigmas[q] * normals.
+ */
+int orc_features_blocks(int dim, int n_blocks, const int64_t *counts, const double *sigmas,
+                        uint64_t seed, double *W, double *b) {
+    const double two_pi = 6.283185307179586476925286766559;
+    int64_t F = 0;
+    for (int q = 0; q < n_blocks; ++q) F += counts[q];
+    int64_t n_norm = F * (int64_t)dim;
+    for (int64_t m = 0; m < n_norm; ++m) {
+        int64_t pair = m / 2;
+        double u1 = uniform01(seed, 1, (uint64_t)(2 * pair));
+        double u2 = uniform01(seed, 1, (uint64_t)(2 * pair + 1));
+        double rad = sqrt(-2.0 * log(1.0 - u1));
+        double th = two_pi * u2;
+        double g = (m % 2 == 0) ? rad * cos(th) : rad * sin(th);
+        int64_t j = m / dim, end = 0;
+        int q = 0;
+        for (q = 0; q < n_blocks; ++q) {
+            end += counts[q];
+            if (j < end) break;
+        }
+        W[m] = sigmas[q] * g;
+    }
+    for (int64_t j = 0; j < F; ++j) b[j] = two_pi * uniform01(seed, 2, (uint64_t)j);
+    return 0;
+}
+
 /* ------------------------------------------------------------------------- */
 /* Symbolic differentiation of  c * Phi_p(W.x + b) * prod_k W_k^{e_k}.        */
 /* State (e, p); Phi_0 = sin, Phi_1 = cos, Phi_2 = -sin, Phi_3 = -cos.        */

@@ -269,13 +269,33 @@ fls_status fls_sync(fls_ctx *ctx) {
 // ---------------------------------------------------------------------------------------------
 fls_status fls_features(fls_ctx *ctx, int32_t dim, int64_t n_features, double sigma,
                         uint64_t seed, double *W, double *b) {
+  return fls_features_blocks(ctx, dim, 1, &n_features, &sigma, seed, W, b);
+}
+
+fls_status fls_features_blocks(fls_ctx *ctx, int32_t dim, int32_t n_blocks,
+                               const int64_t *block_features, const double *sigmas, uint64_t seed,
+                               double *W, double *b) {
   if (fls_status s = check_ctx(ctx)) return s;
   if (dim < 1 || dim > FLS_MAX_DIM) return fail(FLS_EINVAL, "dim %d not in 1..%d", dim, FLS_MAX_DIM);
-  if (n_features < 1) return fail(FLS_EINVAL, "n_features %lld < 1", (long long)n_features);
-  if (!(sigma > 0.0) || !std::isfinite(sigma)) return fail(FLS_EINVAL, "sigma must be > 0 and finite");
+  if (n_blocks < 1 || n_blocks > FLS_MAX_FEAT_BLOCKS)
+    return fail(FLS_EINVAL, "n_blocks %d not in 1..%d", n_blocks, FLS_MAX_FEAT_BLOCKS);
+  if (!block_features || !sigmas) return fail(FLS_EINVAL, "block_features or sigmas is NULL");
+  FeatBlocks fb;
+  std::memset(&fb, 0, sizeof fb);
+  fb.n = n_blocks;
+  int64_t F = 0;
+  for (int q = 0; q < n_blocks; ++q) {
+    if (block_features[q] < 1)
+      return fail(FLS_EINVAL, "block %d: n_features %lld < 1", q, (long long)block_features[q]);
+    if (!(sigmas[q] > 0.0) || !std::isfinite(sigmas[q]))
+      return fail(FLS_EINVAL, "block %d: sigma must be > 0 and finite", q);
+    F += block_features[q];
+    fb.ends[q] = F;
+    fb.sigma[q] = sigmas[q];
+  }
   if (!W || !b) return fail(FLS_EINVAL, "W or b is NULL");
   DeviceGuard g(ctx->device);
-  cudaError_t e = launch_features(dim, n_features, sigma, seed, W, b, ctx->stream);
+  cudaError_t e = launch_features(dim, F, fb, seed, W, b, ctx->stream);
   if (e != cudaSuccess) return cuda_fail(e, "features_kernel");
   return FLS_OK;
 }
@@ -622,7 +642,7 @@ fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int6
   if (fls_status s = fls_sync(ctx)) return s;  // surface pending async errors first
   if (fls_status s = ensure_handles(ctx)) return s;
   if (sqrt_mu > 0.0) {
-    cudaError_t e = launch_ridge_fill(Ab, lda, n_rows, n_features, sqrt_mu, ctx->stream);
+    cudaError_t e = launch_ridge_fill(Ab, lda, n_rows, n_features, n_features + 1, sqrt_mu, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "ridge_fill");
   }
   const int64_t n = n_features + 1;
@@ -646,6 +666,139 @@ fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int6
     return fail(FLS_ECUSOLVER, "cublasDtrsv failed");
   FLS_CUDA(cudaStreamSynchronize(ctx->stream));
   if (resid_norm) *resid_norm = std::fabs(rnn);
+  return FLS_OK;
+}
+
+}  // extern "C"
+
+struct fls_qr {
+  int device = 0;
+  int64_t m = 0, n = 0, ld = 0, m_rows = 0;  // m = factored rows (incl. ridge), m_rows = data rows
+  double *M = nullptr;                        // Householder vectors + R, column-major
+  double *tau = nullptr;
+};
+
+extern "C" {
+
+fls_status fls_qr_factor(fls_ctx *ctx, const double *A, int64_t n_rows, int64_t lda,
+                         int64_t n_features, double sqrt_mu, fls_qr **out) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!A || !out) return fail(FLS_EINVAL, "A or out is NULL");
+  *out = nullptr;
+  if (n_features < 1 || n_rows < 0 || lda < n_rows) return fail(FLS_EINVAL, "bad sizes");
+  if (!(sqrt_mu >= 0.0) || !std::isfinite(sqrt_mu)) return fail(FLS_EINVAL, "sqrt_mu must be >= 0");
+  const int64_t m = n_rows + (sqrt_mu > 0.0 ? n_features : 0);
+  if (m < n_features) return fail(FLS_EINVAL, "underdetermined without ridge");
+  DeviceGuard g(ctx->device);
+  if (fls_status s = fls_sync(ctx)) return s;
+  if (fls_status s = ensure_handles(ctx)) return s;
+  fls_qr *q = new fls_qr();
+  q->device = ctx->device;
+  q->m = m;
+  q->m_rows = n_rows;
+  q->n = n_features;
+  q->ld = (m + 3) / 4 * 4;
+  if (cudaMalloc(&q->M, sizeof(double) * q->ld * n_features) != cudaSuccess ||
+      cudaMalloc(&q->tau, sizeof(double) * n_features) != cudaSuccess) {
+    cudaGetLastError();
+    fls_qr_destroy(q);
+    return fail(FLS_ENOMEM, "fls_qr_factor: %lld x %lld storage", (long long)q->ld, (long long)n_features);
+  }
+  cudaError_t e = cudaMemcpy2DAsync(q->M, sizeof(double) * q->ld, A, sizeof(double) * lda,
+                                    sizeof(double) * n_rows, n_features, cudaMemcpyDeviceToDevice,
+                                    ctx->stream);
+  if (e == cudaSuccess && sqrt_mu > 0.0)
+    e = launch_ridge_fill(q->M, q->ld, n_rows, n_features, n_features, sqrt_mu, ctx->stream);
+  if (e != cudaSuccess) {
+    fls_qr_destroy(q);
+    return cuda_fail(e, "fls_qr_factor copy");
+  }
+  // geqrf keeping tau: reuse geqrf_inplace's path but we need tau -> do it here
+  int lwork = 0;
+  if (cusolverDnDgeqrf_bufferSize(ctx->solver, (int)m, (int)n_features, q->M, (int)q->ld, &lwork) !=
+      CUSOLVER_STATUS_SUCCESS) {
+    fls_qr_destroy(q);
+    return fail(FLS_ECUSOLVER, "geqrf_bufferSize");
+  }
+  double *work = nullptr;
+  if (cudaMallocAsync((void **)&work, sizeof(double) * (lwork + 2), ctx->stream) != cudaSuccess) {
+    cudaGetLastError();
+    fls_qr_destroy(q);
+    return fail(FLS_ENOMEM, "geqrf workspace");
+  }
+  int *info = reinterpret_cast<int *>(work + lwork);
+  cusolverStatus_t st = cusolverDnDgeqrf(ctx->solver, (int)m, (int)n_features, q->M, (int)q->ld,
+                                         q->tau, work, lwork, info);
+  int h_info = 0;
+  double dmin = 0.0;
+  cudaMemcpyAsync(&h_info, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+  launch_min_abs_diag(q->M, q->ld, n_features, ctx->d_scratch, ctx->stream);
+  cudaMemcpyAsync(&dmin, ctx->d_scratch, sizeof dmin, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaFreeAsync(work, ctx->stream);
+  e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    fls_qr_destroy(q);
+    return cuda_fail(e, "fls_qr_factor");
+  }
+  if (st != CUSOLVER_STATUS_SUCCESS || h_info != 0) {
+    fls_qr_destroy(q);
+    return fail(FLS_ECUSOLVER, "geqrf status %d info %d", (int)st, h_info);
+  }
+  if (dmin == 0.0) {
+    fls_qr_destroy(q);
+    return fail(FLS_ERANK, "R has an exactly zero diagonal entry (rank deficient)");
+  }
+  *out = q;
+  return FLS_OK;
+}
+
+fls_status fls_qr_solve(fls_ctx *ctx, const fls_qr *q, const double *B, int64_t ldb, int64_t nrhs,
+                        double *Beta, int64_t ldbeta) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!q || !B || !Beta) return fail(FLS_EINVAL, "qr, B or Beta is NULL");
+  if (nrhs < 1 || ldb < q->m_rows || ldbeta < q->n) return fail(FLS_EINVAL, "bad sizes");
+  if (q->device != ctx->device) return fail(FLS_EINVAL, "qr factored on device %d", q->device);
+  DeviceGuard g(ctx->device);
+  if (fls_status s = ensure_handles(ctx)) return s;
+  double *C = nullptr;
+  const int64_t ldc = q->ld;
+  int lwork = 0;
+  if (cusolverDnDormqr_bufferSize(ctx->solver, CUBLAS_SIDE_LEFT, CUBLAS_OP_T, (int)q->m, (int)nrhs,
+                                  (int)q->n, q->M, (int)q->ld, q->tau, C, (int)ldc, &lwork) !=
+      CUSOLVER_STATUS_SUCCESS)
+    return fail(FLS_ECUSOLVER, "ormqr_bufferSize");
+  const size_t cbytes = sizeof(double) * ldc * nrhs;
+  if (cudaMallocAsync((void **)&C, cbytes + sizeof(double) * (lwork + 2), ctx->stream) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FLS_ENOMEM, "qr_solve workspace");
+  }
+  double *work = C + ldc * nrhs;
+  int *info = reinterpret_cast<int *>(work + lwork);
+  FLS_CUDA(cudaMemsetAsync(C, 0, cbytes, ctx->stream));
+  FLS_CUDA(cudaMemcpy2DAsync(C, sizeof(double) * ldc, B, sizeof(double) * ldb,
+                             sizeof(double) * q->m_rows, nrhs, cudaMemcpyDeviceToDevice, ctx->stream));
+  cusolverStatus_t st = cusolverDnDormqr(ctx->solver, CUBLAS_SIDE_LEFT, CUBLAS_OP_T, (int)q->m,
+                                         (int)nrhs, (int)q->n, q->M, (int)q->ld, q->tau, C,
+                                         (int)ldc, work, lwork, info);
+  const double one = 1.0;
+  cublasStatus_t bs = cublasDtrsm(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                                  CUBLAS_DIAG_NON_UNIT, (int)q->n, (int)nrhs, &one, q->M,
+                                  (int)q->ld, C, (int)ldc);
+  cudaMemcpy2DAsync(Beta, sizeof(double) * ldbeta, C, sizeof(double) * ldc, sizeof(double) * q->n,
+                    nrhs, cudaMemcpyDeviceToDevice, ctx->stream);
+  cudaFreeAsync(C, ctx->stream);
+  FLS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (st != CUSOLVER_STATUS_SUCCESS) return fail(FLS_ECUSOLVER, "ormqr status %d", (int)st);
+  if (bs != CUBLAS_STATUS_SUCCESS) return fail(FLS_ECUSOLVER, "trsm status %d", (int)bs);
+  return FLS_OK;
+}
+
+fls_status fls_qr_destroy(fls_qr *q) {
+  if (!q) return FLS_OK;
+  DeviceGuard g(q->device);
+  cudaFree(q->M);
+  cudaFree(q->tau);
+  delete q;
   return FLS_OK;
 }
 

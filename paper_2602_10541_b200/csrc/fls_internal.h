@@ -93,13 +93,19 @@ __host__ __device__ constexpr int pf_stride(int D, int G, int kmode) {
 }
 
 // launchers (fls_kernels.cu / fls_assemble_*.cu)
-cudaError_t launch_features(int32_t dim, int64_t F, double sigma, uint64_t seed, double *W,
+struct FeatBlocks {  // multi-block bandwidths; n = 1 is the plain basis
+  int32_t n;
+  int64_t ends[FLS_MAX_FEAT_BLOCKS];
+  double sigma[FLS_MAX_FEAT_BLOCKS];
+};
+cudaError_t launch_features(int32_t dim, int64_t F, const FeatBlocks &fb, uint64_t seed, double *W,
                             double *b, cudaStream_t st);
 cudaError_t launch_prefactor(const PrefArgs &a, cudaStream_t st);
 cudaError_t launch_assemble_cm(int D, int G, int kmode, const AsmArgs &a, cudaStream_t st);
 cudaError_t launch_assemble_rm(int D, int G, int kmode, const AsmArgs &a, cudaStream_t st);
 cudaError_t launch_eval(int D, const EvalArgs &a, cudaStream_t st);
-cudaError_t launch_ridge_fill(double *Ab, int64_t lda, int64_t row0, int64_t F, double sqrt_mu,
+cudaError_t launch_ridge_fill(double *Ab, int64_t lda, int64_t row0, int64_t F, int64_t ncols,
+                              double sqrt_mu,
                               cudaStream_t st);
 cudaError_t launch_copy_upper(const double *M, int64_t lda, int64_t k, int64_t n, double *R,
                               int64_t ldr, cudaStream_t st);

@@ -32,10 +32,18 @@ __device__ __forceinline__ double u01(uint64_t r) {
   return (double)(r >> 11) * (1.0 / 9007199254740992.0);
 }
 
+// sigma of feature j under the multi-block basis: block q covers [ends[q-1], ends[q])
+__device__ __forceinline__ double block_sigma(const FeatBlocks &fb, int64_t j) {
+  int q = 0;
+  while (q + 1 < fb.n && j >= fb.ends[q]) ++q;
+  return fb.sigma[q];
+}
+
 // thread t owns Philox block t: raw words 4t..4t+3 of stream 1 -> normals 4t..4t+3
 // (Box-Muller pairs (4t, 4t+1) and (4t+2, 4t+3)); of stream 2 -> b_{4t..4t+3}.
-__global__ void features_kernel(int32_t D, int64_t F, double sigma, uint64_t seed, double *W,
-                                double *b) {
+// W[j][k] = sigma_{block(j)} * normal[j*D + k].
+__global__ void features_kernel(int32_t D, int64_t F, const FeatBlocks fb, uint64_t seed,
+                                double *W, double *b) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n_norm = F * D;
   const double two_pi = 6.283185307179586476925286766559;
@@ -51,8 +59,8 @@ __global__ void features_kernel(int32_t D, int64_t F, double sigma, uint64_t see
       const double th = two_pi * u2;
       double sn, cs;
       sincos(th, &sn, &cs);
-      W[m0] = sigma * (rad * cs);
-      if (m0 + 1 < n_norm) W[m0 + 1] = sigma * (rad * sn);
+      W[m0] = block_sigma(fb, m0 / D) * (rad * cs);
+      if (m0 + 1 < n_norm) W[m0 + 1] = block_sigma(fb, (m0 + 1) / D) * (rad * sn);
     }
   }
   if (4 * t < F) {
@@ -64,11 +72,11 @@ __global__ void features_kernel(int32_t D, int64_t F, double sigma, uint64_t see
   }
 }
 
-cudaError_t launch_features(int32_t dim, int64_t F, double sigma, uint64_t seed, double *W,
+cudaError_t launch_features(int32_t dim, int64_t F, const FeatBlocks &fb, uint64_t seed, double *W,
                             double *b, cudaStream_t st) {
   const int64_t n_norm = F * dim;
   const int64_t blocks4 = (((n_norm > F ? n_norm : F) + 3) / 4 + 255) / 256;
-  features_kernel<<<(unsigned)blocks4, 256, 0, st>>>(dim, F, sigma, seed, W, b);
+  features_kernel<<<(unsigned)blocks4, 256, 0, st>>>(dim, F, fb, seed, W, b);
   return cudaGetLastError();
 }
 
@@ -215,19 +223,19 @@ cudaError_t launch_eval(int D, const EvalArgs &a, cudaStream_t st) {
 // ------------------------------------------------------------------------------------------
 // solve helpers
 // ------------------------------------------------------------------------------------------
-// rows [row0, row0 + F) of columns 0..F of the column-major [A | b]: [sqrt_mu I | 0]
-__global__ void ridge_fill_kernel(double *Ab, int64_t lda, int64_t row0, int64_t F, double sq) {
+// rows [row0, row0 + F) of columns 0..ncols-1 of a column-major buffer: [sqrt_mu I | 0]
+__global__ void ridge_fill_kernel(double *Ab, int64_t lda, int64_t row0, int64_t F, int64_t ncols,
+                                  double sq) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n = F * (F + 1);
-  if (idx >= n) return;
+  if (idx >= F * ncols) return;
   const int64_t col = idx / F, i = idx % F;
   Ab[col * lda + row0 + i] = (col == i) ? sq : 0.0;
 }
 
-cudaError_t launch_ridge_fill(double *Ab, int64_t lda, int64_t row0, int64_t F, double sqrt_mu,
-                              cudaStream_t st) {
-  const int64_t n = F * (F + 1);
-  ridge_fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Ab, lda, row0, F, sqrt_mu);
+cudaError_t launch_ridge_fill(double *Ab, int64_t lda, int64_t row0, int64_t F, int64_t ncols,
+                              double sqrt_mu, cudaStream_t st) {
+  const int64_t n = F * ncols;
+  ridge_fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Ab, lda, row0, F, ncols, sqrt_mu);
   return cudaGetLastError();
 }
 

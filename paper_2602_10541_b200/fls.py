@@ -26,7 +26,7 @@ Term = Tuple[Sequence[int], float, int]   # (alpha, coef, field)
 
 __all__ = ["Context", "Block", "fls_features", "fls_assemble", "fls_solve", "fls_qr_r",
            "fls_frob2", "fls_eval", "fls_sync", "fls_ctx_timing", "fls_ctx_timing_read",
-           "fls_assemble_host", "HostBlockSet", "BlockSet", "FlsError", "FLS_COL_MAJOR", "FLS_ROW_MAJOR",
+           "fls_assemble_host", "HostBlockSet", "BlockSet", "fls_features_blocks", "QRFactor", "FlsError", "FLS_COL_MAJOR", "FLS_ROW_MAJOR",
            "round_up"]
 
 
@@ -127,6 +127,61 @@ def fls_features(ctx: Context, dim: int, n_features: int, sigma: float, seed: in
     check(_abi.load().fls_features(ctx.handle, int(dim), int(n_features), float(sigma),
                                    C.c_uint64(int(seed) & (2**64 - 1)), _ptr(W), _ptr(b)))
     return W, b
+
+
+def fls_features_blocks(ctx: Context, dim: int, block_features: Sequence[int],
+                        sigmas: Sequence[float], seed: int):
+    """multi-block basis: block q = block_features[q] features with bandwidth sigmas[q]"""
+    nb = len(block_features)
+    F = int(sum(block_features))
+    dev = torch.device("cuda", ctx.device)
+    W = torch.empty((F, dim), dtype=torch.float64, device=dev)
+    b = torch.empty((F,), dtype=torch.float64, device=dev)
+    cnt = (C.c_int64 * nb)(*[int(v) for v in block_features])
+    sig = (C.c_double * nb)(*[float(v) for v in sigmas])
+    check(_abi.load().fls_features_blocks(ctx.handle, int(dim), nb, cnt, sig,
+                                          C.c_uint64(int(seed) & (2**64 - 1)), _ptr(W), _ptr(b)))
+    return W, b
+
+
+class QRFactor:
+    """cached Householder factorisation of A (App. I matrix caching):
+    factor once, then solve() any number of right-hand sides"""
+
+    def __init__(self, ctx: Context, A: torch.Tensor, n_rows: int, lda: int, n_features: int,
+                 sqrt_mu: float = 0.0):
+        _dev_f64(A, "A")
+        self.ctx = ctx
+        self.n_rows, self.n_features = int(n_rows), int(n_features)
+        h = C.c_void_p()
+        check(_abi.load().fls_qr_factor(ctx.handle, _ptr(A), self.n_rows, int(lda), self.n_features,
+                                        float(sqrt_mu), C.byref(h)))
+        self.handle = h
+
+    def solve(self, B: torch.Tensor, ldb: Optional[int] = None) -> torch.Tensor:
+        """B: (n_rows,) or flat column-major (n_rows x nrhs, ldb); returns (n_features,) or
+        (nrhs, n_features) rows = solutions"""
+        _dev_f64(B, "B")
+        if B.dim() == 1 and ldb is None:
+            nrhs, ldb = 1, self.n_rows
+        else:
+            ldb = self.n_rows if ldb is None else int(ldb)
+            nrhs = B.numel() // ldb
+        Beta = torch.empty((nrhs, self.n_features), dtype=torch.float64, device=B.device)
+        check(_abi.load().fls_qr_solve(self.ctx.handle, self.handle, _ptr(B), ldb, nrhs, _ptr(Beta),
+                                       self.n_features))
+        return Beta[0] if (B.dim() == 1 and nrhs == 1) else Beta
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _abi.load().fls_qr_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class BlockSet:

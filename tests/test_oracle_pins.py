@@ -74,6 +74,25 @@ def test_features_deterministic_and_distribution():
     assert np.array_equal(W5[:, 0], W6[:7, 0])
 
 
+def test_features_blocks_pins():
+    """pins: one block == orc_features (same streams); per-block W ~ N(0, sigma_q^2)
+    (KS test per block, P:L85 multi-block bandwidths); b identical to the one-block draw."""
+    W1, b1 = oracle.features(2, 3000, 1.7, seed=4)
+    Wb, bb = oracle.features_blocks(2, [3000], [1.7], seed=4)
+    assert np.array_equal(W1, Wb) and np.array_equal(b1, bb)
+    counts, sig = [20000, 5, 30000], [0.5, 3.0, 8.0]
+    W, b = oracle.features_blocks(3, counts, sig, seed=9)
+    Wu, bu = oracle.features(3, sum(counts), 1.0, seed=9)
+    assert np.array_equal(b, bu)
+    off = 0
+    for n, s in zip(counts, sig):
+        blk = W[off:off + n]
+        assert np.array_equal(blk, s * Wu[off:off + n])      # same normals, scaled by sigma_q
+        if n > 100:
+            assert stats.kstest(blk.ravel() / s, "norm").pvalue > 1e-4
+        off += n
+
+
 def test_kernel_limit_has_factor_half():
     """pin: random-Fourier-feature law (Rahimi & Recht, cited P:L83): for W ~ N(0, sigma^2 I),
     b ~ U[0,2pi), E[sin(Wx+b) sin(Wx'+b)] = 1/2 exp(-sigma^2 |x-x'|^2 / 2).  The paper's P:L83

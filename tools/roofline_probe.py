@@ -59,6 +59,23 @@ def main():
         out[f"{name}_dmma_fma_per_s"] = res.value * 256
         out[f"{name}_dfma_per_s"] = r2.value
         out[f"{name}_status"] = st
+    # power split: each probe run back to back for ~4 s with clocks / power sampled
+    if os.environ.get("FLS_POWER_PROBE", "1") == "1":
+        import time as _t
+        for name, call in [
+            ("power_store", lambda: lib.mb_tile_store_bw(C.c_void_p(A.data_ptr()), C.c_int64(1 << 20),
+                                                         C.c_int64(1 << 20), 8192, 10, C.byref(res))),
+            ("power_alu", lambda: lib.mb_entry_rate(C.c_void_p(scratch.data_ptr()), 400_000, C.byref(res))),
+        ]:
+            clk = ClockSampler(0)
+            clk.start()
+            t0 = _t.time()
+            rates = []
+            while _t.time() - t0 < 4.0:
+                call()
+                torch.cuda.synchronize()
+                rates.append(res.value)
+            out[name] = {"rate": sum(rates) / len(rates), "clocks": clk.stop()}
     mhz = out["dfma_per_s_clocks"]["sm_mhz"]
     if mhz:
         out["dfma_per_clk_per_sm"] = out["dfma_per_s"] / (mhz * 1e6) / torch.cuda.get_device_properties(0).multi_processor_count
