@@ -219,6 +219,34 @@ FLS_API fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t l
                      double sqrt_mu, double *beta, double *resid_norm);
 
 /* ---------------------------------------------------------------------------------------- */
+/* Newton-Raphson support (Eq. 4-5): nonlinear PDE  L[u] + N(u) = f  with a      */
+/* pointwise nonlinearity N.  The Jacobian  J_ij = L[phi_j](x_i) + N'(u(x_i)) s phi_j(x_i)  */
+/* is fls_assemble with one extra identity term whose coefficient field is          */
+/* dN = N'(u); this call produces that field and the Newton right-hand side.                 */
+/*   kind FLS_NL_POLY: N(u) = sum_{k=0}^{degree} a[k] u^k  (u^3, Allen-Cahn, ...)             */
+/*   kind FLS_NL_EXP:  N(u) = a[0] exp(a[1] u)            (Bratu: a = {lambda, 1})            */
+/* For i < n:  neg_res_i = f_i - Lu_i - N(u_i)   (= -R_i, the rhs of J delta = -R),           */
+/*             dN_i = N'(u_i)  (dN may be NULL).                                               */
+/* stats (host, optional, blocking when given): {sum neg_res^2, sum u^2, sum (u - u_prev)^2}  */
+/* (u_prev may be NULL -> third entry 0), a fixed-order deterministic reduction.              */
+/* All arrays are device vectors of n doubles.                                                 */
+/* ---------------------------------------------------------------------------------------- */
+#define FLS_NL_POLY 1
+#define FLS_NL_EXP 2
+typedef struct {
+    int32_t kind;     /* FLS_NL_POLY | FLS_NL_EXP */
+    int32_t degree;   /* POLY: 0..7 */
+    double a[8];
+} fls_nonlinearity;
+FLS_API fls_status fls_nl_residual(fls_ctx *ctx, const fls_nonlinearity *nl, int64_t n,
+                                   const double *Lu, const double *u, const double *u_prev,
+                                   const double *f, double *neg_res, double *dN, double *stats);
+/* out_i = y_i + alpha * x_i for i < n (the Newton update beta + alpha delta, Eq. 4).
+ * Device vectors; out may alias y or x.  Asynchronous. */
+FLS_API fls_status fls_axpy(fls_ctx *ctx, int64_t n, double alpha, const double *x,
+                            const double *y, double *out);
+
+/* ---------------------------------------------------------------------------------------- */
 /* Cached / prefactored solves (App. I "Matrix caching": factor A once, then     */
 /* every new right-hand side costs a cached apply; inverse problems P:L395-397).             */
 /* fls_qr_factor copies the column-major A (n_rows x n_features, lda) into ctx-independent   */

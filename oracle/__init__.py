@@ -57,7 +57,9 @@ def lib():
                                    C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_lstsq.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_double,
                                 C.c_void_p, C.c_void_p, C.c_void_p]
-        L.orc_eval.argtypes = [C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
+        L.orc_lstsq_mu.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_double,
+                                   C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_eval.argtypes =[C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
                                C.c_void_p, C.c_int64, C.c_void_p]
         L.orc_max_threads.restype = C.c_int
     return _lib
@@ -183,6 +185,20 @@ def lstsq(A, bvec, ridge_rel: float = 0.0):
         raise MemoryError("orc_lstsq allocation failed")
     if st != 0:
         raise np.linalg.LinAlgError(f"orc_lstsq status {st} (zero diagonal in R)")
+    return beta, float(res[0]), rd
+
+
+def lstsq_mu(A, bvec, sqrt_mu: float):
+    """argmin ||A beta - b||^2 + mu ||beta||^2 with an absolute sqrt(mu) (Newton step)"""
+    A = _f64(A)
+    bvec = _f64(bvec)
+    m, n = A.shape
+    beta = np.zeros(n)
+    res = np.zeros(1)
+    rd = np.zeros(n)
+    st = lib().orc_lstsq_mu(_p(A), m, n, _p(bvec), float(sqrt_mu), _p(beta), _p(res), _p(rd))
+    if st != 0:
+        raise np.linalg.LinAlgError(f"orc_lstsq_mu status {st}")
     return beta, float(res[0]), rd
 
 

@@ -267,13 +267,26 @@ static void house(const double *x, int64_t len, double *v, double *beta_out, dou
  * R_diag_out (optional): the n diagonal entries of R.
  * Returns 0, -1 on a zero diagonal of R (rank deficiency with mu = 0), -3 on allocation failure.
  */
+static int lstsq_core(const double *A, int64_t m, int64_t n, const double *bvec, double sqmu,
+                      double *beta_out, double *resid_out, double *R_diag_out);
+
 int orc_lstsq(const double *A, int64_t m, int64_t n, const double *bvec, double ridge_rel,
               double *beta_out, double *resid_out, double *R_diag_out) {
     double fro = 0.0;
     for (int64_t i = 0; i < m * n; ++i) fro = fro + A[i] * A[i];
     fro = sqrt(fro);
-    double sqmu = ridge_rel * fro;
-    int64_t ma = m + ((ridge_rel > 0.0) ? n : 0);
+    return lstsq_core(A, m, n, bvec, ridge_rel * fro, beta_out, resid_out, R_diag_out);
+}
+
+/* the same with an absolute sqrt(mu) (the Newton-step Tikhonov term, mu = 1e-10 P:L189) */
+int orc_lstsq_mu(const double *A, int64_t m, int64_t n, const double *bvec, double sqrt_mu,
+                 double *beta_out, double *resid_out, double *R_diag_out) {
+    return lstsq_core(A, m, n, bvec, sqrt_mu, beta_out, resid_out, R_diag_out);
+}
+
+static int lstsq_core(const double *A, int64_t m, int64_t n, const double *bvec, double sqmu,
+                      double *beta_out, double *resid_out, double *R_diag_out) {
+    int64_t ma = m + ((sqmu > 0.0) ? n : 0);
     int64_t nc = n + 1;
     double *M = (double *)calloc((size_t)(ma * nc), sizeof(double));
     double *v = (double *)malloc((size_t)ma * sizeof(double));

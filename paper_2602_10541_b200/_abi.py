@@ -46,6 +46,14 @@ class fls_block(C.Structure):
                 ("values", C.c_void_p)]
 
 
+FLS_NL_POLY = 1
+FLS_NL_EXP = 2
+
+
+class fls_nonlinearity(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("degree", C.c_int32), ("a", C.c_double * 8)]
+
+
 _SIGS = {
     "fls_last_error": (C.c_char_p, []),
     "fls_status_string": (C.c_char_p, [C.c_int]),
@@ -68,6 +76,10 @@ _SIGS = {
     "fls_qr_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
                                C.c_int64]),
     "fls_qr_destroy": (C.c_int, [C.c_void_p]),
+    "fls_nl_residual": (C.c_int, [C.c_void_p, C.POINTER(fls_nonlinearity), C.c_int64, C.c_void_p,
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_void_p]),
+    "fls_axpy": (C.c_int, [C.c_void_p, C.c_int64, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     "fls_assemble_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64,
                                     C.c_int32, C.POINTER(fls_block), C.c_int32, C.c_int64,
                                     C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]),

@@ -821,6 +821,56 @@ fls_status fls_qr_r(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda, int64_
   return FLS_OK;
 }
 
+fls_status fls_nl_residual(fls_ctx *ctx, const fls_nonlinearity *nl, int64_t n, const double *Lu,
+                           const double *u, const double *u_prev, const double *f,
+                           double *neg_res, double *dN, double *stats) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!nl) return fail(FLS_EINVAL, "nl is NULL");
+  if (nl->kind != FLS_NL_POLY && nl->kind != FLS_NL_EXP)
+    return fail(FLS_EINVAL, "nonlinearity kind %d unknown", nl->kind);
+  if (nl->kind == FLS_NL_POLY && (nl->degree < 0 || nl->degree > 7))
+    return fail(FLS_EINVAL, "polynomial degree %d not in 0..7", nl->degree);
+  for (int k = 0; k < 8; ++k)
+    if (!std::isfinite(nl->a[k])) return fail(FLS_EINVAL, "nonlinearity coefficient %d not finite", k);
+  if (n < 0) return fail(FLS_EINVAL, "n < 0");
+  if (n > 0 && (!Lu || !u || !f || !neg_res)) return fail(FLS_EINVAL, "NULL vector");
+  DeviceGuard g(ctx->device);
+  NlArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.kind = nl->kind;
+  a.degree = nl->kind == FLS_NL_POLY ? nl->degree : 1;
+  for (int k = 0; k < 8; ++k) a.c[k] = nl->a[k];
+  a.n = n;
+  a.Lu = Lu;
+  a.u = u;
+  a.u_prev = u_prev;
+  a.f = f;
+  a.neg_res = neg_res;
+  a.dN = dN;
+  a.partials = ctx->d_scratch + 8;
+  a.err = ctx->d_err;
+  const int nblk = 296;  // 2 x 148 SMs, fixed -> deterministic sums
+  cudaError_t e = launch_nl_residual(a, nblk, ctx->d_scratch, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "nl_residual");
+  if (stats) {
+    FLS_CUDA(cudaMemcpyAsync(stats, ctx->d_scratch, 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    FLS_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return FLS_OK;
+}
+
+fls_status fls_axpy(fls_ctx *ctx, int64_t n, double alpha, const double *x, const double *y,
+                    double *out) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (n < 0 || !std::isfinite(alpha)) return fail(FLS_EINVAL, "bad n or alpha");
+  if (n > 0 && (!x || !y || !out)) return fail(FLS_EINVAL, "NULL vector");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_axpy(n, alpha, x, y, out, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "axpy");
+  return FLS_OK;
+}
+
 fls_status fls_frob2(fls_ctx *ctx, const double *A, int64_t n_rows, int64_t lda, int64_t n_cols,
                      double *out) {
   if (fls_status s = check_ctx(ctx)) return s;

@@ -111,6 +111,17 @@ cudaError_t launch_copy_upper(const double *M, int64_t lda, int64_t k, int64_t n
                               int64_t ldr, cudaStream_t st);
 cudaError_t launch_min_abs_diag(const double *M, int64_t lda, int64_t n, double *out,
                                 cudaStream_t st);
+struct NlArgs {
+  int32_t kind, degree;
+  double c[8];
+  int64_t n;
+  const double *Lu, *u, *u_prev, *f;
+  double *neg_res, *dN, *partials;
+  unsigned *err;
+};
+cudaError_t launch_nl_residual(const NlArgs &a, int nblk, double *stats, cudaStream_t st);
+cudaError_t launch_axpy(int64_t n, double alpha, const double *x, const double *y, double *out,
+                        cudaStream_t st);
 cudaError_t launch_frob2(const double *A, int64_t lda, int64_t m, int64_t n, double *partials,
                          int nblk, double *out, cudaStream_t st);
 

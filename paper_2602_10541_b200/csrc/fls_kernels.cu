@@ -311,4 +311,86 @@ cudaError_t launch_frob2(const double *A, int64_t lda, int64_t m, int64_t n, dou
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------------------
+// Newton support: pointwise nonlinearity, Newton rhs and N'(u) field, plus the
+// three sums of squares, as per-block partials (fixed grid -> deterministic order).
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void nl_eval(const NlArgs &a, double u, double &N, double &dN) {
+  if (a.kind == 2) {  // a0 exp(a1 u)
+    const double e = exp(a.c[1] * u);
+    N = a.c[0] * e;
+    dN = a.c[0] * a.c[1] * e;
+  } else {            // sum_k a_k u^k (Horner)
+    double p = a.c[a.degree], q = 0.0;
+    for (int k = a.degree - 1; k >= 0; --k) {
+      q = fma(q, u, p);
+      p = fma(p, u, a.c[k]);
+    }
+    N = p;
+    dN = q;
+  }
+}
+
+__global__ void nl_residual_kernel(const NlArgs a) {
+  __shared__ double sm[3][256];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double u = a.u[i];
+    double N, dN;
+    nl_eval(a, u, N, dN);
+    const double r = a.f[i] - a.Lu[i] - N;
+    bad |= !finite(r) || !finite(dN);
+    a.neg_res[i] = r;
+    if (a.dN) a.dN[i] = dN;
+    s0 = fma(r, r, s0);
+    s1 = fma(u, u, s1);
+    if (a.u_prev) {
+      const double du = u - a.u_prev[i];
+      s2 = fma(du, du, s2);
+    }
+  }
+  if (bad) atomicOr(a.err, 1u);
+  sm[0][threadIdx.x] = s0;
+  sm[1][threadIdx.x] = s1;
+  sm[2][threadIdx.x] = s2;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int k = 0; k < 3; ++k) sm[k][threadIdx.x] += sm[k][threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 3; ++k) a.partials[3 * blockIdx.x + k] = sm[k][0];
+}
+
+__global__ void nl_stats_final_kernel(const double *partials, int nblk, double *out) {
+  if (threadIdx.x < 3) {
+    double s = 0.0;
+    for (int i = 0; i < nblk; ++i) s += partials[3 * i + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+}
+
+cudaError_t launch_nl_residual(const NlArgs &a, int nblk, double *stats, cudaStream_t st) {
+  nl_residual_kernel<<<nblk, 256, 0, st>>>(a);
+  nl_stats_final_kernel<<<1, 32, 0, st>>>(a.partials, nblk, stats);
+  return cudaGetLastError();
+}
+
+__global__ void axpy_kernel(int64_t n, double alpha, const double *x, const double *y, double *out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = fma(alpha, x[i], y[i]);
+}
+
+cudaError_t launch_axpy(int64_t n, double alpha, const double *x, const double *y, double *out,
+                        cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  const int64_t nb = (n + 255) / 256;
+  axpy_kernel<<<(unsigned)(nb < 4096 ? nb : 4096), 256, 0, st>>>(n, alpha, x, y, out);
+  return cudaGetLastError();
+}
+
 }  // namespace fls

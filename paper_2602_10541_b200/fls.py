@@ -26,7 +26,8 @@ Term = Tuple[Sequence[int], float, int]   # (alpha, coef, field)
 
 __all__ = ["Context", "Block", "fls_features", "fls_assemble", "fls_solve", "fls_qr_r",
            "fls_frob2", "fls_eval", "fls_sync", "fls_ctx_timing", "fls_ctx_timing_read",
-           "fls_assemble_host", "HostBlockSet", "BlockSet", "fls_features_blocks", "QRFactor", "FlsError", "FLS_COL_MAJOR", "FLS_ROW_MAJOR",
+           "fls_assemble_host", "HostBlockSet", "BlockSet", "fls_features_blocks", "QRFactor",
+           "make_nonlinearity", "fls_nl_residual", "fls_axpy", "FlsError", "FLS_COL_MAJOR", "FLS_ROW_MAJOR",
            "round_up"]
 
 
@@ -142,6 +143,42 @@ def fls_features_blocks(ctx: Context, dim: int, block_features: Sequence[int],
     check(_abi.load().fls_features_blocks(ctx.handle, int(dim), nb, cnt, sig,
                                           C.c_uint64(int(seed) & (2**64 - 1)), _ptr(W), _ptr(b)))
     return W, b
+
+
+def make_nonlinearity(kind: str, coefs: Sequence[float]):
+    """'poly': N(u) = sum_k coefs[k] u^k;  'exp': N(u) = coefs[0] exp(coefs[1] u)"""
+    nl = _abi.fls_nonlinearity()
+    if kind == "poly":
+        nl.kind = _abi.FLS_NL_POLY
+        nl.degree = len(coefs) - 1
+    elif kind == "exp":
+        nl.kind = _abi.FLS_NL_EXP
+        nl.degree = 1
+    else:
+        raise ValueError(kind)
+    for k, v in enumerate(coefs):
+        nl.a[k] = float(v)
+    return nl
+
+
+def fls_nl_residual(ctx: Context, nl, Lu: torch.Tensor, u: torch.Tensor, f: torch.Tensor,
+                    u_prev: Optional[torch.Tensor] = None, neg_res: Optional[torch.Tensor] = None,
+                    dN: Optional[torch.Tensor] = None, stats: bool = True):
+    """neg_res = f - Lu - N(u), dN = N'(u); returns (neg_res, dN, (sum r^2, sum u^2, sum du^2))"""
+    n = int(u.numel())
+    neg_res = torch.empty_like(u) if neg_res is None else neg_res
+    dN = torch.empty_like(u) if dN is None else dN
+    st = (C.c_double * 3)()
+    check(_abi.load().fls_nl_residual(ctx.handle, C.byref(nl), n, _ptr(Lu), _ptr(u), _ptr(u_prev),
+                                      _ptr(f), _ptr(neg_res), _ptr(dN), st if stats else None))
+    return neg_res, dN, (st[0], st[1], st[2])
+
+
+def fls_axpy(ctx: Context, alpha: float, x: torch.Tensor, y: torch.Tensor,
+             out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    out = torch.empty_like(y) if out is None else out
+    check(_abi.load().fls_axpy(ctx.handle, int(y.numel()), float(alpha), _ptr(x), _ptr(y), _ptr(out)))
+    return out
 
 
 class QRFactor:

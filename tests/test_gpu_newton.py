@@ -1,0 +1,61 @@
+"""GPU Newton-Raphson (paper_2602_10541_b200.newton over libfls) vs the oracle Newton
+(oracle/newton.py), same algorithm and parameters: fitted u at held-out points within 1e-6,
+pointwise residual / N' kernel against numpy."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import oracle.newton as on
+import workloads as wl
+from gpu_common import U_TOL, dev_blocks
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2602_10541_b200 import fls
+    from paper_2602_10541_b200.newton import solve_nonlinear
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return fls.Context()
+
+
+@pytest.mark.parametrize("spec", [("poly", [0.3, -1.0, 0.5, 1.0]), ("exp", [-1.0, 1.0])])
+def test_nl_residual_kernel(ctx, spec):
+    g = np.random.default_rng(1)
+    n = 10_007
+    u, Lu, f, up = (g.normal(size=n) for _ in range(4))
+    N, dN = on.nl_funcs(*spec)
+    T = [torch.from_numpy(v).cuda() for v in (u, Lu, f, up)]
+    neg, dn, st = fls.fls_nl_residual(ctx, fls.make_nonlinearity(*spec), T[1], T[0], T[2], u_prev=T[3])
+    ref = f - Lu - N(u)
+    assert np.allclose(neg.cpu().numpy(), ref, rtol=1e-13, atol=1e-13 * np.abs(ref).max())
+    assert np.allclose(dn.cpu().numpy(), dN(u), rtol=1e-13, atol=1e-13)
+    assert abs(st[0] - (ref @ ref)) <= 1e-11 * (ref @ ref)
+    assert abs(st[1] - (u @ u)) <= 1e-12 * (u @ u)
+    assert abs(st[2] - ((u - up) @ (u - up))) <= 1e-12 * ((u - up) @ (u - up))
+    out = fls.fls_axpy(ctx, 0.37, T[0], T[1]).cpu().numpy()
+    assert np.allclose(out, Lu + 0.37 * u, rtol=1e-15, atol=1e-15)
+
+
+@pytest.mark.parametrize("name", wl.NL_NAMES)
+def test_newton_parity_with_oracle(ctx, name):
+    p = wl.make_nl_problem(name)
+    W, b = p.parity_features()
+    Wd, bd = torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda()
+    blocks = dev_blocks(p)
+    beta, hist = solve_nonlinear(ctx, Wd, bd, blocks[0], blocks[1:], *p.nl, max_iter=10, tol=1e-8)
+    beta_o, hist_o = on.newton(W, b, p.blocks[0], p.blocks[1:], p.nl, max_iter=10, tol=1e-8)
+    Xt = p.test_points(2000)
+    u_gpu = fls.fls_eval(ctx, Wd, bd, beta, torch.from_numpy(Xt).cuda()).cpu().numpy()
+    u_orc = oracle.evaluate(W, b, beta_o, Xt)
+    assert np.linalg.norm(u_gpu - u_orc) / np.linalg.norm(u_orc) <= U_TOL
+    assert abs(len(hist) - len(hist_o)) <= 1
+    for h, ho in zip(hist[:3], hist_o[:3]):                 # same residual trajectory early on
+        assert abs(h["resid"] - ho["resid"]) <= 1e-6 * ho["resid"] + 1e-9
+    us = p.u_star(Xt)
+    assert np.linalg.norm(u_gpu - us) / np.linalg.norm(us) < 1e-6

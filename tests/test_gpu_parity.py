@@ -348,6 +348,25 @@ def test_features_blocks_match_oracle(ctx):
     assert torch.equal(W1, Wb) and torch.equal(b1, bb)
 
 
+def _alt_rhs(p):
+    """rhs [f; lam g; ...] of a second manufactured solution u2 on the same points (closed forms)"""
+    pi = math.pi
+    out = []
+    for blk in p.blocks:
+        X = blk.X
+        if p.name == "c2_poisson2d":          # u2 = cos(pi x) y^2 + x, -Lap u2 = pi^2 cos(pi x) y^2 - 2 cos(pi x)
+            u2 = np.cos(pi * X[:, 0]) * X[:, 1] ** 2 + X[:, 0]
+            f2 = pi ** 2 * np.cos(pi * X[:, 0]) * X[:, 1] ** 2 - 2 * np.cos(pi * X[:, 0])
+        elif p.name == "c4_heat2d":           # u2 = e^{-2t} sin(2 pi x) sin(pi y)
+            u2 = np.exp(-2 * X[:, 2]) * np.sin(2 * pi * X[:, 0]) * np.sin(pi * X[:, 1])
+            f2 = (-2 + 0.1 * 5 * pi ** 2) * u2
+        else:                                 # c5: u2 = sin(2 pi x) sin(pi y) sin(pi z)
+            u2 = np.sin(2 * pi * X[:, 0]) * np.sin(pi * X[:, 1]) * np.sin(pi * X[:, 2])
+            f2 = (36 * pi ** 4 + 16 * (1 + X[:, 0])) * u2
+        out.append(blk.weight * (f2 if blk.name == "pde" else u2))
+    return np.concatenate(out)
+
+
 @pytest.mark.parametrize("name,size", [("c2_poisson2d", "full"), ("c4_heat2d", "mini"),
                                        ("c5_biharm3d", "mini")])
 def test_cached_qr_many_rhs(ctx, name, size):
@@ -359,9 +378,11 @@ def test_cached_qr_many_rhs(ctx, name, size):
     Ab, lda = fls.fls_assemble(ctx, Wd, bd, dev_blocks(p))
     sq = p.ridge_rel * math.sqrt(fls.fls_frob2(ctx, Ab, R, lda, F)) if p.ridge_rel > 0 else 0.0
     qr = fls.QRFactor(ctx, Ab, R, lda, F, sq)
-    g = np.random.default_rng(5)
     rhs0 = Ab[F * lda: F * lda + R].cpu().numpy()
-    B = np.stack([rhs0, g.normal(size=R), rhs0 * 2.0 + g.normal(size=R) * 1e-3], axis=1)  # (R, 3)
+    rhs1 = _alt_rhs(p)
+    # well-posed right-hand sides only (manufactured solutions): with a numerically rank-deficient
+    # A the fitted u of an arbitrary rhs is not unique across QR variants
+    B = np.stack([rhs0, rhs1, 2.0 * rhs0 - 0.5 * rhs1], axis=1)                         # (R, 3)
     Bd = torch.from_numpy(np.ascontiguousarray(B.T)).cuda().reshape(-1)                 # col-major
     Beta = qr.solve(Bd, ldb=R)
     Xt = p.test_points(10_000)

@@ -267,6 +267,47 @@ def make_problem(name: str, size: str = "full", seed: int = 0, **override) -> Pr
     raise KeyError(name)
 
 
+# --------------------------------------------------------------------------------------
+# nonlinear problems for the Newton path.  L[u] + N(u) = f with a
+# pointwise N, Dirichlet rows weighted by lambda = 100.  The paper's own nonlinear
+# benchmarks (Table 2) state no manufactured solutions; these are synthetic stand-ins of the
+# same form (NL-Poisson u^3 term, Bratu exponential term).
+# --------------------------------------------------------------------------------------
+def _u_nl(X):
+    x, y = X[:, 0], X[:, 1]
+    return np.sin(PI * x) * np.sin(PI * y) + x * y
+
+
+def _u_bratu(X):
+    return np.sin(PI * X[:, 0]) * np.sin(PI * X[:, 1])
+
+
+NL_NAMES = ["nl_poisson2d", "bratu2d"]
+
+
+def make_nl_problem(name: str, n_int: int = 1500, per_edge: int = 100, n_features: int = 400,
+                    sigma: float = 3.0, seed: int = 0) -> Problem:
+    gi, gb = rng(seed, STREAM_INTERIOR), rng(seed, STREAM_BOUNDARY)
+    lo, hi = np.zeros(2), np.ones(2)
+    Xi = _uniform_box(gi, n_int, lo, hi)
+    Xb = _faces(gb, 2, per_edge, lo, hi, axes=[1, 0])
+    if name == "nl_poisson2d":         # -Lap u + u^3 = f
+        u = _u_nl
+        f = 2 * PI * PI * np.sin(PI * Xi[:, 0]) * np.sin(PI * Xi[:, 1]) + u(Xi) ** 3
+        nl = ("poly", [0.0, 0.0, 0.0, 1.0])
+    elif name == "bratu2d":            # -Lap u - e^u = f  (Bratu, lambda = 1)
+        u = _u_bratu
+        f = 2 * PI * PI * u(Xi) - np.exp(u(Xi))
+        nl = ("exp", [-1.0, 1.0])
+    else:
+        raise KeyError(name)
+    blocks = [Block("pde", _c(Xi), op_laplacian(2, -1.0), 1.0, _c(f)),
+              Block("bc", _c(Xb), op_identity(2), 100.0, _c(u(Xb)))]
+    p = Problem(name, 2, n_features, sigma, blocks, u, lo, hi, 0.0, seed)
+    p.nl = nl
+    return p
+
+
 def sample_rows(n_rows: int, n_shards: int = 8, stride: int = 256) -> np.ndarray:
     """Deterministic sampled global rows: every stride-th row plus the first and last
     row of every shard of an n_shards-way split."""
