@@ -65,6 +65,8 @@ def main():
         for name, call in [
             ("power_store", lambda: lib.mb_tile_store_bw(C.c_void_p(A.data_ptr()), C.c_int64(1 << 20),
                                                          C.c_int64(1 << 20), 8192, 10, C.byref(res))),
+            ("power_chunk_store", lambda: lib.mb_chunk_store_bw(C.c_void_p(A.data_ptr()), C.c_int64(n), 20,
+                                                                C.byref(res))),
             ("power_alu", lambda: lib.mb_entry_rate(C.c_void_p(scratch.data_ptr()), 400_000, C.byref(res))),
         ]:
             clk = ClockSampler(0)
