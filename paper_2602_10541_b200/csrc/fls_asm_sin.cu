@@ -5,18 +5,11 @@
 namespace fls {
 
 template <int D, int G>
-static cudaError_t go_sin(const AsmArgs &a, cudaStream_t st) {
+static cudaError_t go_sin(const AsmArgs &a0, cudaStream_t st) {
   constexpr int S = pf_stride(D, G, KM_SIN);
   const size_t smem = (size_t)kFC * S * sizeof(double);
-  const int64_t span = a.lr1 - (a.lr0 & ~int64_t(1));
-  // grid.y = feature groups: enough CTAs for ~16 waves of 4 CTAs x 148 SMs, while each
-  // CTA re-uses its rows' x_i across as many 128-feature chunks as possible
-  const int64_t row_tiles = (span + kRowsCTA - 1) / kRowsCTA;
-  const int64_t n_chunks = (a.F + kFC - 1) / kFC;
-  int64_t groups = (16 * 4 * 148 + row_tiles - 1) / row_tiles;
-  groups = groups < 1 ? 1 : (groups > n_chunks ? n_chunks : groups);
-  groups = (n_chunks + ((n_chunks + groups - 1) / groups) - 1) / ((n_chunks + groups - 1) / groups);
-  const dim3 grid((unsigned)row_tiles, (unsigned)groups);
+  AsmArgs a = a0;
+  const dim3 grid = asm_grid<D, G, KM_SIN>(a);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(assemble_cm_kernel<D, G, KM_SIN>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

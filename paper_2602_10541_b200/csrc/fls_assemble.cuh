@@ -72,6 +72,43 @@ constexpr int asm_min_blocks() {
   return (KM == KM_SIN && D + G <= 5) ? FLS_MINB : 2;
 }
 
+// Launch shape: grid = (row tiles, feature groups), a.fpc features per CTA.  Picks the fewest
+// feature groups that give >= 8 waves of resident CTAs (148 SMs x asm_min_blocks), then the
+// group count in [g, 2g] whose last wave is fullest.  Each CTA keeps >= 16 features (>= kFC
+// when the block's point data exceed 32 MB and would not stay in L2 between groups).
+template <int D, int G, int KM>
+inline dim3 asm_grid(AsmArgs &a) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int64_t span = a.lr1 - (a.lr0 & ~int64_t(1));
+  const int64_t rt = (span + kRowsCTA - 1) / kRowsCTA;
+  const int64_t resident = (int64_t)sms * asm_min_blocks<D, G, KM>();
+  const bool big_x = span * (D + G + 1) * 8 > ((int64_t)32 << 20);
+  const int64_t min_fpc = big_x ? (a.F < kFC ? a.F : kFC) : (a.F < 16 ? a.F : 16);
+  const int64_t gmax = (a.F + min_fpc - 1) / min_fpc;
+  int64_t g0 = (8 * resident + rt - 1) / rt;
+  g0 = g0 < 1 ? 1 : (g0 > gmax ? gmax : g0);
+  int64_t best = g0;
+  double best_eff = -1.0;
+  for (int64_t g = g0; g <= 2 * g0 && g <= gmax; ++g) {
+    const int64_t fpc = (((a.F + g - 1) / g) + 1) & ~int64_t(1);
+    const int64_t gg = (a.F + fpc - 1) / fpc;
+    const double waves = (double)(rt * gg) / (double)resident;
+    const double eff = waves / ceil(waves);
+    if (eff > best_eff + 1e-3) {
+      best_eff = eff;
+      best = gg;
+    }
+  }
+  a.fpc = (((a.F + best - 1) / best) + 1) & ~int64_t(1);
+  return dim3((unsigned)rt, (unsigned)((a.F + a.fpc - 1) / a.fpc));
+}
+
 template <int D, int G, int KM>
 __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_kernel(const AsmArgs a) {
   using M = EntryMath<D, G, KM>;
@@ -113,14 +150,12 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
   }
   if (bad) atomicOr(a.err, 1u);
 
-  // feature chunks of this CTA's group
-  const int64_t n_chunks = (a.F + kFC - 1) / kFC;
-  const int64_t cpg = (n_chunks + gridDim.y - 1) / gridDim.y;
-  const int64_t c0 = (int64_t)blockIdx.y * cpg;
-  const int64_t c1 = c0 + cpg < n_chunks ? c0 + cpg : n_chunks;
-  for (int64_t ch = c0; ch < c1; ++ch) {
-    const int64_t j0 = ch * kFC;
-    const int nfe = (a.F - j0) < kFC ? (int)(a.F - j0) : kFC;
+  // this CTA's feature range [f0, f1) (a.fpc features per CTA, chosen by the launcher), walked
+  // in shared-memory chunks of at most kFC records
+  const int64_t f0 = (int64_t)blockIdx.y * a.fpc;
+  const int64_t f1 = f0 + a.fpc < a.F ? f0 + a.fpc : a.F;
+  for (int64_t j0 = f0; j0 < f1; j0 += kFC) {
+    const int nfe = (f1 - j0) < kFC ? (int)(f1 - j0) : kFC;
     __syncthreads();  // previous chunk's records no longer in use
     {
       const double2 *src = reinterpret_cast<const double2 *>(a.pf + j0 * S);

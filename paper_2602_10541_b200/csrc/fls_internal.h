@@ -73,6 +73,7 @@ struct AsmArgs {
   unsigned *err;
   int32_t nf;                    // n_fields of the block (row stride of fields)
   int32_t vec;                   // 16-byte vector stores allowed
+  int64_t fpc;                   // features per CTA (set by the launcher)
   int32_t gfield[FLS_MAX_FIELDS];// field id of group g+1
 };
 

@@ -335,6 +335,33 @@ def test_assemble_host_matches_device(ctx, chunk):
         assert np.isnan(A_h.reshape(F + 1, ldh)[:F, n:]).all()     # padding untouched
 
 
+# ------------------------------------------------------------------------------------- full-size solves
+@pytest.mark.parametrize("name", ["c3_poisson5d", "c4_heat2d", "c5_biharm3d"])
+def test_full_size_solve_parity_with_oracle_artifact(ctx, name):
+    """Fitted u at the 10,000 held-out points at BASELINE size (C5: its 262,144-row solve subset)
+    vs tests/golden/oracle_u_<cfg>.npz, written offline by tools/make_oracle_artifacts.py from
+    oracle/ only (Householder QR of the oracle's own term-by-term assembly)."""
+    import os
+    art = os.path.join(os.path.dirname(__file__), "golden", f"oracle_u_{name}.npz")
+    if not os.path.exists(art):
+        pytest.skip(f"no oracle artifact {art}")
+    u_orc = np.load(art)["u_test"]
+    kw = {"n_int": 262_144} if name == "c5_biharm3d" else {}
+    p = wl.make_problem(name, "full", **kw)
+    W, b, Wd, bd = _parity_feats(p)
+    F, R = p.n_features, p.n_rows
+    ridge = p.ridge_rel > 0
+    Ab, lda = fls.fls_assemble(ctx, Wd, bd, dev_blocks(p), extra_rows=F if ridge else 0)
+    sq = p.ridge_rel * math.sqrt(fls.fls_frob2(ctx, Ab, R, lda, F)) if ridge else 0.0
+    beta, _ = fls.fls_solve(ctx, Ab, R, lda, F, sq)
+    del Ab
+    torch.cuda.empty_cache()
+    Xt = p.test_points(10_000)
+    u_gpu = fls.fls_eval(ctx, Wd, bd, beta, torch.from_numpy(Xt).cuda()).cpu().numpy()
+    rel = np.linalg.norm(u_gpu - u_orc) / np.linalg.norm(u_orc)
+    assert rel <= U_TOL, rel
+
+
 # ------------------------------------------------------------------------------------- f3 / f4
 def test_features_blocks_match_oracle(ctx):
     counts, sig = [500, 7, 993], [1.0, 3.0, 12.0]
