@@ -187,7 +187,8 @@ def e2e_measure(args, p, ctx, W, b, a, e, world, local):
             in_bytes_points += 8 * (hi - lo) * per
     hset = fls.HostBlockSet(hblocks, d)
     n_local = e - a
-    ring = min(n_local, args.e2e_ring_rows)
+    # host ring per rank shrinks with the rank count so N ranks pin at most ~17 GB in total
+    ring = min(n_local, max(8192, args.e2e_ring_rows // world))
     A_h = torch.empty((F + 1) * ring, dtype=torch.float64).pin_memory()
     n_calls = (n_local + ring - 1) // ring
 
@@ -300,7 +301,7 @@ def main():
     ap.add_argument("--impl", default="fls", choices=["fls", "reference"])
     ap.add_argument("--workload", default="c5_biharm3d")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
-    ap.add_argument("--ref-rows", type=int, default=64)
+    ap.add_argument("--ref-rows", type=int, default=1024)
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
     ap.add_argument("--no-solve", action="store_true", help="skip the end-to-end solve leg")
     ap.add_argument("--e2e-steps", type=int, default=2)

@@ -46,6 +46,43 @@ class _FlsOps:
         return self.fls.fls_solve(self.ctx, M, n_rows, lda, F, sqrt_mu)
 
 
+def _combine(ops, Rs, ks, F, sqrt_mu, dev):
+    """root step of TSQR: stack the (F+1) x k_r upper-trapezoidal factors, append the ridge rows,
+    QR + trsv (fls_solve)"""
+    nc = F + 1
+    K = sum(ks)
+    ldm = K + (F if sqrt_mu > 0.0 else 0)
+    ldm = ((ldm + 3) // 4) * 4
+    M = torch.zeros((nc * ldm,), dtype=torch.float64, device=dev)
+    Mv = M.view(nc, ldm)
+    off = 0
+    for R, k in zip(Rs, ks):
+        Mv[:, off:off + k] = R[:, :k]
+        off += k
+    return ops.solve(M, K, ldm, F, sqrt_mu)
+
+
+def tsqr_local(blocks, F: int, *, ridge_rel: float = 0.0, ctx=None, ops=None):
+    """TSQR over P row blocks held by ONE process (the 1-GPU test mode of SURVEY §4.5):
+    blocks = [(Ab_r, n_r, lda_r)], each a column-major [A_r | b_r] (destroyed)."""
+    ops = ops if ops is not None else _FlsOps(ctx)
+    dev = blocks[0][0].device
+    nc = F + 1
+    sqrt_mu = 0.0
+    if ridge_rel > 0.0:
+        fro2 = sum(ops.frob2(Ab, n, lda, F) for Ab, n, lda in blocks if n > 0)
+        sqrt_mu = ridge_rel * math.sqrt(fro2)
+    Rs, ks = [], []
+    for Ab, n, lda in blocks:
+        k = min(n, nc)
+        if k == 0:
+            continue
+        R, ldr = ops.qr_r(Ab, n, lda, nc)
+        Rs.append(R[: nc * ldr].view(nc, ldr))
+        ks.append(k)
+    return _combine(ops, Rs, ks, F, sqrt_mu, dev)
+
+
 def tsqr_solve(Ab: torch.Tensor, n_local: int, lda: int, F: int, *, ridge_rel: float = 0.0,
                ctx=None, ops=None, group=None, root: int = 0) -> Tuple[torch.Tensor, float]:
     """beta = argmin ||A beta - b||^2 + mu ||beta||^2 for [A | b] row-sharded over the ranks.
@@ -89,16 +126,7 @@ def tsqr_solve(Ab: torch.Tensor, n_local: int, lda: int, F: int, *, ridge_rel: f
     beta = torch.empty((F,), dtype=torch.float64, device=dev)
     res = 0.0
     if rank == root:
-        K = sum(all_k)
-        ldm = K + (F if sqrt_mu > 0.0 else 0)
-        ldm = ((ldm + 3) // 4) * 4
-        M = torch.zeros((nc * ldm,), dtype=torch.float64, device=dev)
-        Mv = M.view(nc, ldm)
-        off = 0
-        for r in range(world):
-            Mv[:, off:off + all_k[r]] = gathered[r][:, :all_k[r]]
-            off += all_k[r]
-        b_root, res = ops.solve(M, K, ldm, F, sqrt_mu)
+        b_root, res = _combine(ops, gathered, all_k, F, sqrt_mu, dev)
         beta.copy_(b_root)
     dist.broadcast(beta, src=root, group=group)
     return beta, res

@@ -90,6 +90,31 @@ def test_tsqr_two_ranks_matches_single_lstsq(case):
     assert out[0] == out[1]          # replicated bit-identically (broadcast)
 
 
+@pytest.mark.parametrize("P,R,F,ridge", [(4, 300, 40, 0.0), (8, 100, 40, 0.0), (3, 30, 20, 0.1)])
+def test_tsqr_local_logical_blocks(P, R, F, ridge):
+    """single-process TSQR over P logical row blocks (the 1-GPU mode) == one lstsq"""
+    from paper_2602_10541_b200.dist import tsqr_local
+    g = np.random.default_rng(P)
+    A = g.normal(size=(R, F))
+    b = g.normal(size=R)
+    blocks = []
+    for r in range(P):
+        a, e = shard_range(R, r, P)
+        n = e - a
+        lda = max(4, ((n + 3) // 4) * 4)
+        Ab = torch.zeros((F + 1) * lda, dtype=torch.float64)
+        V = Ab.view(F + 1, lda)
+        V[:F, :n] = torch.from_numpy(A[a:e].T.copy())
+        V[F, :n] = torch.from_numpy(b[a:e].copy())
+        blocks.append((Ab, n, lda))
+    beta, _ = tsqr_local(blocks, F, ridge_rel=ridge, ops=NumpyOps())
+    if ridge > 0:
+        sq = ridge * np.linalg.norm(A)
+        A, b = np.vstack([A, sq * np.eye(F)]), np.concatenate([b, np.zeros(F)])
+    ref, *_ = np.linalg.lstsq(A, b, rcond=None)
+    assert np.allclose(beta.numpy(), ref, rtol=1e-9, atol=1e-9 * np.abs(ref).max())
+
+
 def test_shard_ranges_partition_rows():
     for R in (0, 1, 7, 1002, 2_097_152):
         for P in (1, 2, 3, 4, 8):

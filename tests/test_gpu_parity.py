@@ -335,6 +335,31 @@ def test_assemble_host_matches_device(ctx, chunk):
         assert np.isnan(A_h.reshape(F + 1, ldh)[:F, n:]).all()     # padding untouched
 
 
+# ------------------------------------------------------------------------------------- TSQR on one GPU
+@pytest.mark.parametrize("name,size,P", [("c1_poisson1d", "full", 8), ("c2_poisson2d", "full", 4),
+                                         ("c5_biharm3d", "mini", 3)])
+def test_tsqr_logical_blocks_match_oracle(ctx, name, size, P):
+    """TSQR (per-block fls_qr_r, stacked R factors, root fls_solve) over P row shards held on
+    one device; C1 at P=8 has 125-row blocks < F+1 (trapezoidal R).  u vs oracle lstsq."""
+    from paper_2602_10541_b200.dist import tsqr_local
+    p = wl.make_problem(name, size)
+    W, b, Wd, bd = _parity_feats(p)
+    F, R = p.n_features, p.n_rows
+    bset = fls.BlockSet(dev_blocks(p), p.dim)
+    blocks = []
+    for r in range(P):
+        a, e = wl.shard_range(R, r, P)
+        Ab, lda = fls.fls_assemble(ctx, Wd, bd, bset, row_begin=a, row_end=e)
+        blocks.append((Ab, e - a, lda))
+    beta, _ = tsqr_local(blocks, F, ridge_rel=p.ridge_rel, ctx=ctx)
+    Xt = p.test_points(10_000)
+    u_gpu = fls.fls_eval(ctx, Wd, bd, beta, torch.from_numpy(Xt).cuda()).cpu().numpy()
+    Ao, ro, _ = oracle.assemble(W, b, p.blocks, want_scale=False)
+    beta_o, _, _ = oracle.lstsq(Ao, ro, ridge_rel=p.ridge_rel)
+    u_orc = oracle.evaluate(W, b, beta_o, Xt)
+    assert np.linalg.norm(u_gpu - u_orc) / np.linalg.norm(u_orc) <= U_TOL
+
+
 # ------------------------------------------------------------------------------------- full-size solves
 @pytest.mark.parametrize("name", ["c3_poisson5d", "c4_heat2d", "c5_biharm3d"])
 def test_full_size_solve_parity_with_oracle_artifact(ctx, name):
