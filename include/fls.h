@@ -219,6 +219,26 @@ FLS_API fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t l
                      double sqrt_mu, double *beta, double *resid_norm);
 
 /* ---------------------------------------------------------------------------------------- */
+/* Learnable bandwidth (App. E): W_j = L W^_j with frozen W^_j ~ N(0, I) and a    */
+/* learnable d x d factor L (scalar sigma: L = sigma I; anisotropic: lower-triangular        */
+/* Cholesky factor).  The outer loss is  Lout = ||A(L) beta* - b||^2, beta* the     */
+/* least-squares optimum; by optimality of beta* its gradient needs no differentiation of   */
+/* the solve:  dLout/dL_kl = 2 sum_i r_i sum_j beta_j dA_ij/dW_jk W^_jl,  r = A beta* - b,    */
+/* with dA_ij/dW_jk = w s sum_t c_t [alpha_tk prod W^(alpha_t - e_k) Phi_p(z_ij)              */
+/*                                   + prod W^alpha_t x_ik Phi_{p+1}(z_ij)]  (Eq. 2 + chain). */
+/* fls_features_transform: W (F x dim) = rows L W^_j (L host, dim x dim row-major).          */
+/* fls_bandwidth_grad: blocks as for fls_assemble but values = the block's rows of r (device) */
+/*   (constant-coefficient operators only: FLS_EUNSUPPORTED with coefficient fields);       */
+/*   G (host, dim x dim row-major) receives dLout/dL; deterministic; blocking.               */
+/* ---------------------------------------------------------------------------------------- */
+FLS_API fls_status fls_features_transform(fls_ctx *ctx, int32_t dim, int64_t n_features,
+                                          const double *L, const double *W_hat, double *W);
+FLS_API fls_status fls_bandwidth_grad(fls_ctx *ctx, const double *W, const double *W_hat,
+                                      const double *b, int32_t dim, int64_t n_features,
+                                      int32_t normalize, const fls_block *blocks,
+                                      int32_t n_blocks, const double *beta, double *G);
+
+/* ---------------------------------------------------------------------------------------- */
 /* Newton-Raphson support (Eq. 4-5): nonlinear PDE  L[u] + N(u) = f  with a      */
 /* pointwise nonlinearity N.  The Jacobian  J_ij = L[phi_j](x_i) + N'(u(x_i)) s phi_j(x_i)  */
 /* is fls_assemble with one extra identity term whose coefficient field is          */

@@ -79,6 +79,11 @@ _SIGS = {
     "fls_nl_residual": (C.c_int, [C.c_void_p, C.POINTER(fls_nonlinearity), C.c_int64, C.c_void_p,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                   C.c_void_p]),
+    "fls_features_transform": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p,
+                                         C.c_void_p]),
+    "fls_bandwidth_grad": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                     C.c_int64, C.c_int32, C.POINTER(fls_block), C.c_int32,
+                                     C.c_void_p, C.c_void_p]),
     "fls_axpy": (C.c_int, [C.c_void_p, C.c_int64, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     "fls_assemble_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64,
                                     C.c_int32, C.POINTER(fls_block), C.c_int32, C.c_int64,

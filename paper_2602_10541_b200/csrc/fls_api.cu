@@ -200,7 +200,7 @@ fls_status fls_ctx_create(int device, void *cuda_stream, fls_ctx **out) {
 fls_status fls_ctx_destroy(fls_ctx *ctx) {
   if (!ctx) return FLS_OK;
   DeviceGuard g(ctx->device);
-  if (ctx->stream || true) cudaStreamSynchronize(ctx->stream);
+  cudaStreamSynchronize(ctx->stream);  // kernels may still read the workspace
   if (ctx->solver) cusolverDnDestroy(ctx->solver);
   if (ctx->blas) cublasDestroy(ctx->blas);
   for (cudaEvent_t ev : ctx->ev) cudaEventDestroy(ev);
@@ -817,6 +817,110 @@ fls_status fls_qr_r(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda, int64_
   if (fls_status s = geqrf_inplace(ctx, M, n_rows, lda, n_cols)) return s;
   cudaError_t e = launch_copy_upper(M, lda, k, n_cols, R, ldr, ctx->stream);
   if (e != cudaSuccess) return cuda_fail(e, "copy_upper");
+  FLS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return FLS_OK;
+}
+
+fls_status fls_features_transform(fls_ctx *ctx, int32_t dim, int64_t n_features, const double *L,
+                                  const double *W_hat, double *W) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (dim < 1 || dim > FLS_MAX_DIM) return fail(FLS_EINVAL, "dim %d not in 1..%d", dim, FLS_MAX_DIM);
+  if (n_features < 1) return fail(FLS_EINVAL, "n_features < 1");
+  if (!L || !W_hat || !W) return fail(FLS_EINVAL, "NULL pointer");
+  TransformArgs t;
+  std::memset(&t, 0, sizeof t);
+  for (int i = 0; i < dim * dim; ++i) {
+    if (!std::isfinite(L[i])) return fail(FLS_EINVAL, "L[%d] not finite", i);
+    t.L[i] = L[i];
+  }
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_transform(dim, n_features, t, W_hat, W, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "transform_kernel");
+  return FLS_OK;
+}
+
+fls_status fls_bandwidth_grad(fls_ctx *ctx, const double *W, const double *W_hat, const double *b,
+                              int32_t dim, int64_t n_features, int32_t normalize,
+                              const fls_block *blocks, int32_t n_blocks, const double *beta,
+                              double *G) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!W_hat || !beta || !G) return fail(FLS_EINVAL, "W_hat, beta or G is NULL");
+  static thread_local AsmPlan ap;
+  int64_t total = 0;
+  for (int q = 0; blocks && q < n_blocks; ++q) total += blocks[q].n_points;
+  // same block / operator validation as the assembly (no output matrix: pass W as a dummy A
+  // with a row-major lda that always passes)
+  if (fls_status s = validate_assemble(dim, n_features, W, b, blocks, n_blocks, 0, total, W,
+                                       n_features, FLS_ROW_MAJOR, ap))
+    return s;
+  for (int q = 0; q < n_blocks; ++q) {
+    if (blocks[q].n_fields > 0 || ap.plans[q].G > 0)
+      return fail(FLS_EUNSUPPORTED, "block %d: coefficient fields in the bandwidth gradient", q);
+    if (blocks[q].n_points > 0 && !blocks[q].values)
+      return fail(FLS_EINVAL, "block %d: values (the residual rows) is NULL", q);
+  }
+  const int64_t F = n_features;
+  DeviceGuard g(ctx->device);
+  // records: kGradRec doubles per feature per block; partial slots: <= 16 per block
+  if (fls_status s = ensure_ws(ctx, (size_t)n_blocks * F * kGradRec * sizeof(double))) return s;
+  int nslots = 0;
+  int slots_q[64];
+  for (int q = 0; q < n_blocks; ++q) {
+    const int64_t n = blocks[q].n_points;
+    slots_q[q] = n == 0 ? 0 : (int)std::min<int64_t>(16, (n + 255) / 256);
+    nslots += slots_q[q];
+  }
+  double *partials = nullptr;
+  const size_t pbytes = sizeof(double) * ((size_t)std::max(nslots, 1) * F * dim + (size_t)dim * dim);
+  if (cudaMallocAsync((void **)&partials, pbytes, ctx->stream) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FLS_ENOMEM, "bandwidth_grad workspace");
+  }
+  double *Gd = partials + (size_t)std::max(nslots, 1) * F * dim;
+  const double s_norm = normalize ? 1.0 / std::sqrt((double)F) : 1.0;
+  int slot0 = 0;
+  cudaError_t e = cudaSuccess;
+  for (int q = 0; q < n_blocks && e == cudaSuccess; ++q) {
+    if (slots_q[q] == 0) continue;
+    const fls_block &B = blocks[q];
+    PrefArgs pa;
+    std::memset(&pa, 0, sizeof pa);
+    pa.W = W;
+    pa.b = b;
+    pa.F = F;
+    pa.D = dim;
+    pa.n_terms = ap.plans[q].n_terms;
+    pa.S = kGradRec;
+    pa.scale = s_norm * B.weight;
+    pa.pf = ctx->ws + (size_t)q * F * kGradRec;
+    pa.err = ctx->d_err;
+    std::memcpy(pa.terms, ap.plans[q].terms, sizeof pa.terms);
+    e = launch_grad_prefactor(pa, ctx->stream);
+    if (e != cudaSuccess) break;
+    GradArgs ga;
+    std::memset(&ga, 0, sizeof ga);
+    ga.pf = pa.pf;
+    ga.S = kGradRec;
+    ga.F = F;
+    ga.X = B.X;
+    ga.r = B.values;
+    ga.row0 = 0;
+    ga.row1 = B.n_points;
+    ga.rows_per_slot = (B.n_points + slots_q[q] - 1) / slots_q[q];
+    ga.slot0 = slot0;
+    ga.partials = partials;
+    ga.err = ctx->d_err;
+    e = launch_grad_reduce(dim, ga, slots_q[q], ctx->stream);
+    slot0 += slots_q[q];
+  }
+  if (e == cudaSuccess) {
+    if (nslots == 0) e = cudaMemsetAsync(Gd, 0, sizeof(double) * dim * dim, ctx->stream);
+    else e = launch_grad_final(dim, F, nslots, partials, beta, W_hat, Gd, ctx->stream);
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(G, Gd, sizeof(double) * dim * dim, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaFreeAsync(partials, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "bandwidth_grad");
   FLS_CUDA(cudaStreamSynchronize(ctx->stream));
   return FLS_OK;
 }

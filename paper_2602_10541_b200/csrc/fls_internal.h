@@ -121,6 +121,29 @@ struct NlArgs {
   unsigned *err;
 };
 cudaError_t launch_nl_residual(const NlArgs &a, int nblk, double *stats, cudaStream_t st);
+
+// learnable bandwidth (fls_bandwidth.cu)
+struct TransformArgs {
+  double L[FLS_MAX_DIM * FLS_MAX_DIM];
+};
+constexpr int kGradRec = 3 * FLS_MAX_DIM + 4;  // record stride upper bound (doubles)
+struct GradArgs {
+  const double *pf;
+  int32_t S;
+  int64_t F;
+  const double *X;
+  const double *r;
+  int64_t row0, row1, rows_per_slot;
+  int32_t slot0;
+  double *partials;
+  unsigned *err;
+};
+cudaError_t launch_transform(int32_t D, int64_t F, const TransformArgs &t, const double *Wh,
+                             double *W, cudaStream_t st);
+cudaError_t launch_grad_prefactor(const PrefArgs &a, cudaStream_t st);
+cudaError_t launch_grad_reduce(int D, const GradArgs &a, int slots, cudaStream_t st);
+cudaError_t launch_grad_final(int D, int64_t F, int nslots, const double *partials,
+                              const double *beta, const double *Wh, double *G, cudaStream_t st);
 cudaError_t launch_axpy(int64_t n, double alpha, const double *x, const double *y, double *out,
                         cudaStream_t st);
 cudaError_t launch_frob2(const double *A, int64_t lda, int64_t m, int64_t n, double *partials,

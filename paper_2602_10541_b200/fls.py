@@ -27,7 +27,8 @@ Term = Tuple[Sequence[int], float, int]   # (alpha, coef, field)
 __all__ = ["Context", "Block", "fls_features", "fls_assemble", "fls_solve", "fls_qr_r",
            "fls_frob2", "fls_eval", "fls_sync", "fls_ctx_timing", "fls_ctx_timing_read",
            "fls_assemble_host", "HostBlockSet", "BlockSet", "fls_features_blocks", "QRFactor",
-           "make_nonlinearity", "fls_nl_residual", "fls_axpy", "FlsError", "FLS_COL_MAJOR", "FLS_ROW_MAJOR",
+           "make_nonlinearity", "fls_nl_residual", "fls_axpy", "fls_features_transform",
+           "fls_bandwidth_grad", "FlsError", "FLS_COL_MAJOR", "FLS_ROW_MAJOR",
            "round_up"]
 
 
@@ -179,6 +180,29 @@ def fls_axpy(ctx: Context, alpha: float, x: torch.Tensor, y: torch.Tensor,
     out = torch.empty_like(y) if out is None else out
     check(_abi.load().fls_axpy(ctx.handle, int(y.numel()), float(alpha), _ptr(x), _ptr(y), _ptr(out)))
     return out
+
+
+def fls_features_transform(ctx: Context, L, W_hat: torch.Tensor,
+                           W: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """W_j = L W^_j (App. E reparameterisation); L: host (d, d) array-like"""
+    _dev_f64(W_hat, "W_hat")
+    F, d = int(W_hat.shape[0]), int(W_hat.shape[1])
+    Lh = (C.c_double * (d * d))(*[float(v) for row in L for v in row])
+    W = torch.empty_like(W_hat) if W is None else W
+    check(_abi.load().fls_features_transform(ctx.handle, d, F, Lh, _ptr(W_hat), _ptr(W)))
+    return W
+
+
+def fls_bandwidth_grad(ctx: Context, W: torch.Tensor, W_hat: torch.Tensor, b: torch.Tensor,
+                       blocks, beta: torch.Tensor, normalize: bool = True):
+    """dLout/dL (d x d list of lists) for Lout = ||A beta* - b||^2; each block's `values`
+    must hold that block's rows of the residual r = A beta* - b"""
+    F, d = int(W.shape[0]), int(W.shape[1])
+    bs = blocks if isinstance(blocks, BlockSet) else BlockSet(blocks, d)
+    G = (C.c_double * (d * d))()
+    check(_abi.load().fls_bandwidth_grad(ctx.handle, _ptr(W), _ptr(W_hat), _ptr(b), d, F,
+                                         int(bool(normalize)), bs.arr, len(bs.blocks), _ptr(beta), G))
+    return [[G[k * d + l] for l in range(d)] for k in range(d)]
 
 
 class QRFactor:

@@ -308,6 +308,25 @@ def make_nl_problem(name: str, n_int: int = 1500, per_edge: int = 100, n_feature
     return p
 
 
+def make_helmholtz2d(n_int: int = 600, per_edge: int = 40, n_features: int = 120, k: float = 10.0,
+                     seed: int = 0) -> Problem:
+    """Helmholtz 2D (the paper's learnable-bandwidth demonstration case):
+    Lap u + k^2 u = f on [0,1]^2, Dirichlet (lambda = 100), u* = sin(4 pi x) sin(4 pi y) (a
+    synthetic stand-in: the paper states no u*).  Problem.sigma = 1 so parity_features()
+    returns the frozen base weights W^ ~ N(0, I) of App. E."""
+    gi, gb = rng(seed, STREAM_INTERIOR), rng(seed, STREAM_BOUNDARY)
+    lo, hi = np.zeros(2), np.ones(2)
+    Xi = _uniform_box(gi, n_int, lo, hi)
+    Xb = _faces(gb, 2, per_edge, lo, hi, axes=[1, 0])
+
+    def u(X):
+        return np.sin(4 * PI * X[:, 0]) * np.sin(4 * PI * X[:, 1])
+    f = (k * k - 32 * PI * PI) * u(Xi)
+    blocks = [Block("pde", _c(Xi), op_laplacian(2, 1.0) + op_identity(2, k * k), 1.0, _c(f)),
+              Block("bc", _c(Xb), op_identity(2), 100.0, _c(u(Xb)))]
+    return Problem("helmholtz2d", 2, n_features, 1.0, blocks, u, lo, hi, 0.0, seed)
+
+
 def sample_rows(n_rows: int, n_shards: int = 8, stride: int = 256) -> np.ndarray:
     """Deterministic sampled global rows: every stride-th row plus the first and last
     row of every shard of an n_shards-way split."""
