@@ -354,12 +354,15 @@ fls_status validate_assemble(int32_t dim, int64_t n_features, const double *W, c
 
 constexpr int kSmax = pf_stride(FLS_MAX_DIM, FLS_MAX_FIELDS, KM_SINCOS);
 
-// a2: one prefactor launch per block that has rows in [row_begin, row_end)
+// a2: prefactor records of every block that has rows in [row_begin, row_end), up to
+// kMaxBatch blocks per launch
 fls_status launch_prefactors(fls_ctx *ctx, const AsmPlan &ap, const double *W, const double *b,
                              int32_t dim, int64_t F, int32_t normalize, const fls_block *blocks,
                              int64_t row_begin, int64_t row_end, cudaStream_t st) {
   if (fls_status s = ensure_ws(ctx, (size_t)ap.n_blocks * F * kSmax * sizeof(double))) return s;
   const double s_norm = normalize ? 1.0 / std::sqrt((double)F) : 1.0;
+  static thread_local PrefBatch pb;
+  pb.n = 0;
   int64_t g0 = 0;
   for (int q = 0; q < ap.n_blocks; ++q) {
     const fls_block &B = blocks[q];
@@ -367,7 +370,7 @@ fls_status launch_prefactors(fls_ctx *ctx, const AsmPlan &ap, const double *W, c
     g0 += B.n_points;
     if (hi <= lo) continue;
     const OpPlan &pl = ap.plans[q];
-    PrefArgs pa;
+    PrefArgs &pa = pb.blk[pb.n++];
     std::memset(&pa, 0, sizeof pa);
     pa.W = W;
     pa.b = b;
@@ -381,20 +384,56 @@ fls_status launch_prefactors(fls_ctx *ctx, const AsmPlan &ap, const double *W, c
     pa.pf = ctx->ws + (size_t)q * F * kSmax;
     pa.err = ctx->d_err;
     std::memcpy(pa.terms, pl.terms, sizeof pl.terms);
-    cudaError_t e = launch_prefactor(pa, st);
-    if (e != cudaSuccess) return cuda_fail(e, "prefactor_kernel");
+    if (pb.n == kMaxBatch) {
+      cudaError_t e = launch_prefactor_batch(pb, F, st);
+      if (e != cudaSuccess) return cuda_fail(e, "prefactor_batch_kernel");
+      pb.n = 0;
+    }
+  }
+  if (pb.n > 0) {
+    cudaError_t e = launch_prefactor_batch(pb, F, st);
+    if (e != cudaSuccess) return cuda_fail(e, "prefactor_batch_kernel");
   }
   return FLS_OK;
 }
 
 // a3-a8: assembly launches for global rows [row_begin, row_end) into local rows of A / rhs.
 // blocks[q]'s X / fields / values pointers refer to point index pt_base[q] (0 for the caller's
-// own arrays; the slice start for staged copies).
+// own arrays; the slice start for staged copies).  Column-major: consecutive blocks that share
+// the kernel variant (same field-group count and sin / sin+cos family) go into one launch.
 fls_status assemble_range(fls_ctx *ctx, const AsmPlan &ap, int32_t dim, int64_t F,
                           const fls_block *blocks, const int64_t *pt_base, int64_t row_begin,
                           int64_t row_end, double *A, int64_t lda, int32_t layout, double *rhs,
                           cudaStream_t st) {
   const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0);
+  AsmArgs batch[kMaxBatch];
+  int nb = 0, bG = 0, bK = 0;
+  auto flush = [&]() -> fls_status {
+    if (nb == 0) return FLS_OK;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->timing) {
+      if (ctx->ev_used + 2 > ctx->ev.size()) {
+        for (int k = 0; k < 2; ++k) {
+          cudaEvent_t ev;
+          FLS_CUDA(cudaEventCreate(&ev));
+          ctx->ev.push_back(ev);
+        }
+      }
+      e0 = ctx->ev[ctx->ev_used++];
+      e1 = ctx->ev[ctx->ev_used++];
+      FLS_CUDA(cudaEventRecord(e0, st));
+    }
+    cudaError_t e = cudaSuccess;
+    if (layout == FLS_COL_MAJOR) {
+      e = launch_assemble_cm(dim, bG, bK, batch, nb, st);
+    } else {
+      for (int i = 0; i < nb && e == cudaSuccess; ++i) e = launch_assemble_rm(dim, bG, bK, batch[i], st);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "assemble kernel");
+    if (ctx->timing) FLS_CUDA(cudaEventRecord(e1, st));
+    nb = 0;
+    return FLS_OK;
+  };
   int64_t g0 = 0;  // first global row of block q
   for (int q = 0; q < ap.n_blocks; ++q) {
     const fls_block &B = blocks[q];
@@ -403,7 +442,11 @@ fls_status assemble_range(fls_ctx *ctx, const AsmPlan &ap, int32_t dim, int64_t 
     g0 += B.n_points;
     if (hi <= lo) continue;
     const OpPlan &pl = ap.plans[q];
-    AsmArgs aa;
+    if (nb > 0 && (pl.G != bG || pl.kmode != bK || nb == kMaxBatch))
+      if (fls_status s = flush()) return s;
+    bG = pl.G;
+    bK = pl.kmode;
+    AsmArgs &aa = batch[nb++];
     std::memset(&aa, 0, sizeof aa);
     aa.pf = ctx->ws + (size_t)q * F * kSmax;
     aa.F = F;
@@ -421,25 +464,8 @@ fls_status assemble_range(fls_ctx *ctx, const AsmPlan &ap, int32_t dim, int64_t 
     aa.nf = B.n_fields;
     aa.vec = vec ? 1 : 0;
     for (int i = 0; i < FLS_MAX_FIELDS; ++i) aa.gfield[i] = pl.gfield[i];
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (ctx->timing) {
-      if (ctx->ev_used + 2 > ctx->ev.size()) {
-        for (int k = 0; k < 2; ++k) {
-          cudaEvent_t ev;
-          FLS_CUDA(cudaEventCreate(&ev));
-          ctx->ev.push_back(ev);
-        }
-      }
-      e0 = ctx->ev[ctx->ev_used++];
-      e1 = ctx->ev[ctx->ev_used++];
-      FLS_CUDA(cudaEventRecord(e0, st));
-    }
-    cudaError_t e = (layout == FLS_COL_MAJOR) ? launch_assemble_cm(dim, pl.G, pl.kmode, aa, st)
-                                              : launch_assemble_rm(dim, pl.G, pl.kmode, aa, st);
-    if (e != cudaSuccess) return cuda_fail(e, "assemble kernel");
-    if (ctx->timing) FLS_CUDA(cudaEventRecord(e1, st));
   }
-  return FLS_OK;
+  return flush();
 }
 
 fls_status ensure_dev(double *&p, size_t &cap, size_t bytes, cudaStream_t st) {

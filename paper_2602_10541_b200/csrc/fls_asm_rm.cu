@@ -93,12 +93,12 @@ cudaError_t launch_assemble_rm(int D, int G, int kmode, const AsmArgs &a, cudaSt
   return cudaGetLastError();
 }
 
-cudaError_t launch_assemble_cm_sin(int D, int G, const AsmArgs &a, cudaStream_t st);
-cudaError_t launch_assemble_cm_sincos(int D, int G, const AsmArgs &a, cudaStream_t st);
+cudaError_t launch_assemble_cm_sin(int D, int G, AsmArgs *blks, int n, cudaStream_t st);
+cudaError_t launch_assemble_cm_sincos(int D, int G, AsmArgs *blks, int n, cudaStream_t st);
 
-cudaError_t launch_assemble_cm(int D, int G, int kmode, const AsmArgs &a, cudaStream_t st) {
-  return kmode == KM_SIN ? launch_assemble_cm_sin(D, G, a, st)
-                         : launch_assemble_cm_sincos(D, G, a, st);
+cudaError_t launch_assemble_cm(int D, int G, int kmode, AsmArgs *blks, int n, cudaStream_t st) {
+  return kmode == KM_SIN ? launch_assemble_cm_sin(D, G, blks, n, st)
+                         : launch_assemble_cm_sincos(D, G, blks, n, st);
 }
 
 }  // namespace fls

@@ -5,29 +5,37 @@
 namespace fls {
 
 template <int D, int G>
-static cudaError_t go_sincos(const AsmArgs &a0, cudaStream_t st) {
+static cudaError_t go_sincos(AsmArgs *blks, int n, cudaStream_t st) {
   constexpr int S = pf_stride(D, G, KM_SINCOS);
   const size_t smem = (size_t)kFC * S * sizeof(double);
-  AsmArgs a = a0;
-  const dim3 grid = asm_grid<D, G, KM_SINCOS>(a);
+  AsmBatch bt;
+  bt.n = n;
+  int64_t total = 0;
+  for (int q = 0; q < n; ++q) {
+    const dim3 g = asm_grid<D, G, KM_SINCOS>(blks[q]);  // sets blks[q].fpc
+    bt.blk[q] = blks[q];
+    bt.rt[q] = g.x;
+    total += (int64_t)g.x * g.y;
+    bt.cta_end[q] = total;
+  }
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(assemble_cm_kernel<D, G, KM_SINCOS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  assemble_cm_kernel<D, G, KM_SINCOS><<<grid, kNT, smem, st>>>(a);
+  assemble_cm_kernel<D, G, KM_SINCOS><<<(unsigned)total, kNT, smem, st>>>(bt);
   return cudaGetLastError();
 }
 
-cudaError_t launch_assemble_cm_sincos(int D, int G, const AsmArgs &a, cudaStream_t st) {
-#define FLS_G(d)                              \
-  switch (G) {                                \
-    case 0: return go_sincos<d, 0>(a, st);     \
-    case 1: return go_sincos<d, 1>(a, st);     \
-    case 2: return go_sincos<d, 2>(a, st);     \
-    case 3: return go_sincos<d, 3>(a, st);     \
-    case 4: return go_sincos<d, 4>(a, st);     \
-    default: return cudaErrorInvalidValue;    \
+cudaError_t launch_assemble_cm_sincos(int D, int G, AsmArgs *blks, int n, cudaStream_t st) {
+#define FLS_G(d)                                 \
+  switch (G) {                                   \
+    case 0: return go_sincos<d, 0>(blks, n, st);    \
+    case 1: return go_sincos<d, 1>(blks, n, st);    \
+    case 2: return go_sincos<d, 2>(blks, n, st);    \
+    case 3: return go_sincos<d, 3>(blks, n, st);    \
+    case 4: return go_sincos<d, 4>(blks, n, st);    \
+    default: return cudaErrorInvalidValue;       \
   }
   switch (D) {
     case 1: FLS_G(1)

@@ -109,8 +109,11 @@ inline dim3 asm_grid(AsmArgs &a) {
   return dim3((unsigned)rt, (unsigned)((a.F + a.fpc - 1) / a.fpc));
 }
 
+// One launch covers up to kMaxBatch row blocks that share the kernel variant (e.g. a PDE block
+// and its identity BC / IC blocks): the 1-D grid is the concatenation of each block's
+// (row tile, feature group) CTAs, row tile fastest.
 template <int D, int G, int KM>
-__global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_kernel(const AsmArgs a) {
+__global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_kernel(const AsmBatch bt) {
   using M = EntryMath<D, G, KM>;
   constexpr int S = M::S;
   constexpr int GG = G > 0 ? G : 1;
@@ -118,9 +121,15 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
   static_assert(S % 2 == 0, "pf stride must be even for 16-byte smem reads");
   extern __shared__ __align__(16) double sp[];
 
+  int qb = 0;
+  while (qb + 1 < bt.n && (int64_t)blockIdx.x >= bt.cta_end[qb]) ++qb;
+  const AsmArgs &a = bt.blk[qb];
+  const int64_t cta = (int64_t)blockIdx.x - (qb ? bt.cta_end[qb - 1] : 0);
+  const int64_t tile = cta % bt.rt[qb], group = cta / bt.rt[qb];
+
   // local rows (A-relative) of this thread: rbase + p*2*kNT + {0, 1}; rbase is even.
   // The block's points map to local rows [lr0, lr1): point i = pt0 + (r - lr0).
-  const int64_t rbase = (a.lr0 & ~int64_t(1)) + (int64_t)blockIdx.x * kRowsCTA + 2 * threadIdx.x;
+  const int64_t rbase = (a.lr0 & ~int64_t(1)) + tile * kRowsCTA + 2 * threadIdx.x;
   double x[NQ][D];
   double c[NQ][GG];
   bool in[NQ];
@@ -142,7 +151,7 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
       c[q][g] = (G > 0 && in[q]) ? __ldg(a.fields + i * a.nf + a.gfield[g]) : 0.0;
       bad |= !finite(c[q][g]);
     }
-    if (blockIdx.y == 0 && a.rhs != nullptr && in[q]) {
+    if (group == 0 && a.rhs != nullptr && in[q]) {
       const double v = a.values ? __ldg(a.values + i) : 0.0;
       bad |= !finite(v);
       a.rhs[r] = a.weight * v;
@@ -152,7 +161,7 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
 
   // this CTA's feature range [f0, f1) (a.fpc features per CTA, chosen by the launcher), walked
   // in shared-memory chunks of at most kFC records
-  const int64_t f0 = (int64_t)blockIdx.y * a.fpc;
+  const int64_t f0 = group * a.fpc;
   const int64_t f1 = f0 + a.fpc < a.F ? f0 + a.fpc : a.F;
   for (int64_t j0 = f0; j0 < f1; j0 += kFC) {
     const int nfe = (f1 - j0) < kFC ? (int)(f1 - j0) : kFC;

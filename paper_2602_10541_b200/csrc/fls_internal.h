@@ -101,8 +101,23 @@ struct FeatBlocks {  // multi-block bandwidths; n = 1 is the plain basis
 };
 cudaError_t launch_features(int32_t dim, int64_t F, const FeatBlocks &fb, uint64_t seed, double *W,
                             double *b, cudaStream_t st);
+// several row blocks sharing a kernel variant in one launch
+constexpr int kMaxBatch = 4;
+struct AsmBatch {
+  int32_t n;
+  int64_t cta_end[kMaxBatch];  // prefix sums of the blocks' CTA counts
+  int64_t rt[kMaxBatch];       // row tiles per block
+  AsmArgs blk[kMaxBatch];
+};
+struct PrefBatch {
+  int32_t n;
+  PrefArgs blk[kMaxBatch];
+};
+
 cudaError_t launch_prefactor(const PrefArgs &a, cudaStream_t st);
-cudaError_t launch_assemble_cm(int D, int G, int kmode, const AsmArgs &a, cudaStream_t st);
+cudaError_t launch_prefactor_batch(const PrefBatch &b, int64_t F, cudaStream_t st);
+// blks: n (<= kMaxBatch) blocks of one variant; fpc is set per block by the launcher
+cudaError_t launch_assemble_cm(int D, int G, int kmode, AsmArgs *blks, int n, cudaStream_t st);
 cudaError_t launch_assemble_rm(int D, int G, int kmode, const AsmArgs &a, cudaStream_t st);
 cudaError_t launch_eval(int D, const EvalArgs &a, cudaStream_t st);
 cudaError_t launch_ridge_fill(double *Ab, int64_t lda, int64_t row0, int64_t F, int64_t ncols,

@@ -87,9 +87,21 @@ cudaError_t launch_features(int32_t dim, int64_t F, const FeatBlocks &fb, uint64
 //   Pc_gj = s w sum_{t in g, |a_t| odd } c_t (+1,-1 for |a_t| mod 4 = 1,3) prod_k W_jk^a_tk
 // and the per-feature record [W_j / pi, b'_j / pi, P...] the assembly kernel reads.
 // ------------------------------------------------------------------------------------------
+__device__ void prefactor_one(const PrefArgs &a, int64_t j);
+
 __global__ void prefactor_kernel(const PrefArgs a) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= a.F) return;
+  if (j < a.F) prefactor_one(a, j);
+}
+
+// all blocks of one fls_assemble call in one launch (grid.y = block)
+__global__ void prefactor_batch_kernel(const PrefBatch b) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const PrefArgs &a = b.blk[blockIdx.y];
+  if (j < a.F) prefactor_one(a, j);
+}
+
+__device__ void prefactor_one(const PrefArgs &a, int64_t j) {
   double w[FLS_MAX_DIM];
   bool ok = true;
   for (int k = 0; k < a.D; ++k) {
@@ -152,6 +164,12 @@ __global__ void prefactor_kernel(const PrefArgs a) {
 cudaError_t launch_prefactor(const PrefArgs &a, cudaStream_t st) {
   const unsigned nb = (unsigned)((a.F + 127) / 128);
   prefactor_kernel<<<nb, 128, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prefactor_batch(const PrefBatch &b, int64_t F, cudaStream_t st) {
+  const dim3 grid((unsigned)((F + 127) / 128), (unsigned)b.n);
+  prefactor_batch_kernel<<<grid, 128, 0, st>>>(b);
   return cudaGetLastError();
 }
 
