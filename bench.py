@@ -346,7 +346,9 @@ def main():
     Ab = torch.empty(((F + 1) * lda,), dtype=torch.float64, device="cuda")
     W = torch.empty((F, d), dtype=torch.float64, device="cuda")
     b = torch.empty((F,), dtype=torch.float64, device="cuda")
-    launches_per_step = 1 + 2 * len(blocks)          # features + (prefactor, assemble) per block
+    # per step: features + one prefactor launch per <= 4 blocks; assembly launches are counted
+    # by libfls's own timing events (one per batch of blocks sharing a kernel variant)
+    launches_per_step_fixed = 1 + (len(blocks) + 3) // 4
 
     def step():
         fls.fls_features(ctx, d, F, p.sigma, p.seed, W, b)
@@ -410,7 +412,7 @@ def main():
                      "frac": achieved / hbm_peak, "traffic": traffic,
                      "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
                      "kernel": "assemble_cm_kernel", "kernel_ms_avg": k_avg_ms},
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": launches_per_step_fixed * args.steps + k_launches,
         "clocks": clocks,
     }
     # ---------------------------------------------------------------- end to end (host buffers)
