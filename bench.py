@@ -406,12 +406,14 @@ def main():
         "config": {"workload": p.name, "rows": R, "features": F, "dim": d,
                    "operator": "biharmonic + 16(1+x1) u" if p.name == "c5_biharm3d" else p.name,
                    "A_bytes": 8 * R * (F + 1), "parallelism": f"rows{world}",
-                   "l2": "no flush: each step writes the 137 GB output (>1000x the 126 MB L2)"},
-        "hbm_write_gbs": 8.0 * R * (F + 1) / (ms_step / 1e3) / 1e9,
+                   "l2": f"no flush: each step writes {8e-9 * n_local * (F + 1):.1f} GB per GPU "
+                         f"(>> the 126 MB L2)"},
+        "hbm_write_gbs_all_gpus": 8.0 * R * (F + 1) / (ms_step / 1e3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
                      "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                     "kernel": "assemble_cm_kernel", "kernel_ms_avg": k_avg_ms},
+                     "kernel": "assemble_cm_kernel", "kernel_ms_avg": k_avg_ms,
+                     "scope": "rank 0's GPU (per-GPU kernel roofline)"},
         "gpu_launches": launches_per_step_fixed * args.steps + k_launches,
         "clocks": clocks,
     }

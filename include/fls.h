@@ -158,6 +158,21 @@ FLS_API fls_status fls_features_blocks(fls_ctx *ctx, int32_t dim, int32_t n_bloc
                                        const int64_t *block_features, const double *sigmas,
                                        uint64_t seed, double *W, double *b);
 
+/* Alg. 1 line 2 ("Sample collocation points"): seeded points in a box domain, same
+ * Philox4x64-10 generator and uniform map as fls_features (u = (raw >> 11) 2^-53), stream
+ * `stream` (convention: 3 interior, 4 boundary, 5 initial, 6 held-out test).
+ *   fls_sample_box:   X[i][k] = lo_k + (hi_k - lo_k) * u(i*dim + k),  i < n.
+ *   fls_sample_faces: for each axis k with bit k of axes_mask set, in increasing k, per_face
+ *                     points on the face x_k = lo_k then per_face on x_k = hi_k, the other
+ *                     coordinates as in fls_sample_box (point index = running output row).
+ * lo, hi: host arrays of dim with lo_k < hi_k.  X: device, rows x dim (rows = n, or
+ * 2 * per_face * popcount(axes_mask)).  Asynchronous.  Errors: FLS_EINVAL. */
+FLS_API fls_status fls_sample_box(fls_ctx *ctx, int32_t dim, int64_t n, const double *lo,
+                                  const double *hi, uint64_t seed, uint64_t stream, double *X);
+FLS_API fls_status fls_sample_faces(fls_ctx *ctx, int32_t dim, int64_t per_face,
+                                    uint32_t axes_mask, const double *lo, const double *hi,
+                                    uint64_t seed, uint64_t stream, double *X);
+
 #define FLS_COL_MAJOR 0   /* A[j * lda + i]: rows contiguous (what fls_solve consumes) */
 #define FLS_ROW_MAJOR 1   /* A[i * lda + j]: features contiguous */
 

@@ -52,6 +52,10 @@ def lib():
         L.orc_features.argtypes = [C.c_int, C.c_int64, C.c_double, C.c_uint64, C.c_void_p, C.c_void_p]
         L.orc_features_blocks.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64,
                                           C.c_void_p, C.c_void_p]
+        L.orc_sample_box.argtypes = [C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_uint64,
+                                     C.c_uint64, C.c_void_p]
+        L.orc_sample_faces.argtypes = [C.c_int, C.c_int64, C.c_uint32, C.c_void_p, C.c_void_p,
+                                       C.c_uint64, C.c_uint64, C.c_void_p]
         L.orc_diff.argtypes =[C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_assemble.argtypes = [C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
                                    C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
@@ -106,6 +110,23 @@ def features_blocks(dim: int, counts: Sequence[int], sigmas: Sequence[float], se
     s = np.array(sigmas, dtype=np.float64)
     lib().orc_features_blocks(dim, len(counts), _p(c), _p(s), seed, _p(W), _p(b))
     return W, b
+
+
+def sample_box(dim, n, lo, hi, seed, stream):
+    X = np.zeros((n, dim))
+    lo = _f64(lo)
+    hi = _f64(hi)
+    lib().orc_sample_box(dim, n, _p(lo), _p(hi), seed, stream, _p(X))
+    return X
+
+
+def sample_faces(dim, per_face, axes_mask, lo, hi, seed, stream):
+    nax = bin(axes_mask).count("1")
+    X = np.zeros((2 * per_face * nax, dim))
+    lo = _f64(lo)
+    hi = _f64(hi)
+    lib().orc_sample_faces(dim, per_face, axes_mask, _p(lo), _p(hi), seed, stream, _p(X))
+    return X
 
 
 def diff(alpha: Sequence[int]):

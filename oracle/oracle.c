@@ -134,6 +134,39 @@ int orc_features_blocks(int dim, int n_blocks, const int64_t *counts, const doub
     return 0;
 }
 
+/*
+ * Alg. 1 line 2: seeded collocation points in a box (R1 streams).
+ * Coordinate n of the row-major output uses raw word n of the stream: x = lo + (hi - lo) u.
+ * Faces: for each axis k in axes_mask (increasing), per_face points on x_k = lo_k, then
+ * per_face on x_k = hi_k; the face coordinate replaces the drawn one.
+ */
+int orc_sample_box(int dim, int64_t n, const double *lo, const double *hi, uint64_t seed,
+                   uint64_t stream, double *X) {
+    for (int64_t i = 0; i < n; ++i)
+        for (int k = 0; k < dim; ++k) {
+            double u = uniform01(seed, stream, (uint64_t)(i * dim + k));
+            X[i * dim + k] = lo[k] + (hi[k] - lo[k]) * u;
+        }
+    return 0;
+}
+
+int orc_sample_faces(int dim, int64_t per_face, uint32_t axes_mask, const double *lo,
+                     const double *hi, uint64_t seed, uint64_t stream, double *X) {
+    int64_t row = 0;
+    for (int k = 0; k < dim; ++k) {
+        if (!(axes_mask & (1u << k))) continue;
+        for (int side = 0; side < 2; ++side)
+            for (int64_t p = 0; p < per_face; ++p, ++row)
+                for (int l = 0; l < dim; ++l) {
+                    double u = uniform01(seed, stream, (uint64_t)(row * dim + l));
+                    double v = lo[l] + (hi[l] - lo[l]) * u;
+                    if (l == k) v = side ? hi[k] : lo[k];
+                    X[row * dim + l] = v;
+                }
+    }
+    return 0;
+}
+
 /* ------------------------------------------------------------------------- */
 /* Symbolic differentiation of  c * Phi_p(W.x + b) * prod_k W_k^{e_k}.        */
 /* State (e, p); Phi_0 = sin, Phi_1 = cos, Phi_2 = -sin, Phi_3 = -cos.        */

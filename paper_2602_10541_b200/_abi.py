@@ -79,6 +79,10 @@ _SIGS = {
     "fls_nl_residual": (C.c_int, [C.c_void_p, C.POINTER(fls_nonlinearity), C.c_int64, C.c_void_p,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                   C.c_void_p]),
+    "fls_sample_box": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p,
+                                 C.c_uint64, C.c_uint64, C.c_void_p]),
+    "fls_sample_faces": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_void_p,
+                                   C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]),
     "fls_features_transform": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p,
                                          C.c_void_p]),
     "fls_bandwidth_grad": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,

@@ -847,6 +847,62 @@ fls_status fls_qr_r(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda, int64_
   return FLS_OK;
 }
 
+static fls_status sample_common(fls_ctx *ctx, int32_t dim, const double *lo, const double *hi,
+                                SampleArgs &sa) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (dim < 1 || dim > FLS_MAX_DIM) return fail(FLS_EINVAL, "dim %d not in 1..%d", dim, FLS_MAX_DIM);
+  if (!lo || !hi) return fail(FLS_EINVAL, "lo or hi is NULL");
+  sa.D = dim;
+  for (int k = 0; k < dim; ++k) {
+    if (!(lo[k] < hi[k]) || !std::isfinite(lo[k]) || !std::isfinite(hi[k]))
+      return fail(FLS_EINVAL, "need finite lo[%d] < hi[%d]", k, k);
+    sa.lo[k] = lo[k];
+    sa.hi[k] = hi[k];
+  }
+  return FLS_OK;
+}
+
+fls_status fls_sample_box(fls_ctx *ctx, int32_t dim, int64_t n, const double *lo, const double *hi,
+                          uint64_t seed, uint64_t stream, double *X) {
+  SampleArgs sa;
+  std::memset(&sa, 0, sizeof sa);
+  if (fls_status s = sample_common(ctx, dim, lo, hi, sa)) return s;
+  if (n < 0) return fail(FLS_EINVAL, "n < 0");
+  if (n > 0 && !X) return fail(FLS_EINVAL, "X is NULL");
+  sa.rows = n;
+  sa.seed = seed;
+  sa.stream = stream;
+  sa.X = X;
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_sample(sa, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "sample_kernel");
+  return FLS_OK;
+}
+
+fls_status fls_sample_faces(fls_ctx *ctx, int32_t dim, int64_t per_face, uint32_t axes_mask,
+                            const double *lo, const double *hi, uint64_t seed, uint64_t stream,
+                            double *X) {
+  SampleArgs sa;
+  std::memset(&sa, 0, sizeof sa);
+  if (fls_status s = sample_common(ctx, dim, lo, hi, sa)) return s;
+  if (per_face < 0) return fail(FLS_EINVAL, "per_face < 0");
+  if (axes_mask >> dim) return fail(FLS_EINVAL, "axes_mask has bits beyond dim %d", dim);
+  int nax = 0;
+  for (int k = 0; k < dim; ++k)
+    if (axes_mask & (1u << k)) sa.face_axis[nax++] = k;
+  sa.rows = 2 * per_face * nax;
+  if (sa.rows > 0 && !X) return fail(FLS_EINVAL, "X is NULL");
+  sa.per_face = per_face;
+  sa.seed = seed;
+  sa.stream = stream;
+  sa.X = X;
+  if (sa.rows == 0) return FLS_OK;
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_sample(sa, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "sample_kernel");
+  return FLS_OK;
+}
+
 fls_status fls_features_transform(fls_ctx *ctx, int32_t dim, int64_t n_features, const double *L,
                                   const double *W_hat, double *W) {
   if (fls_status s = check_ctx(ctx)) return s;

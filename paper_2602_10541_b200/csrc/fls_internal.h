@@ -101,6 +101,16 @@ struct FeatBlocks {  // multi-block bandwidths; n = 1 is the plain basis
 };
 cudaError_t launch_features(int32_t dim, int64_t F, const FeatBlocks &fb, uint64_t seed, double *W,
                             double *b, cudaStream_t st);
+struct SampleArgs {
+  int32_t D;
+  int64_t rows;
+  double lo[FLS_MAX_DIM], hi[FLS_MAX_DIM];
+  uint64_t seed, stream;
+  int64_t per_face;                  // 0: box interior
+  int32_t face_axis[FLS_MAX_DIM];    // axis of face pair f/2
+  double *X;
+};
+cudaError_t launch_sample(const SampleArgs &a, cudaStream_t st);
 // several row blocks sharing a kernel variant in one launch
 constexpr int kMaxBatch = 4;
 struct AsmBatch {

@@ -81,6 +81,39 @@ cudaError_t launch_features(int32_t dim, int64_t F, const FeatBlocks &fb, uint64
 }
 
 // ------------------------------------------------------------------------------------------
+// Alg. 1 line 2: collocation points.  Thread t owns Philox block t = coordinates
+// 4t..4t+3 of the row-major (rows x D) output; face mode pins the face coordinate.
+// __dmul_rn / __dadd_rn keep lo + (hi - lo) u free of FMA contraction (bit-exact vs the oracle).
+// ------------------------------------------------------------------------------------------
+__global__ void sample_kernel(const SampleArgs a) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = a.rows * a.D;
+  if (4 * t >= total) return;
+  uint64_t c[4] = {(uint64_t)t + 1, 0, 0, 0};
+  philox4x64(c, a.seed, a.stream);
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const int64_t n = 4 * t + w;
+    if (n >= total) break;
+    const int64_t row = n / a.D;
+    const int k = (int)(n % a.D);
+    double v = __dadd_rn(a.lo[k], __dmul_rn(__dsub_rn(a.hi[k], a.lo[k]), u01(c[w])));
+    if (a.per_face > 0) {
+      const int64_t f = row / a.per_face;
+      if (a.face_axis[f / 2] == k) v = (f & 1) ? a.hi[k] : a.lo[k];
+    }
+    a.X[n] = v;
+  }
+}
+
+cudaError_t launch_sample(const SampleArgs &a, cudaStream_t st) {
+  const int64_t blocks4 = ((a.rows * a.D + 3) / 4 + 255) / 256;
+  if (blocks4 == 0) return cudaSuccess;
+  sample_kernel<<<(unsigned)blocks4, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
 // a2 prefactor fold (Eq. 2; Cor. 1 P:L102; App. F angle addition P:L733).
 // For each feature j and coefficient group g:
 //   Ps_gj = s w sum_{t in g, |a_t| even} c_t (+1,-1 for |a_t| mod 4 = 0,2) prod_k W_jk^a_tk

@@ -28,7 +28,7 @@ __all__ = ["Context", "Block", "fls_features", "fls_assemble", "fls_solve", "fls
            "fls_frob2", "fls_eval", "fls_sync", "fls_ctx_timing", "fls_ctx_timing_read",
            "fls_assemble_host", "HostBlockSet", "BlockSet", "fls_features_blocks", "QRFactor",
            "make_nonlinearity", "fls_nl_residual", "fls_axpy", "fls_features_transform",
-           "fls_bandwidth_grad", "FlsError", "FLS_COL_MAJOR", "FLS_ROW_MAJOR",
+           "fls_bandwidth_grad", "fls_sample_box", "fls_sample_faces", "FlsError", "FLS_COL_MAJOR", "FLS_ROW_MAJOR",
            "round_up"]
 
 
@@ -180,6 +180,33 @@ def fls_axpy(ctx: Context, alpha: float, x: torch.Tensor, y: torch.Tensor,
     out = torch.empty_like(y) if out is None else out
     check(_abi.load().fls_axpy(ctx.handle, int(y.numel()), float(alpha), _ptr(x), _ptr(y), _ptr(out)))
     return out
+
+
+def fls_sample_box(ctx: Context, dim: int, n: int, lo, hi, seed: int, stream: int = 3):
+    """Alg. 1 line 2: n seeded uniform points in the box [lo, hi] (device, (n, dim))"""
+    X = torch.empty((n, dim), dtype=torch.float64, device=torch.device("cuda", ctx.device))
+    lo_h = (C.c_double * dim)(*[float(v) for v in lo])
+    hi_h = (C.c_double * dim)(*[float(v) for v in hi])
+    check(_abi.load().fls_sample_box(ctx.handle, dim, int(n), lo_h, hi_h,
+                                     C.c_uint64(int(seed) & (2**64 - 1)), C.c_uint64(int(stream)),
+                                     _ptr(X)))
+    return X
+
+
+def fls_sample_faces(ctx: Context, dim: int, per_face: int, axes: Sequence[int], lo, hi,
+                     seed: int, stream: int = 4):
+    """per_face points on each face x_k = lo_k, x_k = hi_k for k in axes (device)"""
+    mask = 0
+    for k in axes:
+        mask |= 1 << int(k)
+    rows = 2 * per_face * bin(mask).count("1")
+    X = torch.empty((rows, dim), dtype=torch.float64, device=torch.device("cuda", ctx.device))
+    lo_h = (C.c_double * dim)(*[float(v) for v in lo])
+    hi_h = (C.c_double * dim)(*[float(v) for v in hi])
+    check(_abi.load().fls_sample_faces(ctx.handle, dim, int(per_face), C.c_uint32(mask), lo_h, hi_h,
+                                       C.c_uint64(int(seed) & (2**64 - 1)), C.c_uint64(int(stream)),
+                                       _ptr(X)))
+    return X
 
 
 def fls_features_transform(ctx: Context, L, W_hat: torch.Tensor,

@@ -387,6 +387,53 @@ def test_full_size_solve_parity_with_oracle_artifact(ctx, name):
     assert rel <= U_TOL, rel
 
 
+# ------------------------------------------------------------------------------------- Alg. 1 line 2 + pipeline
+def test_sample_points_match_oracle(ctx):
+    lo, hi = [0.0, -1.0, 2.0], [1.0, 1.0, 2.5]
+    Xd = fls.fls_sample_box(ctx, 3, 1001, lo, hi, seed=7, stream=3).cpu().numpy()
+    Xo = oracle.sample_box(3, 1001, lo, hi, 7, 3)
+    assert np.array_equal(Xd, Xo)
+    Fd = fls.fls_sample_faces(ctx, 3, 37, [0, 2], lo, hi, seed=7, stream=4).cpu().numpy()
+    Fo = oracle.sample_faces(3, 37, 0b101, lo, hi, 7, 4)
+    assert np.array_equal(Fd, Fo)
+    assert np.all(Fd[:37, 0] == 0.0) and np.all(Fd[37:74, 0] == 1.0) and np.all(Fd[111:, 2] == 2.5)
+
+
+def test_pipeline_solve_linear_matches_oracle(ctx):
+    """Algorithm 1 through paper_2602_10541_b200.pipeline (features on the device, points from
+    fls_sample_*, operators from paper_2602_10541_b200.operators) vs the oracle chain on the
+    same W, b, points."""
+    from paper_2602_10541_b200 import operators as ops
+    from paper_2602_10541_b200.pipeline import solve_linear
+    pi = math.pi
+    Xi = fls.fls_sample_box(ctx, 2, 3000, [0, 0], [1, 1], seed=0, stream=3)
+    Xb = fls.fls_sample_faces(ctx, 2, 150, [0, 1], [0, 0], [1, 1], seed=0, stream=4)
+
+    def u(X):
+        return torch.sin(pi * X[:, 0]) * torch.sin(2 * pi * X[:, 1])
+    f = 5 * pi * pi * u(Xi)                                  # -Lap u
+    blocks = [fls.Block(Xi, ops.laplacian(2, -1.0), 1.0, f.contiguous()),
+              fls.Block(Xb, ops.identity(2), 100.0, u(Xb).contiguous())]
+    sol = solve_linear(ctx, dim=2, n_features=800, sigma=4.0, seed=0, blocks=blocks)
+    Xt = fls.fls_sample_box(ctx, 2, 2000, [0, 0], [1, 1], seed=0, stream=6)
+    ug = sol.evaluate(Xt).cpu().numpy()
+
+    class B:
+        def __init__(s, X, terms, w, v):
+            s.X, s.terms, s.weight, s.values, s.fields = X, terms, w, v, None
+    hb = [B(blk.X.cpu().numpy(), blk.terms, blk.weight, blk.values.cpu().numpy()) for blk in blocks]
+    W, b = sol.W.cpu().numpy(), sol.b.cpu().numpy()
+    Ao, ro, _ = oracle.assemble(W, b, hb, want_scale=False)
+    bo, _, _ = oracle.lstsq(Ao, ro)
+    uo = oracle.evaluate(W, b, bo, Xt.cpu().numpy())
+    assert np.linalg.norm(ug - uo) / np.linalg.norm(uo) <= U_TOL
+    us = u(Xt).cpu().numpy()
+    assert np.linalg.norm(ug - us) / np.linalg.norm(us) < 1e-6
+    # residual check L[u_N] vs f at the test points (P:L191)
+    Lu = sol.evaluate(Xt, terms=ops.laplacian(2, -1.0)).cpu().numpy()
+    assert np.linalg.norm(Lu - 5 * pi * pi * us) / np.linalg.norm(5 * pi * pi * us) < 1e-4
+
+
 # ------------------------------------------------------------------------------------- f3 / f4
 def test_features_blocks_match_oracle(ctx):
     counts, sig = [500, 7, 993], [1.0, 3.0, 12.0]
