@@ -227,6 +227,45 @@ def test_mode_sin_two_fields_high_order(ctx):
     _mode_case(ctx, terms, fields)
 
 
+@pytest.mark.parametrize("seed", range(12))
+def test_random_operator_fuzz(ctx, seed):
+    """random linear operators: 1..8 terms, |alpha| <= 6 per term, d in 1..8, 0..3 coefficient
+    fields, random weights, with and without the 1/sqrt(N) normalisation (Table 3 ablation)"""
+    g = np.random.default_rng(1000 + seed)
+    d = int(g.integers(1, 9))
+    nf = int(g.integers(0, 4))
+    terms = []
+    for _ in range(int(g.integers(1, 9))):
+        alpha = [0] * d
+        for _k in range(int(g.integers(0, 7))):
+            alpha[int(g.integers(0, d))] += 1
+        field = int(g.integers(-1, nf)) if nf else -1
+        terms.append((tuple(alpha), float(g.normal()), field))
+    F, n = int(g.integers(1, 300)), int(g.integers(1, 1500))
+    W = g.normal(0, g.uniform(0.5, 3), (F, d))
+    b = g.uniform(0, 2 * math.pi, F)
+    X = g.random((n, d))
+    fields = np.ascontiguousarray(g.normal(size=(n, nf))) if nf else None
+    vals = g.normal(size=n)
+    weight = float(g.uniform(0.1, 50))
+    normalize = bool(seed % 2)
+
+    class B:
+        pass
+    h = B()
+    h.X, h.terms, h.weight, h.values, h.fields = X, terms, weight, vals, fields
+    dv = fls.Block(torch.from_numpy(X).cuda(), terms, weight, torch.from_numpy(vals).cuda(),
+                   torch.from_numpy(fields).cuda() if nf else None)
+    Ab, lda = fls.fls_assemble(ctx, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(), [dv],
+                               normalize=normalize)
+    fls.fls_sync(ctx)
+    Ao, ro, S = oracle.assemble(W, b, [h], normalize=normalize)
+    Ag, rg = rows_from_colmajor(Ab, lda, F, np.arange(n))
+    emax, _ = scaled_err(Ag, Ao, S)
+    assert emax <= ENTRY_TOL, (emax, d, terms)
+    assert np.array_equal(rg, ro)
+
+
 @pytest.mark.parametrize("d", [1, 2, 4, 6, 8])
 def test_all_dims(ctx, d):
     _mode_case(ctx, wl.op_laplacian(d, -1.0) + wl.op_identity(d, 2.0), d=d, F=150, n=300, seed=d)
