@@ -17,6 +17,8 @@
 //   kFUnroll features per loop iteration (2*kPairs*kFUnroll independent entries per thread)
 //   for FP64-pipe ILP; full tiles run a predicate-free loop, ragged tiles a masked one.
 #pragma once
+#include <stdlib.h>
+
 #include "fls_device.cuh"
 #include "fls_internal.h"
 
@@ -78,12 +80,16 @@ constexpr int asm_min_blocks() {
 // when the block's point data exceed 32 MB and would not stay in L2 between groups).
 template <int D, int G, int KM>
 inline dim3 asm_grid(AsmArgs &a) {
-  static int sms = 0;
+  static int sms = 0, waves = 8;
   if (!sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
+    if (const char *w = getenv("FLS_ASM_WAVES")) {  // tuning sweeps only
+      const int v = atoi(w);
+      if (v >= 1 && v <= 64) waves = v;
+    }
   }
   const int64_t span = a.lr1 - (a.lr0 & ~int64_t(1));
   const int64_t rt = (span + kRowsCTA - 1) / kRowsCTA;
@@ -91,15 +97,15 @@ inline dim3 asm_grid(AsmArgs &a) {
   const bool big_x = span * (D + G + 1) * 8 > ((int64_t)32 << 20);
   const int64_t min_fpc = big_x ? (a.F < kFC ? a.F : kFC) : (a.F < 16 ? a.F : 16);
   const int64_t gmax = (a.F + min_fpc - 1) / min_fpc;
-  int64_t g0 = (8 * resident + rt - 1) / rt;
+  int64_t g0 = (waves * resident + rt - 1) / rt;
   g0 = g0 < 1 ? 1 : (g0 > gmax ? gmax : g0);
   int64_t best = g0;
   double best_eff = -1.0;
   for (int64_t g = g0; g <= 2 * g0 && g <= gmax; ++g) {
     const int64_t fpc = (((a.F + g - 1) / g) + 1) & ~int64_t(1);
     const int64_t gg = (a.F + fpc - 1) / fpc;
-    const double waves = (double)(rt * gg) / (double)resident;
-    const double eff = waves / ceil(waves);
+    const double nw = (double)(rt * gg) / (double)resident;
+    const double eff = nw / ceil(nw);
     if (eff > best_eff + 1e-3) {
       best_eff = eff;
       best = gg;
