@@ -75,12 +75,12 @@ constexpr int asm_min_blocks() {
 }
 
 // Launch shape: grid = (row tiles, feature groups), a.fpc features per CTA.  Picks the fewest
-// feature groups that give >= 8 waves of resident CTAs (148 SMs x asm_min_blocks), then the
+// feature groups that give >= 4 waves of resident CTAs (148 SMs x asm_min_blocks), then the
 // group count in [g, 2g] whose last wave is fullest.  Each CTA keeps >= 16 features (>= kFC
 // when the block's point data exceed 32 MB and would not stay in L2 between groups).
 template <int D, int G, int KM>
 inline dim3 asm_grid(AsmArgs &a) {
-  static int sms = 0, waves = 8;
+  static int sms = 0, waves = 4;  // tools/waves_sweep.sh: 2-4 waves best for C3, flat for C4/C5
   if (!sms) {
     int dev = 0;
     cudaGetDevice(&dev);
