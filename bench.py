@@ -304,6 +304,8 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=1024)
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
     ap.add_argument("--no-solve", action="store_true", help="skip the end-to-end solve leg")
+    ap.add_argument("--layout", default="col", choices=["col", "row"],
+                    help="A layout (col = what the QR consumes; row = features contiguous)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-ring-rows", type=int, default=262144)
     ap.add_argument("--rows", type=int, default=None,
@@ -342,8 +344,10 @@ def main():
                                 if blk.fields is not None else None))
     ctx = fls.Context(local)
     bset = fls.BlockSet(blocks, d)
-    lda = fls.round_up(n_local, 4)
-    Ab = torch.empty(((F + 1) * lda,), dtype=torch.float64, device="cuda")
+    row_major = args.layout == "row"
+    lda = fls.round_up(F, 2) if row_major else fls.round_up(n_local, 4)
+    Ab = torch.empty(((n_local if row_major else F + 1) * lda,), dtype=torch.float64, device="cuda")
+    rhs = torch.empty((n_local,), dtype=torch.float64, device="cuda") if row_major else None
     W = torch.empty((F, d), dtype=torch.float64, device="cuda")
     b = torch.empty((F,), dtype=torch.float64, device="cuda")
     # per step: features + one prefactor launch per <= 4 blocks; assembly launches are counted
@@ -352,7 +356,10 @@ def main():
 
     def step():
         fls.fls_features(ctx, d, F, p.sigma, p.seed, W, b)
-        fls.fls_assemble(ctx, W, b, bset, A=Ab, lda=lda)
+        if row_major:
+            fls.fls_assemble(ctx, W, b, bset, A=Ab, lda=lda, layout=fls.FLS_ROW_MAJOR, rhs=rhs)
+        else:
+            fls.fls_assemble(ctx, W, b, bset, A=Ab, lda=lda)
 
     for _ in range(args.warmup):
         step()
@@ -412,7 +419,8 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
                      "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                     "kernel": "assemble_cm_kernel", "kernel_ms_avg": k_avg_ms,
+                     "kernel": "assemble_rm_kernel" if row_major else "assemble_cm_kernel",
+                     "kernel_ms_avg": k_avg_ms,
                      "scope": "rank 0's GPU (per-GPU kernel roofline)"},
         "gpu_launches": launches_per_step_fixed * args.steps + k_launches,
         "clocks": clocks,
