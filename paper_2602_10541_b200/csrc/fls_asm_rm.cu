@@ -1,96 +1,132 @@
 // fls_asm_rm.cu -- row-major assembly A[i * lda + j] (features contiguous), for consumers that
-// want rows contiguous (e.g. a row-streaming normal-equations build).  Same arithmetic per
-// entry as the column-major kernel (bit-identical entries).  A warp covers 64 consecutive
-// features of one row (one 16-byte store per lane); each lane keeps its two feature records
-// in registers and the row's x_i is a broadcast load.
-#include "fls_device.cuh"
-#include "fls_internal.h"
+// want rows contiguous.  The column-major kernel with the roles of rows and features swapped:
+// each thread owns TWO consecutive features (their records in registers for the whole CTA),
+// a CTA covers 512 features x a range of rows, and the rows' x_i (and coefficient fields) are
+// staged 64 at a time in shared memory and read as warp-uniform broadcasts.  Every store
+// instruction of a warp writes 64 consecutive features = 512 contiguous bytes of one row
+// (16-byte st.global.cs per lane).  Same per-entry arithmetic (EntryMath) as the column-major
+// kernel, so both layouts hold bit-identical entries.
+#include "fls_assemble.cuh"
 
 namespace fls {
 
-template <int D>
-__global__ void __launch_bounds__(256) assemble_rm_kernel(const AsmArgs a, int G, int km, int S) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t j = (int64_t)blockIdx.y * kRmFeat + 2 * lane;
-  constexpr int MAXREC = FLS_MAX_DIM + 2 + 2 * (FLS_MAX_FIELDS + 1);
-  double rec[2][MAXREC];
+constexpr int kRmNT = 256;
+constexpr int kRmTileF = 2 * kRmNT;   // features per CTA
+constexpr int kRmChunk = 64;          // rows staged per shared-memory chunk
+
+template <int D, int G, int KM>
+__global__ void __launch_bounds__(kRmNT, asm_min_blocks<D, G, KM>()) assemble_rm_kernel(const AsmArgs a) {
+  using M = EntryMath<D, G, KM>;
+  constexpr int S = M::S;
+  constexpr int GG = G > 0 ? G : 1;
+  constexpr int RS = D + GG;          // staged doubles per row
+  __shared__ double xs[kRmChunk * RS];
+
+  const int64_t j = (int64_t)blockIdx.x * kRmTileF + 2 * threadIdx.x;
+  const bool jin0 = j < a.F, jin1 = j + 1 < a.F;
+  double rec0[S], rec1[S];
 #pragma unroll
-  for (int e = 0; e < 2; ++e) {
-    const bool ok = (j + e) < a.F;
-#pragma unroll
-    for (int s = 0; s < MAXREC; ++s) rec[e][s] = (ok && s < S) ? __ldg(a.pf + (j + e) * S + s) : 0.0;
+  for (int s = 0; s < S; ++s) {
+    rec0[s] = jin0 ? __ldg(a.pf + j * S + s) : 0.0;
+    rec1[s] = jin1 ? __ldg(a.pf + (j + 1) * S + s) : 0.0;
   }
+  const bool pair_ok = a.vec && jin1;
+  const int64_t r0 = a.lr0 + (int64_t)blockIdx.y * a.fpc;
+  const int64_t r1 = r0 + a.fpc < a.lr1 ? r0 + a.fpc : a.lr1;
   bool bad = false;
-  for (int k8 = 0; k8 < kRmRows / 8; ++k8) {
-    const int64_t r = a.lr0 + (int64_t)blockIdx.x * kRmRows + warp + 8 * k8;
-    if (r >= a.lr1) break;
-    const int64_t i = a.pt0 + (r - a.lr0);
-    double x[D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      x[k] = __ldg(a.X + i * D + k);
-      bad |= !finite(x[k]);
-    }
-    double c[FLS_MAX_FIELDS];
-#pragma unroll
-    for (int g = 0; g < FLS_MAX_FIELDS; ++g) {
-      c[g] = (g < G) ? __ldg(a.fields + i * a.nf + a.gfield[g]) : 0.0;
-      bad |= !finite(c[g]);
-    }
-    if (blockIdx.y == 0 && lane == 0 && a.rhs != nullptr) {
-      const double v = a.values ? __ldg(a.values + i) : 0.0;
+  for (int64_t rc = r0; rc < r1; rc += kRmChunk) {
+    const int nrow = (r1 - rc) < kRmChunk ? (int)(r1 - rc) : kRmChunk;
+    __syncthreads();
+    for (int t = threadIdx.x; t < nrow * RS; t += kRmNT) {
+      const int rr = t / RS, k = t % RS;
+      const int64_t i = a.pt0 + (rc + rr - a.lr0);
+      double v;
+      if (k < D) v = __ldg(a.X + i * D + k);
+      else v = G > 0 ? __ldg(a.fields + i * a.nf + a.gfield[k - D]) : 0.0;
       bad |= !finite(v);
-      a.rhs[r] = a.weight * v;
+      xs[t] = v;
     }
-    double out[2];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      double h = rec[e][D];
-#pragma unroll
-      for (int k = 0; k < D; ++k) h = fma(rec[e][k], x[k], h);
-      int sgn;
-      const double f = halfturn(h, sgn);
-      const double u = f * f;
-      if (km == KM_SIN) {
-        double P = rec[e][D + 1];
-#pragma unroll
-        for (int g = 0; g < FLS_MAX_FIELDS; ++g)
-          if (g < G) P = fma(c[g], rec[e][D + 2 + g], P);
-        out[e] = P * sinpi_core(flipsign(f, sgn), u);
-      } else {
-        double Ps = rec[e][D + 1], Pc = rec[e][D + 2];
-#pragma unroll
-        for (int g = 0; g < FLS_MAX_FIELDS; ++g)
-          if (g < G) {
-            Ps = fma(c[g], rec[e][D + 3 + 2 * g], Ps);
-            Pc = fma(c[g], rec[e][D + 4 + 2 * g], Pc);
-          }
-        out[e] = flipsign(fma(Ps, sinpi_core(f, u), Pc * cospi_core(u)), sgn);
+    if (blockIdx.x == 0 && a.rhs != nullptr) {
+      for (int rr = threadIdx.x; rr < nrow; rr += kRmNT) {
+        const int64_t i = a.pt0 + (rc + rr - a.lr0);
+        const double v = a.values ? __ldg(a.values + i) : 0.0;
+        bad |= !finite(v);
+        a.rhs[rc + rr] = a.weight * v;
       }
     }
-    double *dst = a.A + r * a.lda + j;
-    if (a.vec && j + 1 < a.F) {
-      __stcs(reinterpret_cast<double2 *>(dst), make_double2(out[0], out[1]));
-    } else {
-      if (j < a.F) __stcs(dst, out[0]);
-      if (j + 1 < a.F) __stcs(dst + 1, out[1]);
+    __syncthreads();
+    for (int rr = 0; rr < nrow; ++rr) {
+      double x[D], c[GG];
+#pragma unroll
+      for (int k = 0; k < D; ++k) x[k] = xs[rr * RS + k];
+#pragma unroll
+      for (int g = 0; g < GG; ++g) c[g] = G > 0 ? xs[rr * RS + D + g] : 0.0;
+      const double o0 = M::entry(rec0, x, c);
+      const double o1 = M::entry(rec1, x, c);
+      double *dst = a.A + (rc + rr) * a.lda + j;
+      if (pair_ok) {
+        __stcs(reinterpret_cast<double2 *>(dst), make_double2(o0, o1));
+      } else {
+        if (jin0) __stcs(dst, o0);
+        if (jin1) __stcs(dst + 1, o1);
+      }
     }
   }
   if (bad) atomicOr(a.err, 1u);
 }
 
-cudaError_t launch_assemble_rm(int D, int G, int kmode, const AsmArgs &a, cudaStream_t st) {
-  const int S = pf_stride(D, G, kmode);
-  const dim3 grid((unsigned)((a.lr1 - a.lr0 + kRmRows - 1) / kRmRows),
-                  (unsigned)((a.F + kRmFeat - 1) / kRmFeat));
-  switch (D) {
-#define FLS_RM(d) \
-  case d: assemble_rm_kernel<d><<<grid, 256, 0, st>>>(a, G, kmode, S); break;
-    FLS_RM(1) FLS_RM(2) FLS_RM(3) FLS_RM(4) FLS_RM(5) FLS_RM(6) FLS_RM(7) FLS_RM(8)
-#undef FLS_RM
-    default: return cudaErrorInvalidValue;
+template <int D, int G, int KM>
+static cudaError_t go_rm(const AsmArgs &a0, cudaStream_t st) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
   }
+  AsmArgs a = a0;
+  const int64_t rows = a.lr1 - a.lr0;
+  const int64_t ft = (a.F + kRmTileF - 1) / kRmTileF;
+  const int64_t resident = (int64_t)sms * asm_min_blocks<D, G, KM>();
+  // >= 4 waves of CTAs, >= 64 rows per CTA (a.fpc = rows per CTA in this kernel)
+  int64_t g = (4 * resident + ft - 1) / ft;
+  const int64_t gmax = (rows + kRmChunk - 1) / kRmChunk;
+  g = g < 1 ? 1 : (g > gmax ? gmax : g);
+  a.fpc = (rows + g - 1) / g;
+  const dim3 grid((unsigned)ft, (unsigned)((rows + a.fpc - 1) / a.fpc));
+  assemble_rm_kernel<D, G, KM><<<grid, kRmNT, 0, st>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_assemble_rm(int D, int G, int kmode, const AsmArgs &a, cudaStream_t st) {
+#define FLS_RM_G(d, km)                              \
+  switch (G) {                                       \
+    case 0: return go_rm<d, 0, km>(a, st);           \
+    case 1: return go_rm<d, 1, km>(a, st);           \
+    case 2: return go_rm<d, 2, km>(a, st);           \
+    case 3: return go_rm<d, 3, km>(a, st);           \
+    case 4: return go_rm<d, 4, km>(a, st);           \
+    default: return cudaErrorInvalidValue;           \
+  }
+#define FLS_RM_D(km)                                 \
+  switch (D) {                                       \
+    case 1: FLS_RM_G(1, km)                          \
+    case 2: FLS_RM_G(2, km)                          \
+    case 3: FLS_RM_G(3, km)                          \
+    case 4: FLS_RM_G(4, km)                          \
+    case 5: FLS_RM_G(5, km)                          \
+    case 6: FLS_RM_G(6, km)                          \
+    case 7: FLS_RM_G(7, km)                          \
+    case 8: FLS_RM_G(8, km)                          \
+    default: return cudaErrorInvalidValue;           \
+  }
+  if (kmode == KM_SIN) {
+    FLS_RM_D(KM_SIN)
+  } else {
+    FLS_RM_D(KM_SINCOS)
+  }
+#undef FLS_RM_D
+#undef FLS_RM_G
 }
 
 cudaError_t launch_assemble_cm_sin(int D, int G, AsmArgs *blks, int n, cudaStream_t st);
