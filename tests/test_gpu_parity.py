@@ -307,6 +307,37 @@ def test_error_paths(ctx):
         fls.fls_solve(ctx, M, 8, 8, 2)
 
 
+def test_error_paths_extended(ctx):
+    """argument errors of the non-assembly entry points return FLS_EINVAL / FLS_EUNSUPPORTED"""
+    from paper_2602_10541_b200._abi import FlsError
+    dev = "cuda"
+    with pytest.raises(FlsError, match="EINVAL"):
+        fls.fls_sample_box(ctx, 2, 10, [0, 1], [1, 1], seed=0)          # lo == hi on axis 1
+    with pytest.raises(FlsError, match="EINVAL"):
+        fls.fls_features_blocks(ctx, 2, [10, 0], [1.0, 2.0], 0)         # empty block
+    with pytest.raises(FlsError, match="EINVAL"):
+        fls.fls_features_blocks(ctx, 2, [10], [-1.0], 0)
+    A = torch.randn(10 * 3, dtype=torch.float64, device=dev)
+    with pytest.raises(FlsError, match="EINVAL"):
+        fls.QRFactor(ctx, A, 2, 10, 3)                                   # 2 rows < 3 features
+    u = torch.zeros(5, dtype=torch.float64, device=dev)
+    bad = fls.make_nonlinearity("poly", [0.0] * 3)
+    bad.degree = 9
+    with pytest.raises(FlsError, match="EINVAL"):
+        fls.fls_nl_residual(ctx, bad, u, u, u)
+    X = torch.rand((20, 2), dtype=torch.float64, device=dev)
+    W = torch.randn((7, 2), dtype=torch.float64, device=dev)
+    b = torch.rand(7, dtype=torch.float64, device=dev)
+    blk = fls.Block(X, [((0, 0), 1.0, 0)], 1.0, torch.zeros(20, dtype=torch.float64, device=dev),
+                    torch.ones((20, 1), dtype=torch.float64, device=dev))
+    with pytest.raises(FlsError, match="EUNSUPPORTED"):
+        fls.fls_bandwidth_grad(ctx, W, W, b, [blk], torch.zeros(7, dtype=torch.float64, device=dev))
+    with pytest.raises(FlsError, match="EINVAL"):                        # eval op with a field
+        fls.fls_eval(ctx, W, b, torch.zeros(7, dtype=torch.float64, device=dev), X,
+                     terms=[((0, 0), 1.0, 0)])
+    fls.fls_sync(ctx)
+
+
 # ------------------------------------------------------------------------------------- solve + eval
 @pytest.mark.parametrize("name,size", [("c1_poisson1d", "full"), ("c2_poisson2d", "full"),
                                        ("c3_poisson5d", "mini"), ("c4_heat2d", "mini"),
