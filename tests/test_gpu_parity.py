@@ -336,6 +336,14 @@ def test_error_paths_extended(ctx):
         fls.fls_eval(ctx, W, b, torch.zeros(7, dtype=torch.float64, device=dev), X,
                      terms=[((0, 0), 1.0, 0)])
     fls.fls_sync(ctx)
+    # FLS_ENOMEM: a workspace request far beyond the device (10^10 features), raw ABI call
+    import ctypes as C
+    from paper_2602_10541_b200 import _abi
+    bs = fls.BlockSet([fls.Block(X, [((2, 0), 1.0, -1)], 1.0, None)], 2)
+    A = torch.empty(64, dtype=torch.float64, device=dev)
+    st = _abi.load().fls_assemble(ctx.handle, C.c_void_p(W.data_ptr()), C.c_void_p(b.data_ptr()), 2,
+                                  10 ** 10, 1, bs.arr, 1, 0, 20, C.c_void_p(A.data_ptr()), 20, 0, None)
+    assert _abi.STATUS[st] == "FLS_ENOMEM", _abi.load().fls_last_error()
 
 
 # ------------------------------------------------------------------------------------- solve + eval
