@@ -239,6 +239,27 @@ def test_sign_and_index_errors_would_fail():
     assert abs(A[0, 0] - (-(1.7 * -0.4) * math.sin(z))) < 1e-14
 
 
+def test_linearity_in_the_operator():
+    """pin: L -> A is linear: A(a L1 + b L2) = a A(L1) + b A(L2) to rounding"""
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+
+    @settings(max_examples=25, deadline=None)
+    @given(st.integers(1, 4), st.floats(-3, 3), st.floats(-3, 3), st.integers(0, 10_000))
+    def check(d, ca, cb, seed):
+        g = np.random.default_rng(seed)
+        W, b = rand_basis(d, 17, 2.0, seed)
+        X = g.random((9, d))
+        L1 = [(tuple(int(v) for v in g.integers(0, 3, d)), float(g.normal()), -1) for _ in range(2)]
+        L2 = [(tuple(int(v) for v in g.integers(0, 3, d)), float(g.normal()), -1) for _ in range(3)]
+        A1, S1 = col(W, b, X, L1)
+        A2, S2 = col(W, b, X, L2)
+        A12, _ = col(W, b, X, [(a, ca * c, f) for a, c, f in L1] + [(a, cb * c, f) for a, c, f in L2])
+        scale = abs(ca) * S1 + abs(cb) * S2
+        assert np.all(np.abs(A12 - (ca * A1 + cb * A2)) <= 1e-13 * np.maximum(scale, 1e-300) + 1e-300)
+    check()
+
+
 # ----------------------------------------------------------------------------- blocks / fields
 def test_row_blocks_lambda_and_rhs():
     """pins: Eq. 3 row order pde -> bc and weights on both A and b; doubling lambda
