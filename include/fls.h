@@ -276,6 +276,17 @@ typedef struct {
 FLS_API fls_status fls_nl_residual(fls_ctx *ctx, const fls_nonlinearity *nl, int64_t n,
                                    const double *Lu, const double *u, const double *u_prev,
                                    const double *f, double *neg_res, double *dN, double *stats);
+/* Quasi-linear nonlinearities that also depend on one derivative Du = D^e u of the solution
+ * (steady Burgers u u_x): kind FLS_NL_UDU, N(u, Du) = a[0] u Du.  For i < n:
+ *   neg_res_i = f_i - Lu_i - N(u_i, Du_i),  dN_du_i = dN/du,  dN_dDu_i = dN/dDu
+ * (the Jacobian gets dN_du on the identity term and dN_dDu on the D^e term).
+ * Du may be NULL for the pointwise kinds (then dN_dDu is not written).  stats as for
+ * fls_nl_residual.  fls_nl_residual(...) == fls_nl_residual2(..., Du = NULL, dN_dDu = NULL). */
+#define FLS_NL_UDU 3
+FLS_API fls_status fls_nl_residual2(fls_ctx *ctx, const fls_nonlinearity *nl, int64_t n,
+                                    const double *Lu, const double *u, const double *Du,
+                                    const double *u_prev, const double *f, double *neg_res,
+                                    double *dN_du, double *dN_dDu, double *stats);
 /* out_i = y_i + alpha * x_i for i < n (the Newton update beta + alpha delta, Eq. 4).
  * Device vectors; out may alias y or x.  Asynchronous. */
 FLS_API fls_status fls_axpy(fls_ctx *ctx, int64_t n, double alpha, const double *x,

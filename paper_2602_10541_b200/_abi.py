@@ -48,6 +48,7 @@ class fls_block(C.Structure):
 
 FLS_NL_POLY = 1
 FLS_NL_EXP = 2
+FLS_NL_UDU = 3
 
 
 class fls_nonlinearity(C.Structure):
@@ -88,6 +89,9 @@ _SIGS = {
     "fls_bandwidth_grad": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                      C.c_int64, C.c_int32, C.POINTER(fls_block), C.c_int32,
                                      C.c_void_p, C.c_void_p]),
+    "fls_nl_residual2": (C.c_int, [C.c_void_p, C.POINTER(fls_nonlinearity), C.c_int64, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_void_p]),
     "fls_axpy": (C.c_int, [C.c_void_p, C.c_int64, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     "fls_assemble_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64,
                                     C.c_int32, C.POINTER(fls_block), C.c_int32, C.c_int64,

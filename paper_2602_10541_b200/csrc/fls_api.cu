@@ -1010,10 +1010,19 @@ fls_status fls_bandwidth_grad(fls_ctx *ctx, const double *W, const double *W_hat
 fls_status fls_nl_residual(fls_ctx *ctx, const fls_nonlinearity *nl, int64_t n, const double *Lu,
                            const double *u, const double *u_prev, const double *f,
                            double *neg_res, double *dN, double *stats) {
+  return fls_nl_residual2(ctx, nl, n, Lu, u, nullptr, u_prev, f, neg_res, dN, nullptr, stats);
+}
+
+fls_status fls_nl_residual2(fls_ctx *ctx, const fls_nonlinearity *nl, int64_t n, const double *Lu,
+                            const double *u, const double *Du, const double *u_prev,
+                            const double *f, double *neg_res, double *dN, double *dN_dDu,
+                            double *stats) {
   if (fls_status s = check_ctx(ctx)) return s;
   if (!nl) return fail(FLS_EINVAL, "nl is NULL");
-  if (nl->kind != FLS_NL_POLY && nl->kind != FLS_NL_EXP)
+  if (nl->kind != FLS_NL_POLY && nl->kind != FLS_NL_EXP && nl->kind != FLS_NL_UDU)
     return fail(FLS_EINVAL, "nonlinearity kind %d unknown", nl->kind);
+  if (nl->kind == FLS_NL_UDU && n > 0 && !Du)
+    return fail(FLS_EINVAL, "FLS_NL_UDU needs the derivative vector Du");
   if (nl->kind == FLS_NL_POLY && (nl->degree < 0 || nl->degree > 7))
     return fail(FLS_EINVAL, "polynomial degree %d not in 0..7", nl->degree);
   for (int k = 0; k < 8; ++k)
@@ -1033,6 +1042,8 @@ fls_status fls_nl_residual(fls_ctx *ctx, const fls_nonlinearity *nl, int64_t n, 
   a.f = f;
   a.neg_res = neg_res;
   a.dN = dN;
+  a.Du = Du;
+  a.dN2 = dN_dDu;
   a.partials = ctx->d_scratch + 8;
   a.err = ctx->d_err;
   const int nblk = 296;  // 2 x 148 SMs, fixed -> deterministic sums

@@ -144,6 +144,8 @@ struct NlArgs {
   const double *Lu, *u, *u_prev, *f;
   double *neg_res, *dN, *partials;
   unsigned *err;
+  const double *Du;  // FLS_NL_UDU: the derivative D^e u
+  double *dN2;       // FLS_NL_UDU: dN/dDu
 };
 cudaError_t launch_nl_residual(const NlArgs &a, int nblk, double *stats, cudaStream_t st);
 

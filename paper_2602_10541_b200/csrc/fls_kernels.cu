@@ -390,7 +390,14 @@ __global__ void nl_residual_kernel(const NlArgs a) {
        i += (int64_t)gridDim.x * blockDim.x) {
     const double u = a.u[i];
     double N, dN;
-    nl_eval(a, u, N, dN);
+    if (a.kind == 3) {  // a0 u Du (Burgers-type quasi-linear term)
+      const double du = a.Du[i];
+      N = a.c[0] * u * du;
+      dN = a.c[0] * du;
+      if (a.dN2) a.dN2[i] = a.c[0] * u;
+    } else {
+      nl_eval(a, u, N, dN);
+    }
     const double r = a.f[i] - a.Lu[i] - N;
     bad |= !finite(r) || !finite(dN);
     a.neg_res[i] = r;

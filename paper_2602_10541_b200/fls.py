@@ -155,6 +155,9 @@ def make_nonlinearity(kind: str, coefs: Sequence[float]):
     elif kind == "exp":
         nl.kind = _abi.FLS_NL_EXP
         nl.degree = 1
+    elif kind == "udu":                 # coefs[0] * u * D^e u  (Burgers u u_x)
+        nl.kind = _abi.FLS_NL_UDU
+        nl.degree = 1
     else:
         raise ValueError(kind)
     for k, v in enumerate(coefs):
@@ -173,6 +176,18 @@ def fls_nl_residual(ctx: Context, nl, Lu: torch.Tensor, u: torch.Tensor, f: torc
     check(_abi.load().fls_nl_residual(ctx.handle, C.byref(nl), n, _ptr(Lu), _ptr(u), _ptr(u_prev),
                                       _ptr(f), _ptr(neg_res), _ptr(dN), st if stats else None))
     return neg_res, dN, (st[0], st[1], st[2])
+
+
+def fls_nl_residual2(ctx: Context, nl, Lu: torch.Tensor, u: torch.Tensor, Du: torch.Tensor,
+                     f: torch.Tensor, u_prev: Optional[torch.Tensor] = None, stats: bool = True):
+    """quasi-linear N(u, Du): returns (neg_res, dN/du, dN/dDu, sums of squares)"""
+    n = int(u.numel())
+    neg_res, dN, dN2 = torch.empty_like(u), torch.empty_like(u), torch.empty_like(u)
+    st = (C.c_double * 3)()
+    check(_abi.load().fls_nl_residual2(ctx.handle, C.byref(nl), n, _ptr(Lu), _ptr(u), _ptr(Du),
+                                       _ptr(u_prev), _ptr(f), _ptr(neg_res), _ptr(dN), _ptr(dN2),
+                                       st if stats else None))
+    return neg_res, dN, dN2, (st[0], st[1], st[2])
 
 
 def fls_axpy(ctx: Context, alpha: float, x: torch.Tensor, y: torch.Tensor,

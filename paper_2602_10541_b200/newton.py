@@ -1,18 +1,22 @@
-"""Newton-Raphson for nonlinear PDEs  L[u] + N(u) = f  (Eq. 4-5) on the device.
+"""Newton-Raphson for nonlinear PDEs  L[u] + N(u, Du) = f  (Eq. 4-5) on the device.
 
 Host orchestration only; every arithmetic step is a libfls call:
-  u, L[u_N] at the collocation points   fls_eval (identity / operator; A never materialised)
-  -R and N'(u)                          fls_nl_residual (pointwise N, deterministic norms)
-  J = [L + N'(u) I ; lam I] rows        fls_assemble (the N' term is one coefficient field)
+  u, L[u_N], D^e u_N at the points      fls_eval (identity / operator; A never materialised)
+  -R and the N' fields                  fls_nl_residual / fls_nl_residual2
+  J = [L + N_u I + N_Du D^e ; lam I]    fls_assemble (each N' term is one coefficient field)
   delta = argmin |J d + R|^2 + mu |d|^2 fls_solve (Householder QR with sqrt(mu) I rows)
   beta + alpha delta                    fls_axpy
 Warm start from the linear part, Armijo backtracking on the residual norm, stop on
-||du|| / ||u|| at the collocation points (readings N1-N5 in DESIGN.md §3).
+||du|| / ||u|| at the collocation points, and continuation (homotopy) over a parameter
+schedule for advection-dominated problems (readings N1-N5 in DESIGN.md §3).
+
+Nonlinearities: ('poly', [a0, a1, ...]) = sum_k a_k u^k; ('exp', [a0, a1]) = a0 exp(a1 u);
+('udu', [a0], alpha) = a0 u D^alpha u (steady Burgers u u_x with alpha = e_x).
 """
 from __future__ import annotations
 
 import math
-from typing import List, Sequence
+from typing import Callable, List, Optional, Sequence
 
 import torch
 
@@ -20,27 +24,42 @@ from . import fls
 
 
 def solve_nonlinear(ctx: fls.Context, W: torch.Tensor, b: torch.Tensor, pde: fls.Block,
-                    bcs: Sequence[fls.Block], nl_kind: str, nl_coefs: Sequence[float], *,
-                    mu: float = 1e-10, max_iter: int = 30, tol: float = 1e-10,
-                    c_armijo: float = 1e-4, max_halvings: int = 30):
+                    bcs: Sequence[fls.Block], nl_kind: str, nl_coefs: Sequence[float],
+                    nl_alpha: Optional[Sequence[int]] = None, *, mu: float = 1e-10,
+                    max_iter: int = 30, tol: float = 1e-10, c_armijo: float = 1e-4,
+                    max_halvings: int = 30, beta0: Optional[torch.Tensor] = None):
     """Returns (beta, history).  pde.values = f, bc.values = g; pde.terms = L (constant
-    coefficients); every bc block's operator is evaluated as the identity (Dirichlet rows)."""
+    coefficients); bc blocks are evaluated as the identity (Dirichlet rows).  beta0: start
+    from these coefficients instead of the linear warm start (continuation)."""
     F, d = int(W.shape[0]), int(W.shape[1])
     nl = fls.make_nonlinearity(nl_kind, nl_coefs)
+    quasi = nl_kind == "udu"
+    if quasi and nl_alpha is None:
+        raise ValueError("'udu' needs nl_alpha (the derivative D^alpha in a0 u D^alpha u)")
+    d_terms = [(tuple(nl_alpha), 1.0, -1)] if quasi else None
     zero_nl = fls.make_nonlinearity("poly", [0.0])
     sq = math.sqrt(mu)
     R = pde.n + sum(bc.n for bc in bcs)
     lda = fls.round_up(R + F, 4)
     Ab = torch.empty(((F + 1) * lda,), dtype=torch.float64, device=W.device)
-    # warm start: the linear part (N dropped), one Tikhonov-regularised solve
-    fls.fls_assemble(ctx, W, b, [pde] + list(bcs), A=Ab, lda=lda)
-    beta, _ = fls.fls_solve(ctx, Ab, R, lda, F, sq)
+    if beta0 is None:
+        # warm start: the linear part (N dropped), one Tikhonov-regularised solve
+        fls.fls_assemble(ctx, W, b, [pde] + list(bcs), A=Ab, lda=lda)
+        beta, _ = fls.fls_solve(ctx, Ab, R, lda, F, sq)
+    else:
+        beta = beta0.clone()
     zero = tuple([0] * d)
 
     def state(beta, u_prev=None):
         u = fls.fls_eval(ctx, W, b, beta, pde.X)
         Lu = fls.fls_eval(ctx, W, b, beta, pde.X, terms=pde.terms)
-        neg, dN, st = fls.fls_nl_residual(ctx, nl, Lu, u, pde.values, u_prev=u_prev)
+        if quasi:
+            Du = fls.fls_eval(ctx, W, b, beta, pde.X, terms=d_terms)
+            neg, dN, dN2, st = fls.fls_nl_residual2(ctx, nl, Lu, u, Du, pde.values, u_prev=u_prev)
+            fields = [dN, dN2]
+        else:
+            neg, dN, st = fls.fls_nl_residual(ctx, nl, Lu, u, pde.values, u_prev=u_prev)
+            fields = [dN]
         r2 = st[0]
         negs = [neg]
         for bc in bcs:
@@ -48,27 +67,45 @@ def solve_nonlinear(ctx: fls.Context, W: torch.Tensor, b: torch.Tensor, pde: fls
             nb, _, stb = fls.fls_nl_residual(ctx, zero_nl, ub, ub, bc.values)
             negs.append(nb)
             r2 += bc.weight ** 2 * stb[0]
-        return u, dN, negs, math.sqrt(r2), st
+        return u, fields, negs, math.sqrt(r2), st
 
-    u, dN, negs, rn, _ = state(beta)
+    u, fields, negs, rn, _ = state(beta)
     hist: List[dict] = [{"resid": rn, "alpha": None, "du_rel": None}]
     for _ in range(max_iter):
-        fields = dN.view(-1, 1) if pde.fields is None else torch.cat([pde.fields, dN.view(-1, 1)], 1)
-        gid = 0 if pde.fields is None else int(pde.fields.shape[1])
-        J = [fls.Block(pde.X, list(pde.terms) + [(zero, 1.0, gid)], 1.0, negs[0], fields.contiguous())]
+        base = 0 if pde.fields is None else int(pde.fields.shape[1])
+        cols = ([pde.fields] if pde.fields is not None else []) + [f.view(-1, 1) for f in fields]
+        jac_terms = list(pde.terms) + [(zero, 1.0, base)]
+        if quasi:
+            jac_terms.append((tuple(nl_alpha), 1.0, base + 1))
+        J = [fls.Block(pde.X, jac_terms, 1.0, negs[0], torch.cat(cols, 1).contiguous())]
         J += [fls.Block(bc.X, bc.terms, bc.weight, nb) for bc, nb in zip(bcs, negs[1:])]
         fls.fls_assemble(ctx, W, b, J, A=Ab, lda=lda)
         delta, _ = fls.fls_solve(ctx, Ab, R, lda, F, sq)
         alpha = 1.0
         for _h in range(max_halvings):
             trial = fls.fls_axpy(ctx, alpha, delta, beta)
-            u_t, dN_t, negs_t, rn_t, st_t = state(trial, u_prev=u)
+            u_t, fields_t, negs_t, rn_t, st_t = state(trial, u_prev=u)
             if rn_t <= (1.0 - c_armijo * alpha) * rn:
                 break
             alpha *= 0.5
         du = math.sqrt(st_t[2]) / max(math.sqrt(st_t[1]), 1e-300)
-        beta, u, dN, negs, rn = trial, u_t, dN_t, negs_t, rn_t
+        beta, u, fields, negs, rn = trial, u_t, fields_t, negs_t, rn_t
         hist.append({"resid": rn, "alpha": alpha, "du_rel": du})
         if du < tol:
             break
     return beta, hist
+
+
+def solve_continuation(ctx: fls.Context, W: torch.Tensor, b: torch.Tensor,
+                       make_pde: Callable[[float], fls.Block], bcs: Sequence[fls.Block],
+                       nl_kind: str, nl_coefs: Sequence[float], schedule: Sequence[float],
+                       nl_alpha: Optional[Sequence[int]] = None, **kw):
+    """Continuation / homotopy: solve along the parameter schedule (e.g. viscosity
+    1.0 -> 0.5 -> 0.2 -> 0.1), each stage warm-started from the previous stage's beta.
+    Returns (beta, [history per stage])."""
+    beta, hists = None, []
+    for p in schedule:
+        beta, h = solve_nonlinear(ctx, W, b, make_pde(p), bcs, nl_kind, nl_coefs, nl_alpha,
+                                  beta0=beta, **kw)
+        hists.append(h)
+    return beta, hists

@@ -59,3 +59,42 @@ def test_newton_parity_with_oracle(ctx, name):
         assert abs(h["resid"] - ho["resid"]) <= 1e-6 * ho["resid"] + 1e-9
     us = p.u_star(Xt)
     assert np.linalg.norm(u_gpu - us) / np.linalg.norm(us) < 1e-6
+
+
+def test_burgers_continuation_parity(ctx):
+    """quasi-linear N = u u_x (FLS_NL_UDU) + continuation nu = 1 -> 0.5 -> 0.2:
+    GPU vs oracle after the same schedule, and both vs u* = -tanh(x / 0.4)"""
+    from paper_2602_10541_b200.newton import solve_continuation
+    p, mk = wl.make_burgers1d()
+    W, b = p.parity_features()
+    Wd, bd = torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda()
+    bcs = dev_blocks(p)[1:]
+
+    def mk_dev(nu):
+        blk = mk(nu)
+        return fls.Block(torch.from_numpy(blk.X).cuda(), blk.terms, blk.weight,
+                         torch.from_numpy(blk.values).cuda())
+    beta, hs = solve_continuation(ctx, Wd, bd, mk_dev, bcs, "udu", [1.0], [1.0, 0.5, 0.2],
+                                  nl_alpha=(1,), max_iter=8, tol=1e-9)
+    beta_o, hs_o = on.continuation(W, b, mk, p.blocks[1:], p.nl, [1.0, 0.5, 0.2], max_iter=8,
+                                   tol=1e-9)
+    Xt = p.test_points(1000)
+    u_gpu = fls.fls_eval(ctx, Wd, bd, beta, torch.from_numpy(Xt).cuda()).cpu().numpy()
+    u_orc = oracle.evaluate(W, b, beta_o, Xt)
+    assert np.linalg.norm(u_gpu - u_orc) / np.linalg.norm(u_orc) <= U_TOL
+    us = p.u_star(Xt)
+    assert np.linalg.norm(u_gpu - us) / np.linalg.norm(us) < 1e-5
+    assert [len(h) for h in hs] == [len(h) for h in hs_o] or all(abs(len(a) - len(c)) <= 1 for a, c in zip(hs, hs_o))
+
+
+def test_udu_residual_kernel(ctx):
+    g = np.random.default_rng(3)
+    n = 5003
+    u, Lu, Du, f = (g.normal(size=n) for _ in range(4))
+    T = [torch.from_numpy(v).cuda() for v in (u, Lu, Du, f)]
+    neg, dNu, dNd, st = fls.fls_nl_residual2(ctx, fls.make_nonlinearity("udu", [0.7]), T[1], T[0],
+                                             T[2], T[3])
+    ref = f - Lu - 0.7 * u * Du
+    assert np.allclose(neg.cpu().numpy(), ref, rtol=1e-14, atol=1e-14)
+    assert np.allclose(dNu.cpu().numpy(), 0.7 * Du, rtol=1e-15, atol=0)
+    assert np.allclose(dNd.cpu().numpy(), 0.7 * u, rtol=1e-15, atol=0)

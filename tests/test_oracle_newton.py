@@ -63,3 +63,16 @@ def test_lstsq_mu_matches_stacked_library():
     ref, *_ = np.linalg.lstsq(np.vstack([A, sq * np.eye(12)]), np.concatenate([bv, np.zeros(12)]),
                               rcond=None)
     assert np.allclose(beta, ref, rtol=1e-10, atol=1e-12)
+
+
+def test_burgers_continuation_recovers_exact_solution():
+    """pin: closed form -- steady viscous Burgers -nu u'' + u u' = 0 has u* = -tanh(x/(2 nu));
+    continuation nu = 1 -> 0.5 -> 0.2 with the quasi-linear u u_x Jacobian."""
+    p, mk = wl.make_burgers1d()
+    W, b = p.parity_features()
+    beta, hs = on.continuation(W, b, mk, p.blocks[1:], p.nl, [1.0, 0.5, 0.2], max_iter=8, tol=1e-9)
+    Xt = p.test_points(1000)
+    u = oracle.evaluate(W, b, beta, Xt)
+    us = p.u_star(Xt)
+    assert np.linalg.norm(u - us) / np.linalg.norm(us) < 1e-5
+    assert len(hs) == 3 and hs[-1][-1]["resid"] < hs[-1][0]["resid"]

@@ -308,6 +308,28 @@ def make_nl_problem(name: str, n_int: int = 1500, per_edge: int = 100, n_feature
     return p
 
 
+def make_burgers1d(nu_final: float = 0.2, n_int: int = 400, n_features: int = 200,
+                   sigma: float = 8.0, seed: int = 0):
+    """Steady viscous Burgers  -nu u'' + u u' = 0  on [-1, 1] (the paper's continuation case,
+    P:L167), Dirichlet rows u(-1) = -u(1) = tanh(1/(2 nu_final)) (lambda = 100) so that
+    u* = -tanh(x / (2 nu_final)) solves the final stage exactly.  Returns (problem, make_pde):
+    make_pde(nu) gives the PDE block for one continuation stage (f = 0)."""
+    gi = rng(seed, STREAM_INTERIOR)
+    lo, hi = np.array([-1.0]), np.array([1.0])
+    Xi = _c(_uniform_box(gi, n_int, lo, hi))
+    Xb = np.array([[-1.0], [1.0]])
+
+    def u(X):
+        return -np.tanh(X[:, 0] / (2.0 * nu_final))
+
+    def make_pde(nu):
+        return Block("pde", Xi, op_partial(1, 0, 2, -float(nu)), 1.0, np.zeros(n_int))
+    blocks = [make_pde(nu_final), Block("bc", _c(Xb), op_identity(1), 100.0, _c(u(Xb)))]
+    p = Problem("burgers1d", 1, n_features, sigma, blocks, u, lo, hi, 0.0, seed)
+    p.nl = ("udu", [1.0], (1,))
+    return p, make_pde
+
+
 def make_helmholtz2d(n_int: int = 600, per_edge: int = 40, n_features: int = 120, k: float = 10.0,
                      seed: int = 0) -> Problem:
     """Helmholtz 2D (the paper's learnable-bandwidth demonstration case):
