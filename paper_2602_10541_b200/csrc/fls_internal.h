@@ -33,8 +33,6 @@ constexpr int kPairs = FLS_PAIRS;           // 16-byte row pairs per thread
 constexpr int kFUnroll = FLS_FUNROLL;       // features per loop iteration
 constexpr int kRowsCTA = 2 * kPairs * kNT;  // rows per CTA tile
 constexpr int kFC = 128;                    // features per shared-memory chunk
-constexpr int kRmRows = 64;        // rows per CTA, row-major assembly
-constexpr int kRmFeat = 64;        // features per CTA (2 per lane), row-major assembly
 
 struct TermDev {
   double coef;
