@@ -66,6 +66,7 @@ def lib():
         L.orc_eval.argtypes =[C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
                                C.c_void_p, C.c_int64, C.c_void_p]
         L.orc_max_threads.restype = C.c_int
+        L.orc_set_threads.argtypes = [C.c_int]
     return _lib
 
 
@@ -79,6 +80,10 @@ def _f64(a) -> np.ndarray:
 
 def max_threads() -> int:
     return int(lib().orc_max_threads())
+
+
+def set_threads(n: int) -> None:
+    lib().orc_set_threads(int(n))
 
 
 def philox4x64(ctr: Sequence[int], key: Sequence[int]) -> np.ndarray:

@@ -388,6 +388,16 @@ int orc_eval(int dim, int64_t n_features, const double *W, const double *b, int 
     return 0;
 }
 
+/* thread count of the OpenMP loops (cpu_baseline reports 1 thread and all host threads) */
+void orc_set_threads(int n) {
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int orc_max_threads(void) {
 #ifdef _OPENMP
     extern int omp_get_max_threads(void);
