@@ -7,8 +7,7 @@ namespace fls {
 template <int D, int G>
 static cudaError_t go_sin(AsmArgs *blks, int n, cudaStream_t st) {
   constexpr int S = pf_stride(D, G, KM_SIN);
-  const size_t smem = (size_t)kFC * S * sizeof(double) +
-                      (FLS_TMA_STORE ? (size_t)(kNT / 32) * 2 * kFUnroll * kPairs * 64 * sizeof(double) : 0);
+  const size_t smem = (size_t)kFC * S * sizeof(double);
   AsmBatch bt;
   bt.n = n;
   int64_t total = 0;

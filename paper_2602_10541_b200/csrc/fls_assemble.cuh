@@ -22,10 +22,6 @@
 #include "fls_device.cuh"
 #include "fls_internal.h"
 
-#ifndef FLS_TMA_STORE
-#define FLS_TMA_STORE 0  // experiment: bulk async (TMA) stores from shared-memory staging
-#endif
-
 #ifndef FLS_MINB
 #define FLS_MINB 4   // 4 CTAs x 256 threads per SM -> <= 64 registers
 #endif
@@ -168,10 +164,6 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
     }
   }
   if (bad) atomicOr(a.err, 1u);
-#if FLS_TMA_STORE
-  double *tma_stage = sp + kFC * S + (threadIdx.x >> 5) * (2 * kFUnroll * kPairs * 64);
-  int tma_buf = 0;
-#endif
 
   // this CTA's feature range [f0, f1) (a.fpc features per CTA, chosen by the launcher), walked
   // in shared-memory chunks of at most kFC records
@@ -199,44 +191,12 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
 #pragma unroll
           for (int q = 0; q < NQ; ++q) o[u][q] = M::entry(rec, x[q], c[q]);
         }
-#if FLS_TMA_STORE
-        // experiment: stage the warp's 512-byte column segments in shared memory and write
-        // them with bulk async copies (cp.async.bulk, the TMA engine) instead of STG
-        {
-          const int lane = threadIdx.x & 31;
-          double *stg = tma_stage + tma_buf * (kFUnroll * kPairs * 64);
-#pragma unroll
-          for (int u = 0; u < kFUnroll; ++u)
-#pragma unroll
-            for (int pr = 0; pr < kPairs; ++pr)
-              reinterpret_cast<double2 *>(stg + (u * kPairs + pr) * 64)[lane] =
-                  make_double2(o[u][2 * pr], o[u][2 * pr + 1]);
-          __syncwarp();
-          if (lane == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#pragma unroll
-            for (int u = 0; u < kFUnroll; ++u)
-#pragma unroll
-              for (int pr = 0; pr < kPairs; ++pr) {
-                double *g = colp + u * a.lda + pr * (2 * kNT);
-                const unsigned s = (unsigned)__cvta_generic_to_shared(stg + (u * kPairs + pr) * 64);
-                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 512;"
-                             :: "l"(g), "r"(s) : "memory");
-              }
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          }
-          __syncwarp();
-          tma_buf ^= 1;
-        }
-#else
 #pragma unroll
         for (int u = 0; u < kFUnroll; ++u)
 #pragma unroll
           for (int pr = 0; pr < kPairs; ++pr)
             __stcs(reinterpret_cast<double2 *>(colp + u * a.lda + pr * (2 * kNT)),
                    make_double2(o[u][2 * pr], o[u][2 * pr + 1]));
-#endif
       }
       for (; jj < nfe; ++jj, colp += a.lda) {
         double rec[S];
@@ -268,9 +228,6 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
       }
     }
   }
-#if FLS_TMA_STORE
-  if ((threadIdx.x & 31) == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-#endif
 }
 
 }  // namespace fls
