@@ -67,17 +67,23 @@ def main():
                                                          C.c_int64(1 << 20), 8192, 10, C.byref(res))),
             ("power_chunk_store", lambda: lib.mb_chunk_store_bw(C.c_void_p(A.data_ptr()), C.c_int64(n), 20,
                                                                 C.byref(res))),
+            ("power_dmma", lambda: lib.mb_dmma_rate(0, C.c_void_p(scratch.data_ptr()), 1_000_000,
+                                                    C.byref(res), C.byref(r2))),
+            ("power_dfma", lambda: lib.mb_dmma_rate(2, C.c_void_p(scratch.data_ptr()), 1_000_000,
+                                                    C.byref(res), C.byref(r2))),
             ("power_alu", lambda: lib.mb_entry_rate(C.c_void_p(scratch.data_ptr()), 400_000, C.byref(res))),
         ]:
             clk = ClockSampler(0)
             clk.start()
             t0 = _t.time()
-            rates = []
+            rates, rates2 = [], []
             while _t.time() - t0 < 4.0:
                 call()
                 torch.cuda.synchronize()
                 rates.append(res.value)
-            out[name] = {"rate": sum(rates) / len(rates), "clocks": clk.stop()}
+                rates2.append(r2.value)
+            out[name] = {"rate": sum(rates) / len(rates), "rate2": sum(rates2) / len(rates2),
+                         "clocks": clk.stop()}
     mhz = out["dfma_per_s_clocks"]["sm_mhz"]
     if mhz:
         out["dfma_per_clk_per_sm"] = out["dfma_per_s"] / (mhz * 1e6) / torch.cuda.get_device_properties(0).multi_processor_count
