@@ -166,6 +166,14 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _cdev():
+    """device for the timing collectives: the GPU under NCCL, the host under gloo"""
+    import torch.distributed as dist
+    if dist.is_initialized() and dist.get_backend() == "gloo":
+        return "cpu"
+    return "cuda"
+
+
 def e2e_measure(args, p, ctx, W, b, a, e, world, local):
     """The same metric through the C ABI with HOST buffers (fls_assemble_host): every step copies
     this rank's inputs (points, fields, values, W, b) from pinned host memory and every entry of
@@ -220,7 +228,7 @@ def e2e_measure(args, p, ctx, W, b, a, e, world, local):
         step()
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
-    t = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=_cdev())
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     s_step = float(t.item())
@@ -287,7 +295,7 @@ def solve_measure(args, world, rank, local):
     run()                                   # warm-up (cuSOLVER workspace, handles)
     u, res = run()
     ph = [ev[k].elapsed_time(ev[k + 1]) for k in range(4)]
-    t = torch.tensor(ph, dtype=torch.float64, device="cuda")
+    t = torch.tensor(ph, dtype=torch.float64, device=_cdev())
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ph = [float(v) for v in t.tolist()]
@@ -333,9 +341,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local %= max(1, torch.cuda.device_count())      # ranks > GPUs only in the gloo test mode
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL over NVLink; FLS_DIST_BACKEND=gloo runs the multi-rank host logic with host
+        # collectives (e.g. 2 ranks sharing one GPU in a test; no kernel waits on another rank)
+        backend = os.environ.get("FLS_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     p = wl.make_problem(args.workload, "full", **({"n_int": args.rows} if args.rows else {}))
     F, R, d = p.n_features, p.n_rows, p.dim
@@ -396,7 +411,7 @@ def main():
     ms_total = e0.elapsed_time(e1)
     k_ms, k_launches = fls.fls_ctx_timing_read(ctx)
     fls.fls_ctx_timing(ctx, False)
-    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms_total], dtype=torch.float64, device=_cdev())
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())

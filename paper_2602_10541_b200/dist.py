@@ -93,11 +93,14 @@ def tsqr_solve(Ab: torch.Tensor, n_local: int, lda: int, F: int, *, ridge_rel: f
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     dev = Ab.device
+    # collectives run on the device for NCCL; gloo (CPU tests, or FLS_DIST_BACKEND=gloo to
+    # exercise the multi-rank host logic on one GPU) exchanges host copies
+    cdev = torch.device("cpu") if (world > 1 and dist.get_backend(group) == "gloo") else dev
     nc = F + 1
     sqrt_mu = 0.0
     if ridge_rel > 0.0:
         fro2 = torch.tensor([ops.frob2(Ab, n_local, lda, F) if n_local > 0 else 0.0],
-                            dtype=torch.float64, device=dev)
+                            dtype=torch.float64, device=cdev)
         if world > 1:
             dist.all_reduce(fro2, op=dist.ReduceOp.SUM, group=group)
         sqrt_mu = ridge_rel * math.sqrt(float(fro2.item()))
@@ -114,19 +117,19 @@ def tsqr_solve(Ab: torch.Tensor, n_local: int, lda: int, F: int, *, ridge_rel: f
         Rl = R[: nc * ldr].view(nc, ldr)[:, :k]           # (nc, k): column j = R[0:k, j]
     else:
         Rl = torch.zeros((nc, 0), dtype=torch.float64, device=dev)
-    ks = torch.tensor([k], dtype=torch.int64, device=dev)
+    ks = torch.tensor([k], dtype=torch.int64, device=cdev)
     all_k = [torch.zeros_like(ks) for _ in range(world)]
     dist.all_gather(all_k, ks, group=group)
     all_k = [int(t.item()) for t in all_k]
     kmax = max(all_k)
-    send = torch.zeros((nc, kmax), dtype=torch.float64, device=dev)
-    send[:, :k] = Rl
+    send = torch.zeros((nc, kmax), dtype=torch.float64, device=cdev)
+    send[:, :k] = Rl.to(cdev)
     gathered = [torch.empty_like(send) for _ in range(world)] if rank == root else None
     dist.gather(send, gathered, dst=root, group=group)
-    beta = torch.empty((F,), dtype=torch.float64, device=dev)
+    beta = torch.empty((F,), dtype=torch.float64, device=cdev)
     res = 0.0
     if rank == root:
-        b_root, res = _combine(ops, gathered, all_k, F, sqrt_mu, dev)
+        b_root, res = _combine(ops, [g.to(dev) for g in gathered], all_k, F, sqrt_mu, dev)
         beta.copy_(b_root)
     dist.broadcast(beta, src=root, group=group)
-    return beta, res
+    return beta.to(dev), res
