@@ -107,6 +107,29 @@ def test_row_major_and_shards_bit_identical(ctx):
     fls.fls_sync(ctx)
 
 
+def test_user_stream_and_timing_hook(ctx):
+    """a ctx on a user stream produces the same entries; the timing hook counts the assembly
+    launches (one per batch of blocks sharing a kernel variant) and resets on read"""
+    p = wl.make_problem("c4_heat2d", "mini")
+    _, _, Wd, bd = _parity_feats(p)
+    blocks = fls.BlockSet(dev_blocks(p), 3)
+    ref, lda = fls.fls_assemble(ctx, Wd, bd, blocks)
+    fls.fls_sync(ctx)
+    s = torch.cuda.Stream()
+    c2 = fls.Context(stream=s)
+    with torch.cuda.stream(s):
+        fls.fls_ctx_timing(c2, True)
+        got, _ = fls.fls_assemble(c2, Wd, bd, blocks)
+        fls.fls_assemble(c2, Wd, bd, blocks, A=got, lda=lda)
+        ms, n = fls.fls_ctx_timing_read(c2)
+        ms2, n2 = fls.fls_ctx_timing_read(c2)
+    fls.fls_sync(c2)
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+    assert n == 2 and ms > 0 and n2 == 0          # pde + bc + ic share one variant -> 1 launch/call
+    c2.close()
+
+
 def test_unaligned_lda_and_pointer_scalar_path(ctx):
     p = wl.make_problem("c2_poisson2d", "mini")
     _, _, Wd, bd = _parity_feats(p)
