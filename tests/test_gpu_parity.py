@@ -287,6 +287,10 @@ def test_random_operator_fuzz(ctx, seed):
     emax, _ = scaled_err(Ag, Ao, S)
     assert emax <= ENTRY_TOL, (emax, d, terms)
     assert np.array_equal(rg, ro)
+    # the row-major kernel holds bit-identical entries for every operator family
+    Arm, rrm = fls.fls_assemble(ctx, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(), [dv],
+                                normalize=normalize, layout=fls.FLS_ROW_MAJOR)
+    assert np.array_equal(Arm[:, :F].cpu().numpy(), Ag) and np.array_equal(rrm.cpu().numpy(), rg)
 
 
 @pytest.mark.parametrize("d", [1, 2, 4, 6, 8])
