@@ -323,6 +323,9 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=1024)
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
     ap.add_argument("--no-solve", action="store_true", help="skip the end-to-end solve leg")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the config's rows split over the ranks (BASELINE config 5's "
+                         "sweep, default); weak: every rank keeps the config's full row count")
     ap.add_argument("--layout", default="col", choices=["col", "row"],
                     help="A layout (col = what the QR consumes; row = features contiguous)")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -352,7 +355,12 @@ def main():
         else:
             dist.init_process_group(backend)
 
-    p = wl.make_problem(args.workload, "full", **({"n_int": args.rows} if args.rows else {}))
+    kw = {"n_int": args.rows} if args.rows else {}
+    if args.scaling == "weak":
+        # every rank keeps the config's full row count: the job is world x the config's rows
+        base_rows = args.rows or wl.FULL[args.workload]["n_int"]
+        kw["n_int"] = base_rows * world
+    p = wl.make_problem(args.workload, "full", **kw)
     F, R, d = p.n_features, p.n_rows, p.dim
     a, e = wl.shard_range(R, rank, world)
     n_local = e - a
@@ -435,7 +443,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": p.name, "rows": R, "features": F, "dim": d,
                    "operator": "biharmonic + 16(1+x1) u" if p.name == "c5_biharm3d" else p.name,
                    "A_bytes": 8 * R * (F + 1), "parallelism": f"rows{world}",
