@@ -26,6 +26,10 @@
  *                       then back substitution                     P:L124 ("via QR"), P:L156-160 (Tikhonov)
  *   orc_eval            u_N(x) = (1/sqrt N) sum_j beta_j sin(W_j.x+b_j)
  *                       (or L[u_N](x) through orc_assemble rows)   P:L77-82 (Eq.1), Alg.1 l.6
+ *   orc_features_blocks multi-block bandwidths
+ *   orc_sample_box/faces seeded collocation points                 Alg.1 l.2
+ *   orc_lstsq_mu        the Tikhonov solve with an absolute sqrt(mu) P:L158 (Newton step)
+ * Newton (oracle/newton.py) and learnable bandwidth (oracle/learnable.py) are Python on top.
  *
  * Parity pins for every function: tests/test_oracle_pins.py.
  */
