@@ -405,7 +405,11 @@ fls_status assemble_range(fls_ctx *ctx, const AsmPlan &ap, int32_t dim, int64_t 
                           const fls_block *blocks, const int64_t *pt_base, int64_t row_begin,
                           int64_t row_end, double *A, int64_t lda, int32_t layout, double *rhs,
                           cudaStream_t st) {
-  const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0);
+  // vector stores need every column segment aligned: 16 B (row pairs) or 32 B (kQuad rows);
+  // the row-major kernel always stores feature pairs (16 B)
+  const bool quad = kQuad && layout == FLS_COL_MAJOR;
+  const bool vec = quad ? ((reinterpret_cast<uintptr_t>(A) & 31) == 0) && (lda % 4 == 0)
+                        : ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0);
   AsmArgs batch[kMaxBatch];
   int nb = 0, bG = 0, bK = 0;
   auto flush = [&]() -> fls_status {

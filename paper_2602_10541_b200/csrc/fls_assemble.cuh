@@ -91,7 +91,7 @@ inline dim3 asm_grid(AsmArgs &a) {
       if (v >= 1 && v <= 64) waves = v;
     }
   }
-  const int64_t span = a.lr1 - (a.lr0 & ~int64_t(1));
+  const int64_t span = a.lr1 - (a.lr0 & ~int64_t(kRowAlign - 1));
   const int64_t rt = (span + kRowsCTA - 1) / kRowsCTA;
   const int64_t resident = (int64_t)sms * asm_min_blocks<D, G, KM>();
   const bool big_x = span * (D + G + 1) * 8 > ((int64_t)32 << 20);
@@ -115,6 +115,21 @@ inline dim3 asm_grid(AsmArgs &a) {
   return dim3((unsigned)rt, (unsigned)((a.F + a.fpc - 1) / a.fpc));
 }
 
+// full-tile store of one feature column's entries of this thread: two 16-byte streaming stores
+// (row pairs 2*kNT apart) or, with kQuad, one 32-byte store of 4 consecutive rows
+template <int NQ>
+__device__ __forceinline__ void store_full(double *colp, const double (&o)[NQ]) {
+  if constexpr (kQuad) {
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(colp), "d"(o[0]), "d"(o[1]),
+                 "d"(o[2]), "d"(o[3])
+                 : "memory");
+  } else {
+#pragma unroll
+    for (int pr = 0; pr < NQ / 2; ++pr)
+      __stcs(reinterpret_cast<double2 *>(colp + pr * (2 * kNT)), make_double2(o[2 * pr], o[2 * pr + 1]));
+  }
+}
+
 // One launch covers up to kMaxBatch row blocks that share the kernel variant (e.g. a PDE block
 // and its identity BC / IC blocks): the 1-D grid is the concatenation of each block's
 // (row tile, feature group) CTAs, row tile fastest.
@@ -135,7 +150,7 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
 
   // local rows (A-relative) of this thread: rbase + p*2*kNT + {0, 1}; rbase is even.
   // The block's points map to local rows [lr0, lr1): point i = pt0 + (r - lr0).
-  const int64_t rbase = (a.lr0 & ~int64_t(1)) + tile * kRowsCTA + 2 * threadIdx.x;
+  const int64_t rbase = (a.lr0 & ~int64_t(kRowAlign - 1)) + tile * kRowsCTA + kRowAlign * threadIdx.x;
   double x[NQ][D];
   double c[NQ][GG];
   bool in[NQ];
@@ -143,7 +158,7 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
   bool full = a.vec;
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
-    const int64_t r = rbase + (q >> 1) * (2 * kNT) + (q & 1);
+    const int64_t r = kQuad ? rbase + q : rbase + (q >> 1) * (2 * kNT) + (q & 1);
     in[q] = (r >= a.lr0) && (r < a.lr1);
     full = full && in[q];
     const int64_t i = a.pt0 + (r - a.lr0);
@@ -192,11 +207,7 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
           for (int q = 0; q < NQ; ++q) o[u][q] = M::entry(rec, x[q], c[q]);
         }
 #pragma unroll
-        for (int u = 0; u < kFUnroll; ++u)
-#pragma unroll
-          for (int pr = 0; pr < kPairs; ++pr)
-            __stcs(reinterpret_cast<double2 *>(colp + u * a.lda + pr * (2 * kNT)),
-                   make_double2(o[u][2 * pr], o[u][2 * pr + 1]));
+        for (int u = 0; u < kFUnroll; ++u) store_full(colp + u * a.lda, o[u]);
       }
       for (; jj < nfe; ++jj, colp += a.lda) {
         double rec[S];
@@ -204,9 +215,7 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
         double o[NQ];
 #pragma unroll
         for (int q = 0; q < NQ; ++q) o[q] = M::entry(rec, x[q], c[q]);
-#pragma unroll
-        for (int pr = 0; pr < kPairs; ++pr)
-          __stcs(reinterpret_cast<double2 *>(colp + pr * (2 * kNT)), make_double2(o[2 * pr], o[2 * pr + 1]));
+        store_full(colp, o);
       }
     } else {
       for (int jj = 0; jj < nfe; ++jj, colp += a.lda) {
@@ -215,14 +224,20 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
         double o[NQ];
 #pragma unroll
         for (int q = 0; q < NQ; ++q) o[q] = M::entry(rec, x[q], c[q]);
+        if (kQuad) {
 #pragma unroll
-        for (int pr = 0; pr < kPairs; ++pr) {
-          double *dst = colp + pr * (2 * kNT);
-          if (a.vec && in[2 * pr] && in[2 * pr + 1]) {
-            __stcs(reinterpret_cast<double2 *>(dst), make_double2(o[2 * pr], o[2 * pr + 1]));
-          } else {
-            if (in[2 * pr]) __stcs(dst, o[2 * pr]);
-            if (in[2 * pr + 1]) __stcs(dst + 1, o[2 * pr + 1]);
+          for (int q = 0; q < NQ; ++q)
+            if (in[q]) __stcs(colp + q, o[q]);
+        } else {
+#pragma unroll
+          for (int pr = 0; pr < kPairs; ++pr) {
+            double *dst = colp + pr * (2 * kNT);
+            if (a.vec && in[2 * pr] && in[2 * pr + 1]) {
+              __stcs(reinterpret_cast<double2 *>(dst), make_double2(o[2 * pr], o[2 * pr + 1]));
+            } else {
+              if (in[2 * pr]) __stcs(dst, o[2 * pr]);
+              if (in[2 * pr + 1]) __stcs(dst + 1, o[2 * pr + 1]);
+            }
           }
         }
       }

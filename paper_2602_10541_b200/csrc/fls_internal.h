@@ -28,6 +28,11 @@ enum KMode : int32_t { KM_SIN = 0, KM_SINCOS = 1 };
 #ifndef FLS_NT
 #define FLS_NT 256
 #endif
+#ifndef FLS_QUAD
+#define FLS_QUAD 0  // 1: 4 consecutive rows per thread, one 32-byte store per feature
+#endif
+constexpr bool kQuad = FLS_QUAD != 0 && FLS_PAIRS == 2;
+constexpr int kRowAlign = kQuad ? 4 : 2;    // rows per thread-contiguous store
 constexpr int kNT = FLS_NT;                 // threads per CTA
 constexpr int kPairs = FLS_PAIRS;           // 16-byte row pairs per thread
 constexpr int kFUnroll = FLS_FUNROLL;       // features per loop iteration
