@@ -234,10 +234,23 @@ def e2e_measure(args, p, ctx, W, b, a, e, world, local):
     s_step = float(t.item())
     h2d = in_bytes_points + n_calls * 8 * (F * d + F)
     d2h = 8 * n_local * (F + 1)
+    # the bound of this path: plain device -> pinned-host copy bandwidth of the same link
+    probe = torch.empty(min(A_h.numel(), 1 << 28), dtype=torch.float64, device="cuda")
+    host = A_h[: probe.numel()]
+    host.copy_(probe, non_blocking=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        host.copy_(probe, non_blocking=True)
+    torch.cuda.synchronize()
+    d2h_peak = 3 * 8 * probe.numel() / (time.perf_counter() - t0) / 1e9
+    del probe
     return {"value": p.n_rows * F / s_step, "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "s_per_step": s_step, "steps": args.e2e_steps,
             "api": "fls_assemble_host (C ABI, host buffers)",
             "d2h_gbs": d2h / s_step / 1e9,
+            "d2h_copy_peak_gbs": d2h_peak,
+            "frac_of_d2h_copy_peak": (d2h / s_step / 1e9) / d2h_peak,
             "note": f"pinned host ring of {ring} rows x {F + 1} columns, {n_calls} calls per step"}
 
 
