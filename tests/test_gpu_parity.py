@@ -62,7 +62,7 @@ def test_assemble_parity_mini(ctx, name):
     assert np.array_equal(rg, ro)
 
 
-@pytest.mark.parametrize("name", ["c3_poisson5d", "c4_heat2d", "c5_biharm3d"])
+@pytest.mark.parametrize("name", ["c2_poisson2d", "c3_poisson5d", "c4_heat2d", "c5_biharm3d"])
 def test_assemble_parity_full_size_sampled_rows(ctx, name):
     """BASELINE.json full sizes in the bench's launch configuration, oracle on sampled rows."""
     p = wl.make_problem(name, "full")
