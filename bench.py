@@ -3,7 +3,7 @@
 HBM GB/s, fp64).
 
 One STEP = one pass of the whole hot path of SURVEY §8(a) over the workload:
-  a1 fls_features (W, b from Philox on the device)  +  a2-a8 fls_assemble (prefactor fold,
+  a1 + a2-a8 fls_features_assemble (W, b from Philox on the device, prefactor fold,
   phase, trig, combine, weighted row blocks, rhs, streaming fp64 stores of [A | b]).
 Default workload = BASELINE.json config 5 (3D biharmonic + variable-coefficient Helmholtz,
 2,097,152 rows x 8,192 features = 1.718e10 entries, 137.4 GB of fp64), row-sharded over the
@@ -397,16 +397,17 @@ def main():
     rhs = torch.empty((n_local,), dtype=torch.float64, device="cuda") if row_major else None
     W = torch.empty((F, d), dtype=torch.float64, device="cuda")
     b = torch.empty((F,), dtype=torch.float64, device="cuda")
-    # per step: features + one prefactor launch per <= 4 blocks; assembly launches are counted
-    # by libfls's own timing events (one per batch of blocks sharing a kernel variant)
-    launches_per_step_fixed = 1 + (len(blocks) + 3) // 4
+    # per step: one fused features + prefactor launch (plus one prefactor launch per <= 4 blocks
+    # when more than 4 blocks); assembly launches are counted by libfls's own timing events
+    # (one per batch of blocks sharing a kernel variant)
+    launches_per_step_fixed = 1 if len(blocks) <= 4 else 1 + (len(blocks) + 3) // 4
 
     def step():
-        fls.fls_features(ctx, d, F, p.sigma, p.seed, W, b)
         if row_major:
-            fls.fls_assemble(ctx, W, b, bset, A=Ab, lda=lda, layout=fls.FLS_ROW_MAJOR, rhs=rhs)
+            fls.fls_features_assemble(ctx, d, F, p.sigma, p.seed, bset, W=W, b=b, A=Ab, lda=lda,
+                                      layout=fls.FLS_ROW_MAJOR, rhs=rhs)
         else:
-            fls.fls_assemble(ctx, W, b, bset, A=Ab, lda=lda)
+            fls.fls_features_assemble(ctx, d, F, p.sigma, p.seed, bset, W=W, b=b, A=Ab, lda=lda)
 
     for _ in range(args.warmup):
         step()

@@ -200,6 +200,17 @@ FLS_API fls_status fls_assemble(fls_ctx *ctx, const double *W, const double *b, 
                         int32_t n_blocks, int64_t row_begin, int64_t row_end, double *A,
                         int64_t lda, int32_t layout, double *rhs);
 
+/* Alg. 1 lines 1 + 3-5 in one call: fls_features(ctx, dim, n_features, sigma, seed, W, b)
+ * followed by fls_assemble(ctx, W, b, ...), with the feature draw and the per-block prefactor
+ * fold fused into one kernel (saves a launch on latency-bound problems).  W and b are written
+ * (bit-identical to fls_features) and must be device buffers of n_features x dim and
+ * n_features.  Other arguments, errors and asynchrony as fls_assemble. */
+FLS_API fls_status fls_features_assemble(fls_ctx *ctx, int32_t dim, int64_t n_features,
+                                         double sigma, uint64_t seed, double *W, double *b,
+                                         int32_t normalize, const fls_block *blocks,
+                                         int32_t n_blocks, int64_t row_begin, int64_t row_end,
+                                         double *A, int64_t lda, int32_t layout, double *rhs);
+
 /* ---------------------------------------------------------------------------------------- */
 /* fls_assemble with HOST buffers (the end-to-end path of a caller whose data lives in host  */
 /* memory).  Same arguments and semantics as fls_assemble with FLS_COL_MAJOR, except that    */

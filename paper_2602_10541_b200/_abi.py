@@ -70,6 +70,10 @@ _SIGS = {
     "fls_assemble": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int32,
                                C.POINTER(fls_block), C.c_int32, C.c_int64, C.c_int64, C.c_void_p,
                                C.c_int64, C.c_int32, C.c_void_p]),
+    "fls_features_assemble": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.c_uint64,
+                                        C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(fls_block),
+                                        C.c_int32, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
+                                        C.c_int32, C.c_void_p]),
     "fls_features_blocks": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                       C.c_uint64, C.c_void_p, C.c_void_p]),
     "fls_qr_factor": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_double,

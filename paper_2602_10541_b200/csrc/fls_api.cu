@@ -492,6 +492,69 @@ fls_status ensure_dev(double *&p, size_t &cap, size_t bytes, cudaStream_t st) {
 
 extern "C" {
 
+fls_status fls_features_assemble(fls_ctx *ctx, int32_t dim, int64_t n_features, double sigma,
+                                 uint64_t seed, double *W, double *b, int32_t normalize,
+                                 const fls_block *blocks, int32_t n_blocks, int64_t row_begin,
+                                 int64_t row_end, double *A, int64_t lda, int32_t layout,
+                                 double *rhs) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!(sigma > 0.0) || !std::isfinite(sigma)) return fail(FLS_EINVAL, "sigma must be > 0 and finite");
+  static thread_local AsmPlan ap;
+  if (fls_status s = validate_assemble(dim, n_features, W, b, blocks, n_blocks, row_begin, row_end,
+                                       A, lda, layout, ap))
+    return s;
+  const int64_t F = n_features;
+  DeviceGuard g(ctx->device);
+  if (fls_status s = ensure_ws(ctx, (size_t)ap.n_blocks * F * kSmax * sizeof(double))) return s;
+  FeatBlocks fb;
+  std::memset(&fb, 0, sizeof fb);
+  fb.n = 1;
+  fb.ends[0] = F;
+  fb.sigma[0] = sigma;
+  // records of the blocks that have rows in range (kMaxBatch fit in the fused launch)
+  static thread_local PrefBatch pb;
+  pb.n = 0;
+  const double s_norm = normalize ? 1.0 / std::sqrt((double)F) : 1.0;
+  int64_t g0 = 0;
+  bool overflow = false;
+  for (int q = 0; q < ap.n_blocks; ++q) {
+    const fls_block &B = blocks[q];
+    const int64_t lo = std::max(g0, row_begin), hi = std::min(g0 + B.n_points, row_end);
+    g0 += B.n_points;
+    if (hi <= lo) continue;
+    if (pb.n == kMaxBatch) {
+      overflow = true;
+      break;
+    }
+    const OpPlan &pl = ap.plans[q];
+    PrefArgs &pa = pb.blk[pb.n++];
+    std::memset(&pa, 0, sizeof pa);
+    pa.W = W;
+    pa.b = b;
+    pa.F = F;
+    pa.D = dim;
+    pa.n_terms = pl.n_terms;
+    pa.G = pl.G;
+    pa.pmode = pl.pmode;
+    pa.S = pf_stride(dim, pl.G, pl.kmode);
+    pa.scale = s_norm * B.weight;
+    pa.pf = ctx->ws + (size_t)q * F * kSmax;
+    pa.err = ctx->d_err;
+    std::memcpy(pa.terms, pl.terms, sizeof pl.terms);
+  }
+  if (overflow) pb.n = 0;  // many blocks: fused features only, prefactors in batches below
+  cudaError_t e = launch_features_prefactor(dim, F, fb, seed, W, b, pb, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "features_prefactor_kernel");
+  if (overflow) {
+    if (fls_status s = launch_prefactors(ctx, ap, W, b, dim, F, normalize, blocks, row_begin,
+                                         row_end, ctx->stream))
+      return s;
+  }
+  if (row_end == row_begin) return FLS_OK;
+  return assemble_range(ctx, ap, dim, F, blocks, nullptr, row_begin, row_end, A, lda, layout, rhs,
+                        ctx->stream);
+}
+
 fls_status fls_assemble(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
                         int64_t n_features, int32_t normalize, const fls_block *blocks,
                         int32_t n_blocks, int64_t row_begin, int64_t row_end, double *A,

@@ -129,6 +129,8 @@ struct PrefBatch {
 
 cudaError_t launch_prefactor(const PrefArgs &a, cudaStream_t st);
 cudaError_t launch_prefactor_batch(const PrefBatch &b, int64_t F, cudaStream_t st);
+cudaError_t launch_features_prefactor(int32_t dim, int64_t F, const FeatBlocks &fb, uint64_t seed,
+                                      double *W, double *b, const PrefBatch &pb, cudaStream_t st);
 // blks: n (<= kMaxBatch) blocks of one variant; fpc is set per block by the launcher
 cudaError_t launch_assemble_cm(int D, int G, int kmode, AsmArgs *blks, int n, cudaStream_t st);
 cudaError_t launch_assemble_rm(int D, int G, int kmode, const AsmArgs &a, cudaStream_t st);

@@ -134,6 +134,8 @@ __global__ void prefactor_batch_kernel(const PrefBatch b) {
   if (j < a.F) prefactor_one(a, j);
 }
 
+__device__ void prefactor_core(const PrefArgs &a, int64_t j, const double *w, double bj);
+
 __device__ void prefactor_one(const PrefArgs &a, int64_t j) {
   double w[FLS_MAX_DIM];
   bool ok = true;
@@ -144,6 +146,49 @@ __device__ void prefactor_one(const PrefArgs &a, int64_t j) {
   double bj = a.b[j];
   ok &= finite(bj);
   if (!ok) atomicOr(a.err, 1u);
+  prefactor_core(a, j, w, bj);
+}
+
+// a1 + a2 fused (fls_features_assemble): one thread per feature draws W_j, b_j exactly as
+// features_kernel does (same Philox words, same Box-Muller arithmetic -> bit-identical), writes
+// them, and folds every block's prefactor record from the registers.
+__global__ void features_prefactor_kernel(int32_t D, int64_t F, const FeatBlocks fb,
+                                          uint64_t seed, double *W, double *b, const PrefBatch pb) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= F) return;
+  const double two_pi = 6.283185307179586476925286766559;
+  const double sig = block_sigma(fb, j);
+  double w[FLS_MAX_DIM];
+  for (int k = 0; k < D; ++k) {
+    const int64_t m = j * D + k;          // normal index; pair m/2 uses raw words m&~1, m|1
+    const int64_t word0 = m & ~int64_t(1);
+    uint64_t c[4] = {(uint64_t)(word0 / 4) + 1, 0, 0, 0};
+    philox4x64(c, seed, 1);
+    const int o = (int)(word0 % 4);
+    const double u1 = u01(c[o]), u2 = u01(c[o + 1]);
+    const double rad = sqrt(-2.0 * log(1.0 - u1));
+    const double th = two_pi * u2;
+    double sn, cs;
+    sincos(th, &sn, &cs);
+    w[k] = sig * (rad * ((m & 1) ? sn : cs));
+    W[m] = w[k];
+  }
+  uint64_t c[4] = {(uint64_t)(j / 4) + 1, 0, 0, 0};
+  philox4x64(c, seed, 2);
+  const double bj = two_pi * u01(c[j % 4]);
+  b[j] = bj;
+  for (int q = 0; q < pb.n; ++q) prefactor_core(pb.blk[q], j, w, bj);
+}
+
+cudaError_t launch_features_prefactor(int32_t dim, int64_t F, const FeatBlocks &fb, uint64_t seed,
+                                      double *W, double *b, const PrefBatch &pb, cudaStream_t st) {
+  features_prefactor_kernel<<<(unsigned)((F + 127) / 128), 128, 0, st>>>(dim, F, fb, seed, W, b, pb);
+  return cudaGetLastError();
+}
+
+// explicit _rn arithmetic: no FMA contraction, so every call site (prefactor_one,
+// features_prefactor_kernel) rounds identically whatever the inliner does around it
+__device__ void prefactor_core(const PrefArgs &a, int64_t j, const double *w, double bj) {
   double Ps[FLS_MAX_FIELDS + 1], Pc[FLS_MAX_FIELDS + 1];
   for (int g = 0; g <= FLS_MAX_FIELDS; ++g) Ps[g] = Pc[g] = 0.0;
   for (int t = 0; t < a.n_terms; ++t) {
@@ -152,35 +197,35 @@ __device__ void prefactor_one(const PrefArgs &a, int64_t j) {
     int order = 0;
     for (int k = 0; k < a.D; ++k)
       for (int e = 0; e < T.alpha[k]; ++e) {
-        m *= w[k];
+        m = __dmul_rn(m, w[k]);
         ++order;
       }
     const int p = order & 3;  // Phi_{|alpha| mod 4}: sin, cos, -sin, -cos
     if (p & 2) m = -m;
     if (p & 1)
-      Pc[T.group] += m;
+      Pc[T.group] = __dadd_rn(Pc[T.group], m);
     else
-      Ps[T.group] += m;
+      Ps[T.group] = __dadd_rn(Ps[T.group], m);
   }
   double *out = a.pf + j * a.S;
-  for (int k = 0; k < a.D; ++k) out[k] = w[k] * kInvPi;
+  for (int k = 0; k < a.D; ++k) out[k] = __dmul_rn(w[k], kInvPi);
   double bp = bj;
   int o = a.D + 1;
   switch (a.pmode) {
     case PM_SIN:
       for (int g = 0; g <= a.G; ++g) out[o++] = a.scale * Ps[g];
-      out[a.D] = bp * kInvPi;
+      out[a.D] = __dmul_rn(bp, kInvPi);
       break;
     case PM_COSSHIFT:  // cos z = sin(z + pi/2)  (App. F quarter-wave shift)
       for (int g = 0; g <= a.G; ++g) out[o++] = a.scale * Pc[g];
-      out[a.D] = bp * kInvPi + 0.5;
+      out[a.D] = __dadd_rn(__dmul_rn(bp, kInvPi), 0.5);
       break;
     case PM_FOLD: {    // Ps sin z + Pc cos z = rho sin(z + psi)
       const double ps = a.scale * Ps[0], pc = a.scale * Pc[0];
       const double rho = hypot(ps, pc);
       const double psi = atan2(pc, ps);
       out[o++] = rho;
-      out[a.D] = (bp + psi) * kInvPi;
+      out[a.D] = __dmul_rn(__dadd_rn(bp, psi), kInvPi);
       break;
     }
     default:           // PM_SINCOS
@@ -188,7 +233,7 @@ __device__ void prefactor_one(const PrefArgs &a, int64_t j) {
         out[o++] = a.scale * Ps[g];
         out[o++] = a.scale * Pc[g];
       }
-      out[a.D] = bp * kInvPi;
+      out[a.D] = __dmul_rn(bp, kInvPi);
       break;
   }
   for (; o < a.S; ++o) out[o] = 0.0;

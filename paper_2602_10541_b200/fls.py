@@ -24,7 +24,7 @@ from ._abi import FLS_COL_MAJOR, FLS_ROW_MAJOR, FlsError, check
 
 Term = Tuple[Sequence[int], float, int]   # (alpha, coef, field)
 
-__all__ = ["Context", "Block", "fls_features", "fls_assemble", "fls_solve", "fls_qr_r",
+__all__ = ["Context", "Block", "fls_features", "fls_assemble", "fls_features_assemble", "fls_solve", "fls_qr_r",
            "fls_frob2", "fls_eval", "fls_sync", "fls_ctx_timing", "fls_ctx_timing_read",
            "fls_assemble_host", "HostBlockSet", "BlockSet", "fls_features_blocks", "QRFactor",
            "make_nonlinearity", "fls_nl_residual", "fls_axpy", "fls_features_transform",
@@ -354,6 +354,50 @@ def fls_assemble(ctx: Context, W: torch.Tensor, b: torch.Tensor, blocks, *,
     if layout == FLS_COL_MAJOR:
         return A, lda
     return A, rhs
+
+
+def fls_features_assemble(ctx: Context, dim: int, n_features: int, sigma: float, seed: int,
+                          blocks, *, W: Optional[torch.Tensor] = None,
+                          b: Optional[torch.Tensor] = None, normalize: bool = True,
+                          row_begin: int = 0, row_end: Optional[int] = None,
+                          A: Optional[torch.Tensor] = None, lda: Optional[int] = None,
+                          layout: int = FLS_COL_MAJOR, rhs: Optional[torch.Tensor] = None,
+                          extra_rows: int = 0):
+    """fls_features + fls_assemble in one call (fused feature draw + prefactor launch).
+
+    Returns (W, b, Ab, lda) column-major or (W, b, A, rhs) row-major."""
+    dev = torch.device("cuda", ctx.device)
+    F = int(n_features)
+    if W is None:
+        W = torch.empty((F, dim), dtype=torch.float64, device=dev)
+    if b is None:
+        b = torch.empty((F,), dtype=torch.float64, device=dev)
+    _dev_f64(W, "W")
+    _dev_f64(b, "b")
+    bs = blocks if isinstance(blocks, BlockSet) else BlockSet(blocks, dim)
+    row_end = bs.total if row_end is None else int(row_end)
+    n_local = row_end - int(row_begin)
+    if layout == FLS_COL_MAJOR:
+        if lda is None:
+            lda = round_up(max(n_local + extra_rows, 1), 4)
+        if A is None:
+            A = torch.empty(((F + 1) * lda,), dtype=torch.float64, device=dev)
+        if rhs is None:
+            rhs = A[F * lda:]
+    else:
+        if lda is None:
+            lda = round_up(F, 2)
+        if A is None:
+            A = torch.empty((max(n_local, 0), lda), dtype=torch.float64, device=dev)
+        if rhs is None:
+            rhs = torch.empty((max(n_local, 0),), dtype=torch.float64, device=dev)
+    check(_abi.load().fls_features_assemble(
+        ctx.handle, int(dim), F, float(sigma), int(seed) & (2**64 - 1), _ptr(W), _ptr(b),
+        int(bool(normalize)), bs.arr, len(bs.blocks), int(row_begin), row_end, _ptr(A), int(lda),
+        int(layout), _ptr(rhs)))
+    if layout == FLS_COL_MAJOR:
+        return W, b, A, lda
+    return W, b, A, rhs
 
 
 def _host_ptr(a):

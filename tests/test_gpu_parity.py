@@ -599,3 +599,40 @@ def test_cached_qr_many_rhs(ctx, name, size):
         rel = np.linalg.norm(u_gpu - u_orc) / np.linalg.norm(u_orc)
         assert rel <= U_TOL, (k, rel)
     qr.close()
+
+
+# ------------------------------------------------------------------------------------- fused a1+a2
+@pytest.mark.parametrize("name", ["c1_poisson1d", "c4_heat2d", "c5_biharm3d"])
+def test_features_assemble_fused_bit_identical(ctx, name):
+    """fls_features_assemble == fls_features then fls_assemble, bit for bit: one block batch
+    (fused prefactors), more blocks than one prefactor batch holds, shards and row-major"""
+    p = wl.make_problem(name, "mini")
+    F, d = p.n_features, p.dim
+    sigma, seed = float(p.sigma), int(p.seed)
+    Wd, bd = fls.fls_features(ctx, d, F, sigma, seed)
+    base = dev_blocks(p)
+    for blks in (base, base + base):
+        bs = fls.BlockSet(blks, d)
+        ref, lda = fls.fls_assemble(ctx, Wd, bd, bs)
+        W2, b2, got, lda2 = fls.fls_features_assemble(ctx, d, F, sigma, seed, bs)
+        fls.fls_sync(ctx)
+        assert lda2 == lda
+        assert torch.equal(W2, Wd) and torch.equal(b2, bd)
+        R = bs.total
+
+        def cols(Ab, ld, n):   # (F + 1, n) valid part of a flat column-major [A | b]
+            return Ab[: (F + 1) * ld].view(F + 1, ld)[:, :n]
+        nbad = int((cols(got, lda, R) != cols(ref, lda, R)).sum())
+        assert nbad == 0, (len(blks), nbad)
+        a, e = wl.shard_range(R, 1, 3)
+        ref_s, ls = fls.fls_assemble(ctx, Wd, bd, bs, row_begin=a, row_end=e)
+        _, _, got_s, _ = fls.fls_features_assemble(ctx, d, F, sigma, seed, bs, row_begin=a,
+                                                   row_end=e)
+        Arm, rrm = fls.fls_assemble(ctx, Wd, bd, bs, layout=fls.FLS_ROW_MAJOR)
+        _, _, Arm2, rrm2 = fls.fls_features_assemble(ctx, d, F, sigma, seed, bs,
+                                                     layout=fls.FLS_ROW_MAJOR)
+        fls.fls_sync(ctx)
+        assert torch.equal(cols(got_s, ls, e - a), cols(ref_s, ls, e - a))
+        assert torch.equal(Arm2[:, :F], Arm[:, :F]) and torch.equal(rrm2, rrm)
+    with pytest.raises(fls.FlsError):
+        fls.fls_features_assemble(ctx, d, F, -1.0, seed, base)

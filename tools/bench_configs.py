@@ -33,7 +33,7 @@ def dev_blocks(p):
             for blk in p.blocks]
 
 
-def assembly_rate(p, reps):
+def assembly_rate(p, reps, fused=True):
     F, R, d = p.n_features, p.n_rows, p.dim
     ctx = fls.Context()
     bset = fls.BlockSet(dev_blocks(p), d)
@@ -45,8 +45,11 @@ def assembly_rate(p, reps):
     ctx.set_stream(s)
 
     def step():
-        fls.fls_features(ctx, d, F, p.sigma, p.seed, W, b)
-        fls.fls_assemble(ctx, W, b, bset, A=Ab, lda=lda)
+        if fused:   # one launch for features + prefactors (fls_features_assemble)
+            fls.fls_features_assemble(ctx, d, F, p.sigma, p.seed, bset, W=W, b=b, A=Ab, lda=lda)
+        else:
+            fls.fls_features(ctx, d, F, p.sigma, p.seed, W, b)
+            fls.fls_assemble(ctx, W, b, bset, A=Ab, lda=lda)
 
     with torch.cuda.stream(s):
         for _ in range(3):
@@ -96,11 +99,13 @@ def main(names):
         F, R = p.n_features, p.n_rows
         reps = max(5, min(2000, int(2e10 / (R * F))))
         ms, single_ms, clocks = assembly_rate(p, reps)
+        ms_sep, single_sep, _ = assembly_rate(p, reps, fused=False)
         rec = {"config": name, "rows": R, "features": F, "entries": R * F,
                "graph_ms_per_step": ms, "entries_per_s": R * F / (ms / 1e3),
                "hbm_write_gbs": 8.0 * R * (F + 1) / (ms / 1e3) / 1e9,
                "frac_of_copy_peak": 8.0 * R * F / (ms / 1e3) / 1e9 / hbm_peak,
-               "single_shot_ms": single_ms, "reps": reps, "clocks": clocks}
+               "single_shot_ms": single_ms, "reps": reps, "clocks": clocks,
+               "unfused": {"graph_ms_per_step": ms_sep, "single_shot_ms": single_sep}}
         # end-to-end solve (C5: 262,144-row subset) and fitted-u parity
         import bench
 
