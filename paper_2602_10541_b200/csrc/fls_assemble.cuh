@@ -67,11 +67,15 @@ struct EntryMath {
   }
 };
 
-// resident CTAs per SM the register budget is sized for: the small sin-only kernels (all
-// BASELINE configs) fit 64 registers (4 CTAs); wide ones (many dims / fields, sin+cos) get 128
+// resident CTAs per SM the register budget is sized for (checked against ptxas -v spills):
+// sin-only with G <= 1, D + G <= 4 fits 64 registers (4 CTAs: C1, C2, C4, C5), D + G <= 5
+// fits 80 (3 CTAs: C3); wider ones get 128 (2 CTAs) or 255 (1 CTA)
 template <int D, int G, int KM>
 constexpr int asm_min_blocks() {
-  return (KM == KM_SIN && D + G <= 5) ? FLS_MINB : 2;
+  if (KM != KM_SIN) return D + G >= 9 ? 1 : 2;
+  if (G <= 1 && D + G <= 4) return FLS_MINB;
+  if (D + G <= 5) return 3;
+  return D + G >= 10 ? 1 : 2;
 }
 
 // Launch shape: grid = (row tiles, feature groups), a.fpc features per CTA.  Picks the fewest
