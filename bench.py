@@ -46,6 +46,21 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def fp64_ops_per_entry(p):
+    """FP64-pipe instructions per entry of the sin-family assembly kernel (SASS-
+    checked for C5): d phase DFMA + 3 DADD rounding + f^2 + 6 DFMA polynomial + 1 DMUL (·f) +
+    1 DMUL (·P) + 1 DFMA per coefficient-field group.  Row-weighted over the blocks; None when
+    a block needs the sin+cos variant (mixed parity with coefficient fields)."""
+    tot = 0.0
+    for blk in p.blocks:
+        groups = {int(f) for _, _, f in blk.terms if int(f) >= 0}
+        parities = {sum(a) % 2 for a, _, _ in blk.terms}
+        if groups and len(parities) > 1:
+            return None
+        tot += blk.n * (p.dim + 12 + len(groups))
+    return tot / max(p.n_rows, 1)
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region"""
 
@@ -454,6 +469,19 @@ def main():
             traffic = json.load(open(tf)).get(args.workload, {}).get("traffic_bytes_per_launch")
         except Exception:
             traffic = None
+    # the FP64 co-bound (north_star: "the slower of HBM bandwidth and fp64 issue rate"): FP64-pipe
+    # lane-ops per second vs 148 SMs x 64 FP64 lanes/clk at the max and the median loaded clock
+    ops = fp64_ops_per_entry(p)
+    fp64 = None
+    if ops is not None:
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        ach = ops * n_local * F / (k_ms_step / 1e3) / 1e12
+        fp64 = {"ops_per_entry": ops, "achieved_tops": ach}
+        for tag, mhz in (("max_clock", clocks.get("sm_max_mhz")), ("median_clock", clocks.get("sm_mhz"))):
+            if mhz:
+                pk = sms * 64 * mhz * 1e6 / 1e12
+                fp64[f"peak_tops_{tag}"] = pk
+                fp64[f"frac_{tag}"] = ach / pk
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -468,7 +496,7 @@ def main():
                      "frac": achieved / hbm_peak, "traffic": traffic,
                      "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
                      "kernel": "assemble_rm_kernel" if row_major else "assemble_cm_kernel",
-                     "kernel_ms_avg": k_avg_ms,
+                     "kernel_ms_avg": k_avg_ms, "fp64_pipe": fp64,
                      "scope": "rank 0's GPU (per-GPU kernel roofline)"},
         "gpu_launches": launches_per_step_fixed * args.steps + k_launches,
         "clocks": clocks,
