@@ -25,6 +25,9 @@
 #ifndef FLS_MINB
 #define FLS_MINB 4   // 4 CTAs x 256 threads per SM -> <= 64 registers
 #endif
+#ifndef FLS_MINB5
+#define FLS_MINB5 3  // d + G = 5 (C3): 3 CTAs -> <= 80 registers
+#endif
 
 namespace fls {
 
@@ -74,17 +77,17 @@ template <int D, int G, int KM>
 constexpr int asm_min_blocks() {
   if (KM != KM_SIN) return D + G >= 9 ? 1 : 2;
   if (G <= 1 && D + G <= 4) return FLS_MINB;
-  if (D + G <= 5) return 3;
+  if (D + G <= 5) return FLS_MINB5;
   return D + G >= 10 ? 1 : 2;
 }
 
 // Launch shape: grid = (row tiles, feature groups), a.fpc features per CTA.  Picks the fewest
-// feature groups that give >= 4 waves of resident CTAs (148 SMs x asm_min_blocks), then the
+// feature groups that give >= 2 waves of resident CTAs (148 SMs x asm_min_blocks), then the
 // group count in [g, 2g] whose last wave is fullest.  Each CTA keeps >= 16 features (>= kFC
 // when the block's point data exceed 32 MB and would not stay in L2 between groups).
 template <int D, int G, int KM>
 inline dim3 asm_grid(AsmArgs &a) {
-  static int sms = 0, waves = 4;  // tools/waves_sweep.sh: 2-4 waves best for C3, flat for C4/C5
+  static int sms = 0, waves = 2;  // tools/waves_sweep.sh, variant_sweep_c3.sh: 2 best for C3, flat for C2/C4/C5
   if (!sms) {
     int dev = 0;
     cudaGetDevice(&dev);
