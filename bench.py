@@ -20,6 +20,7 @@ around each assembly launch (fls_ctx_timing).  Rank 0 prints ONE JSON line.
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -64,7 +65,7 @@ def fp64_ops_per_entry(p):
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region"""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -72,6 +73,13 @@ class ClockSampler:
         self.idx = gpu_index
         self.rows = []
         self.proc = None
+        self.t0 = self.t1 = None
+
+    def mark_begin(self):   # host wall-clock bracket of the timed region (samples outside are
+        self.t0 = datetime.datetime.now()   # idle or warm-up and are dropped when possible)
+
+    def mark_end(self):
+        self.t1 = datetime.datetime.now()
 
     def start(self):
         try:
@@ -86,8 +94,12 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 9:
-                self.rows.append(parts)
+            if len(parts) >= 10:
+                try:
+                    ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f")
+                except ValueError:
+                    ts = None
+                self.rows.append((ts, parts[1:]))
 
     def stop(self):
         if self.proc:
@@ -98,7 +110,13 @@ class ClockSampler:
                 self.proc.kill()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         sm, mx, reasons, pw = [], 0.0, set(), []
-        for r in self.rows:
+        rows = [r for ts, r in self.rows]
+        window = "sampler lifetime"
+        if self.t0 and self.t1:
+            inside = [r for ts, r in self.rows if ts is not None and self.t0 <= ts <= self.t1]
+            if inside:
+                rows, window = inside, "timed region"
+        for r in rows:
             try:
                 sm.append(float(r[1]))
                 mx = max(mx, float(r[2]))
@@ -111,7 +129,7 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
                 "sm_min_mhz": min(sm) if sm else None, "power_w_max": max(pw) if pw else None,
                 "power_w_median": statistics.median(pw) if pw else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "window": window}
 
 
 def cpu_baseline(problem, rows_budget_s: float = 12.0):
@@ -428,19 +446,21 @@ def main():
         step()
     fls.fls_sync(ctx)
     clk = ClockSampler(local)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     clk.start()
-    time.sleep(0.3)
+    time.sleep(0.3)                      # let nvidia-smi start sampling
     fls.fls_ctx_timing(ctx, True)
     st = ctx.stream
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk.mark_begin()
     e0.record(st)
     for _ in range(args.steps):
         step()
     e1.record(st)
     torch.cuda.synchronize()
+    clk.mark_end()
     if world > 1:
         dist.barrier()
     clocks = clk.stop()

@@ -44,3 +44,25 @@ def test_reference_arm_two_ranks_prints_once():
     assert r.returncode == 0, r.stderr[-2000:]
     lines = _json_lines(r.stdout)
     assert len(lines) == 1 and lines[0]["n_gpus"] == 2
+
+
+def test_clock_sampler_keeps_timed_window_and_flags_reasons():
+    import datetime
+    sys.path.insert(0, ROOT)
+    import bench
+    c = bench.ClockSampler(0)
+    t = datetime.datetime(2026, 1, 1, 12, 0, 0)
+
+    def row(sec, mhz, power_cap="Not Active", thermal="Not Active"):
+        return (t + datetime.timedelta(seconds=sec),
+                ["0", str(mhz), "1965", "500.0", "0x0", "Not Active", "Not Active", thermal, power_cap])
+    c.rows = [row(0.0, 1965), row(1.0, 1500, "Active"), row(1.1, 1600, "Active"), row(3.0, 1965)]
+    c.t0, c.t1 = t + datetime.timedelta(seconds=0.5), t + datetime.timedelta(seconds=2)
+    out = c.stop()
+    assert out["window"] == "timed region" and out["samples"] == 2
+    assert out["sm_mhz"] == 1550 and out["sm_max_mhz"] == 1965 and out["reasons"] == ["sw_power_cap"]
+    c.t0, c.t1 = t + datetime.timedelta(seconds=5), t + datetime.timedelta(seconds=6)
+    c.rows.append(row(3.5, 1200, thermal="Active"))
+    out = c.stop()                       # nothing inside the window: every sample counts
+    assert out["window"] == "sampler lifetime" and out["samples"] == 5
+    assert out["reasons"] == ["sw_power_cap", "sw_thermal_slowdown"]

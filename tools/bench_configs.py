@@ -68,12 +68,16 @@ def assembly_rate(p, reps, fused=True):
             g.replay()
         clk = ClockSampler(0)
         clk.start()
+        time.sleep(0.3)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        clk.mark_begin()
         e0.record(s)
         for _ in range(reps):
             g.replay()
         e1.record(s)
         torch.cuda.synchronize()
+        clk.mark_end()
         clocks = clk.stop()
     fls.fls_sync(ctx)
     ms = e0.elapsed_time(e1) / reps
