@@ -308,7 +308,7 @@ FLS_API fls_status fls_axpy(fls_ctx *ctx, int64_t n, double alpha, const double 
 /* every new right-hand side costs a cached apply; inverse problems P:L395-397).             */
 /* fls_qr_factor copies the column-major A (n_rows x n_features, lda) into ctx-independent   */
 /* device storage owned by the returned handle, appends [sqrt_mu I] rows when sqrt_mu > 0,   */
-/* and runs Householder QR (geqrf).  fls_qr_solve then computes, for each of nrhs columns of  */
+/* and runs Householder QR (fls_geqrf).  fls_qr_solve then computes, for each of nrhs columns of  */
 /* B (n_rows x nrhs, ldb; the ridge rows' rhs are 0), beta = R^-1 (Q^T [b; 0])[0:n_features] */
 /* (ormqr + trsm) into Beta (n_features x nrhs, ldbeta).  All device pointers; blocking.      */
 /* The handle is immutable after factoring and may be used from any ctx on the same device.  */
@@ -327,6 +327,19 @@ FLS_API fls_status fls_qr_destroy(fls_qr *qr);
  * the diagonal) into R (device, column-major, ldr >= min(n_rows, n_cols)).  Blocking. */
 FLS_API fls_status fls_qr_r(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda, int64_t n_cols,
                     double *R, int64_t ldr);
+
+/* Householder QR of the column-major block M (n_rows x n_cols, lda) in place, in LAPACK /
+ * cuSOLVER geqrf format: R in the upper trapezoid, the Householder vectors v_j (v_jj = 1
+ * implicit) below the diagonal, tau (device, min(n_rows, n_cols) doubles), H_j = I - tau_j
+ * v_j v_j^T, Q = H_1 ... H_k.  This is the factorisation fls_solve / fls_qr_factor / fls_qr_r
+ * run (Alg. 1 line 5): libfls's blocked QR (nb-column compact-WY panels factored
+ * recursively on cuBLAS DGEMM, <= 32-column leaves in one cooperative kernel per leaf) for
+ * n_cols >= 1024, a single cusolverDnDgeqrf call for narrower blocks; the environment
+ * variable FLS_QR=blocked / FLS_QR=cusolver forces one of the two (read at every call).
+ *   Errors: FLS_EINVAL (sizes, NULL), FLS_EUNSUPPORTED (a dimension > INT32_MAX), FLS_ENOMEM,
+ *   FLS_ECUSOLVER (cuBLAS failure).  Blocking. */
+FLS_API fls_status fls_geqrf(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda, int64_t n_cols,
+                             double *tau);
 
 /* sum of squares of the n_rows x n_cols column-major block (for ||A||_F^2).  out: host.
  * Blocking. */

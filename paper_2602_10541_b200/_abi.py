@@ -102,6 +102,7 @@ _SIGS = {
                                     C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]),
     "fls_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_double,
                             C.c_void_p, C.POINTER(C.c_double)]),
+    "fls_geqrf": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p]),
     "fls_qr_r": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
                            C.c_int64]),
     "fls_frob2": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,

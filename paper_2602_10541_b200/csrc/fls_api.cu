@@ -688,24 +688,59 @@ static fls_status ensure_handles(fls_ctx *ctx) {
   return FLS_OK;
 }
 
-// Householder QR of an m x n column-major block in place (R in the upper trapezoid)
-static fls_status geqrf_inplace(fls_ctx *ctx, double *M, int64_t m, int64_t lda, int64_t n) {
+// Householder QR of an m x n column-major block in place (R in the upper trapezoid, reflectors
+// below, geqrf format).  Default: libfls's blocked QR (fls_qr.cu) for n >= 1024 columns, one
+// cusolverDnDgeqrf call below that.  tau_out (k = min(m, n) doubles) may be NULL.
+constexpr int64_t kQrBlockedMinCols = 1024;
+
+// FLS_QR: "cusolver" / "blocked" force a method (A/B timing, tests); unset = by size.  Read
+// per call so a test can switch it.
+static int qr_method() {
+  const char *s = getenv("FLS_QR");
+  if (s && std::strcmp(s, "cusolver") == 0) return 1;
+  if (s && std::strcmp(s, "blocked") == 0) return 2;
+  return 0;
+}
+
+static fls_status geqrf_inplace(fls_ctx *ctx, double *M, int64_t m, int64_t lda, int64_t n,
+                                double *tau_out = nullptr) {
   if (m > INT32_MAX || n > INT32_MAX || lda > INT32_MAX)
     return fail(FLS_EUNSUPPORTED, "geqrf: dimensions exceed int32 (m=%lld n=%lld lda=%lld)",
                 (long long)m, (long long)n, (long long)lda);
+  const int64_t k = m < n ? m : n;
+  // small problems (C1: 1,002 x 501) are launch-latency bound: one cuSOLVER call is faster
+  const int method = qr_method();
+  if (method != 1 && m <= qr_blocked_max_rows() && (method == 2 || n >= kQrBlockedMinCols)) {
+    double *tau = tau_out;
+    if (!tau && cudaMallocAsync((void **)&tau, (size_t)(k > 0 ? k : 1) * sizeof(double), ctx->stream) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(FLS_ENOMEM, "qr tau");
+    }
+    cudaError_t ce;
+    cublasStatus_t be;
+    const char *msg = qr_blocked(ctx->blas, ctx->stream, M, m, n, lda, tau, &ce, &be);
+    if (!tau_out) cudaFreeAsync(tau, ctx->stream);
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (msg) {
+      if (ce == cudaErrorMemoryAllocation) return fail(FLS_ENOMEM, "blocked QR: %s", msg);
+      if (ce != cudaSuccess) return cuda_fail(ce, msg);
+      return fail(FLS_ECUSOLVER, "blocked QR: %s (cublas status %d)", msg, (int)be);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "blocked QR");
+    return FLS_OK;
+  }
   int lwork = 0;
   if (cusolverDnDgeqrf_bufferSize(ctx->solver, (int)m, (int)n, M, (int)lda, &lwork) !=
       CUSOLVER_STATUS_SUCCESS)
     return fail(FLS_ECUSOLVER, "cusolverDnDgeqrf_bufferSize failed");
-  const int64_t k = m < n ? m : n;
   double *work = nullptr;
   size_t bytes = ((size_t)lwork + (size_t)k + 2) * sizeof(double);
   if (cudaMallocAsync((void **)&work, bytes, ctx->stream) != cudaSuccess) {
     cudaGetLastError();
     return fail(FLS_ENOMEM, "geqrf workspace of %zu bytes", bytes);
   }
-  double *tau = work + lwork;
-  int *info = reinterpret_cast<int *>(tau + k);
+  double *tau = tau_out ? tau_out : work + lwork;
+  int *info = reinterpret_cast<int *>(work + lwork + k);
   cusolverStatus_t st = cusolverDnDgeqrf(ctx->solver, (int)m, (int)n, M, (int)lda, tau, work,
                                          lwork, info);
   int h_info = 0;
@@ -806,36 +841,17 @@ fls_status fls_qr_factor(fls_ctx *ctx, const double *A, int64_t n_rows, int64_t 
     fls_qr_destroy(q);
     return cuda_fail(e, "fls_qr_factor copy");
   }
-  // geqrf keeping tau: reuse geqrf_inplace's path but we need tau -> do it here
-  int lwork = 0;
-  if (cusolverDnDgeqrf_bufferSize(ctx->solver, (int)m, (int)n_features, q->M, (int)q->ld, &lwork) !=
-      CUSOLVER_STATUS_SUCCESS) {
+  if (fls_status s = geqrf_inplace(ctx, q->M, m, q->ld, n_features, q->tau)) {
     fls_qr_destroy(q);
-    return fail(FLS_ECUSOLVER, "geqrf_bufferSize");
+    return s;
   }
-  double *work = nullptr;
-  if (cudaMallocAsync((void **)&work, sizeof(double) * (lwork + 2), ctx->stream) != cudaSuccess) {
-    cudaGetLastError();
-    fls_qr_destroy(q);
-    return fail(FLS_ENOMEM, "geqrf workspace");
-  }
-  int *info = reinterpret_cast<int *>(work + lwork);
-  cusolverStatus_t st = cusolverDnDgeqrf(ctx->solver, (int)m, (int)n_features, q->M, (int)q->ld,
-                                         q->tau, work, lwork, info);
-  int h_info = 0;
   double dmin = 0.0;
-  cudaMemcpyAsync(&h_info, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
   launch_min_abs_diag(q->M, q->ld, n_features, ctx->d_scratch, ctx->stream);
   cudaMemcpyAsync(&dmin, ctx->d_scratch, sizeof dmin, cudaMemcpyDeviceToHost, ctx->stream);
-  cudaFreeAsync(work, ctx->stream);
   e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) {
     fls_qr_destroy(q);
     return cuda_fail(e, "fls_qr_factor");
-  }
-  if (st != CUSOLVER_STATUS_SUCCESS || h_info != 0) {
-    fls_qr_destroy(q);
-    return fail(FLS_ECUSOLVER, "geqrf status %d info %d", (int)st, h_info);
   }
   if (dmin == 0.0) {
     fls_qr_destroy(q);
@@ -893,6 +909,19 @@ fls_status fls_qr_destroy(fls_qr *q) {
   cudaFree(q->tau);
   delete q;
   return FLS_OK;
+}
+
+fls_status fls_geqrf(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda, int64_t n_cols,
+                     double *tau) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!M || !tau) return fail(FLS_EINVAL, "M or tau is NULL");
+  if (n_rows < 1 || n_cols < 1 || lda < n_rows)
+    return fail(FLS_EINVAL, "bad sizes n_rows %lld n_cols %lld lda %lld", (long long)n_rows,
+                (long long)n_cols, (long long)lda);
+  DeviceGuard g(ctx->device);
+  if (fls_status s = fls_sync(ctx)) return s;
+  if (fls_status s = ensure_handles(ctx)) return s;
+  return geqrf_inplace(ctx, M, n_rows, lda, n_cols, tau);
 }
 
 fls_status fls_qr_r(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda, int64_t n_cols,

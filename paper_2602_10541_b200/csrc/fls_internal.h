@@ -1,5 +1,6 @@
 // fls_internal.h -- host-side internals of libfls (ctx, errors, kernel launch interfaces).
 #pragma once
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -180,5 +181,11 @@ cudaError_t launch_axpy(int64_t n, double alpha, const double *x, const double *
                         cudaStream_t st);
 cudaError_t launch_frob2(const double *A, int64_t lda, int64_t m, int64_t n, double *partials,
                          int nblk, double *out, cudaStream_t st);
+
+// blocked Householder QR (fls_qr.cu), geqrf output format; nullptr or a failure message
+const char *qr_blocked(cublasHandle_t h, cudaStream_t st, double *A, int64_t m, int64_t n,
+                       int64_t lda, double *tau, cudaError_t *cerr, cublasStatus_t *berr);
+int qr_panel_width();
+int64_t qr_blocked_max_rows();  // taller blocks use cusolverDnDgeqrf
 
 }  // namespace fls

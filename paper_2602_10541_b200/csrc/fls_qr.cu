@@ -1,0 +1,425 @@
+// fls_qr.cu -- blocked Householder QR for the least-squares solve (Alg. 1 line 5, P:L124;
+// Tikhonov form P:L156-160).  Output format = LAPACK / cuSOLVER geqrf: R in the upper
+// trapezoid, the Householder vectors v_j (v_jj = 1 implicit) below the diagonal, tau_j, so
+// cuSOLVER ormqr and cuBLAS trsv consume it unchanged.
+//
+// Why not one cusolverDnDgeqrf call: on this pool's B200 its panel factorisation costs ~30-65 us
+// per column (a few launches each), so geqrf runs at 6 / 16 / 22 TFLOP/s on C3 / C4 / C5-subset
+// while DGEMM runs at 34-36 TFLOP/s at the same shapes (tools/probe_dgemm.py).  Here:
+//   * outer loop over panels of nb columns (compact WY: H_1..H_nb = I - V T V^T), the trailing
+//     matrix updated by two DGEMMs and one DTRMM per panel;
+//   * each panel factored recursively (Elmroth-Gustavson): left half, WY update of the right
+//     half, right half, then T12 = -T1 (V1^T V2) T2 -- all cuBLAS DGEMM / DTRMM;
+//   * the recursion's leaves (<= 32 columns, fewer when the rows are many) run in ONE
+//     cooperative kernel per leaf: each CTA keeps its row slab of the leaf in shared memory,
+//     and one grid-wide barrier per column separates "partial sums of ||x||^2 and x^T a_c over
+//     my rows" from "finish dlarfg, update my rows", so a leaf column costs one grid sync
+//     instead of several kernel launches and no global-memory pass.
+// Householder vector per column (LAPACK dlarfg): beta = -sign(alpha) ||[alpha; x]||,
+// tau = (beta - alpha) / beta, v = x / (alpha - beta); ||x|| = 0 gives tau = 0 (H = I).
+#include <cooperative_groups.h>
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "fls_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace fls {
+
+constexpr int kQrB = 32;    // leaf width (columns per cooperative kernel)
+constexpr int kQrNT = 256;  // threads per CTA of the leaf kernel
+constexpr int kQrW = kQrNT / 32;
+constexpr size_t kQrSlab = 216 * 1024;  // shared-memory slab budget per CTA (one CTA per SM)
+constexpr int kQrMaxGrid = 256;         // leaf CTAs at most (one per SM)
+constexpr int kQrMinLeaf = 4;           // narrowest leaf; taller blocks go to cuSOLVER
+
+struct QrLeafArgs {
+  double *A;     // leaf top-left (its diagonal starts at row 0), column-major
+  int64_t lda;
+  int64_t m;     // rows from the leaf's top
+  int64_t rc;    // rows per CTA (the shared-memory slab height)
+  int32_t b;     // columns (<= kQrB)
+  double *V;     // explicit V (zeros above, ones on the diagonal), same row origin as A
+  int64_t ldv;
+  double *tau;
+  double *part;  // [2][gridDim.x][kQrB + 1] per-CTA partial sums
+  double *rowb;  // [2][kQrB + 1] the diagonal row a_jj.. at the start of column jj
+};
+
+// One leaf (b <= 32 columns, m rows) of the recursive QR.  CTA k owns rows [k rc, (k+1) rc)
+// and keeps them (b columns) in shared memory for the whole leaf: the global memory traffic is
+// one read and one write of the leaf plus the per-column partial sums.
+__global__ void __launch_bounds__(kQrNT) qr_leaf_kernel(const QrLeafArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double slab[];  // [b][rc], column-major
+  __shared__ double red[kQrW][kQrB + 1];
+  __shared__ double tot[kQrB + 1], rowv[kQrB + 1];
+  __shared__ double s_tau, s_scale, s_beta;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t rc = a.rc;
+  const int64_t r_lo = (int64_t)blockIdx.x * rc;
+  const int nr = (int)(r_lo >= a.m ? 0 : (a.m - r_lo < rc ? a.m - r_lo : rc));
+  const int b = a.b;
+  for (int q = 0; q < b; ++q)
+    for (int r = threadIdx.x; r < nr; r += kQrNT) slab[q * rc + r] = a.A[(int64_t)q * a.lda + r_lo + r];
+  __syncthreads();
+  for (int jj = 0; jj < b; ++jj) {
+    const int nc = b - jj;  // slot 0: ||x||^2, slot q: x^T a_{jj+q}
+    double *part = a.part + (size_t)(jj & 1) * gridDim.x * (kQrB + 1);
+    double *rowb = a.rowb + (jj & 1) * (kQrB + 1);
+    const double *xs = slab + jj * rc;
+    // ---- partial sums over my rows below the diagonal
+    double acc[kQrB];
+#pragma unroll
+    for (int q = 0; q < kQrB; ++q) acc[q] = 0.0;
+    const int r0 = jj + 1 - r_lo > 0 ? (int)(jj + 1 - r_lo) : 0;
+    for (int r = r0 + threadIdx.x; r < nr; r += kQrNT) {
+      const double x = xs[r];
+      acc[0] = fma(x, x, acc[0]);
+#pragma unroll
+      for (int q = 1; q < kQrB; ++q)
+        if (q < nc) acc[q] = fma(x, xs[q * rc + r], acc[q]);
+    }
+    // 32 warp sums in 31 shuffles (recursive halving): afterwards lane l holds sum of acc[l]
+#pragma unroll
+    for (int sh = 16; sh >= 1; sh >>= 1) {
+      const bool up = lane & sh;
+#pragma unroll
+      for (int t = 0; t < sh; ++t) {
+        const double send = up ? acc[t] : acc[t + sh];
+        const double keep = up ? acc[t + sh] : acc[t];
+        acc[t] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
+      }
+    }
+    red[warp][lane] = acc[0];
+    __syncthreads();
+    if (threadIdx.x < nc) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < kQrW; ++w) s += red[w][threadIdx.x];
+      part[(int64_t)blockIdx.x * (kQrB + 1) + threadIdx.x] = s;
+    }
+    // the owner of row jj publishes it before the barrier
+    if (jj >= r_lo && jj < r_lo + nr && threadIdx.x < nc)
+      rowb[threadIdx.x] = xs[threadIdx.x * rc + (jj - r_lo)];
+    grid.sync();
+    // ---- totals (warp q sums slot q over the CTAs; same order in every CTA), then dlarfg;
+    // the diagonal row is fetched in the same round trip
+    if (threadIdx.x >= kQrNT - 32 && threadIdx.x - (kQrNT - 32) < nc)
+      rowv[threadIdx.x - (kQrNT - 32)] = rowb[threadIdx.x - (kQrNT - 32)];
+    for (int q = warp; q < nc; q += kQrW) {
+      double v[kQrMaxGrid / 32];  // all loads in flight before the adds (one L2 round trip)
+#pragma unroll
+      for (int t = 0; t < kQrMaxGrid / 32; ++t) {
+        const unsigned k = lane + 32 * t;
+        v[t] = k < gridDim.x ? part[(int64_t)k * (kQrB + 1) + q] : 0.0;
+      }
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < kQrMaxGrid / 32; ++t) s += v[t];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) tot[q] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double alpha = rowv[0];
+      double tau = 0.0, scale = 0.0, beta = alpha;
+      if (tot[0] > 0.0) {
+        beta = -copysign(hypot(alpha, sqrt(tot[0])), alpha);
+        tau = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      s_tau = tau;
+      s_scale = scale;
+      s_beta = beta;
+    }
+    __syncthreads();
+    const double tau = s_tau, scale = s_scale;
+    // tau * (v^T a_c), v_jj = 1
+    if (threadIdx.x >= 1 && threadIdx.x < nc)
+      tot[threadIdx.x] = tau * fma(scale, tot[threadIdx.x], rowv[threadIdx.x]);
+    __syncthreads();
+    // ---- apply H_jj to my rows of the remaining columns (v overwrites x below the diagonal)
+    double *xw = slab + jj * rc;
+    const int rd = jj - r_lo >= 0 ? (int)(jj - r_lo) : -1;  // my row index of the diagonal
+    for (int r = (rd > 0 ? rd : 0) + threadIdx.x; r < nr; r += kQrNT) {
+      if (r > rd) {
+        const double v = tau != 0.0 ? xw[r] * scale : xw[r];
+        xw[r] = v;
+#pragma unroll
+        for (int q = 1; q < kQrB; ++q)
+          if (q < nc) xw[q * rc + r] -= v * tot[q];
+      } else {  // r == rd: the diagonal row
+        xw[r] = s_beta;
+#pragma unroll
+        for (int q = 1; q < kQrB; ++q)
+          if (q < nc) xw[q * rc + r] -= tot[q];
+      }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.tau[jj] = tau;
+    __syncthreads();
+  }
+  // write back R / v and the explicit V (zeros above, ones on the diagonal)
+  for (int q = 0; q < b; ++q)
+    for (int r = threadIdx.x; r < nr; r += kQrNT) {
+      const int64_t i = r_lo + r;
+      const double x = slab[q * rc + r];
+      a.A[(int64_t)q * a.lda + i] = x;
+      a.V[(int64_t)q * a.ldv + i] = i > q ? x : (i == q ? 1.0 : 0.0);
+    }
+}
+
+// T of a leaf from S = V^T V (b x b) and tau (LAPACK dlarft, forward, columnwise):
+// T_jj = tau_j, T(0:j, j) = -tau_j T(0:j, 0:j) S(0:j, j)
+__global__ void qr_larft_kernel(const double *S, int b, const double *tau, double *T, int64_t ldt) {
+  __shared__ double Ts[kQrB][kQrB + 1];
+  __shared__ double Ss[kQrB][kQrB + 1];
+  __shared__ double tmp[kQrB], taus[kQrB];
+  const int i = threadIdx.x;
+  if (i < b) {
+    for (int j = 0; j < b; ++j) Ss[i][j] = S[(int64_t)j * b + i];
+    taus[i] = tau[i];
+  }
+  __syncthreads();
+  for (int j = 0; j < b; ++j) {
+    if (i < j) {
+      double t = 0.0;
+      for (int l = i; l < j; ++l) t += Ts[i][l] * Ss[l][j];
+      tmp[i] = -taus[j] * t;
+    }
+    __syncthreads();
+    if (i < b) Ts[i][j] = i < j ? tmp[i] : (i == j ? taus[j] : 0.0);
+    __syncthreads();
+  }
+  if (i < b)
+    for (int j = 0; j < b; ++j) T[(int64_t)j * ldt + i] = Ts[i][j];
+}
+
+int64_t qr_leaf_rows();
+
+namespace {
+
+struct QrCtx {
+  cublasHandle_t h;
+  cudaStream_t st;
+  double *A;
+  int64_t lda;
+  double *V;     // panel V, ldv rows
+  int64_t ldv;
+  double *T;     // nb x nb
+  int64_t ldt;
+  double *W;     // nb x n scratch
+  double *S;     // kQrB x kQrB
+  double *part, *rowb;
+  int grid;        // CTAs of a leaf launch (one per SM)
+  int bleaf;       // leaf width for the current panel (slab fits shared memory)
+  const char *fail = nullptr;
+  cudaError_t cerr = cudaSuccess;
+  cublasStatus_t berr = CUBLAS_STATUS_SUCCESS;
+};
+
+bool ok_blas(QrCtx &q, cublasStatus_t s, const char *what) {
+  if (s != CUBLAS_STATUS_SUCCESS && q.berr == CUBLAS_STATUS_SUCCESS) {
+    q.berr = s;
+    q.fail = what;
+  }
+  return s == CUBLAS_STATUS_SUCCESS;
+}
+
+bool ok_cuda(QrCtx &q, cudaError_t e, const char *what) {
+  if (e != cudaSuccess && q.cerr == cudaSuccess) {
+    q.cerr = e;
+    q.fail = what;
+  }
+  return e == cudaSuccess;
+}
+
+// factor panel columns [c, c+w) (rows [c, mp) of the panel whose top-left is P), filling V and
+// the diagonal block T[c:c+w, c:c+w] of the panel's T
+bool rec_panel(QrCtx &q, double *P, int64_t mp, int64_t c, int64_t w, double *tau) {
+  const double one = 1.0, zero = 0.0, mone = -1.0;
+  double *Vc = q.V + c * q.ldv;  // V columns c.. (rows from the panel top)
+  if (w <= q.bleaf) {
+    if (c > 0 && !ok_cuda(q, cudaMemset2DAsync(Vc, q.ldv * sizeof(double), 0, c * sizeof(double), w, q.st),
+                          "V zero"))
+      return false;
+    QrLeafArgs a;
+    a.A = P + c * q.lda + c;
+    a.lda = q.lda;
+    a.m = mp - c;
+    a.b = (int32_t)w;
+    a.V = Vc + c;
+    a.ldv = q.ldv;
+    a.tau = tau + c;
+    a.part = q.part;
+    a.rowb = q.rowb;
+    // fewest CTAs that hold the leaf in shared memory, but about qr_leaf_rows() rows each:
+    // fewer CTAs make the per-column grid barrier and partial-sum reduction cheaper
+    const int64_t slab_rows = (int64_t)kQrSlab / (w * (int64_t)sizeof(double));
+    int64_t g = std::max<int64_t>((a.m + qr_leaf_rows() - 1) / qr_leaf_rows(),
+                                  (a.m + slab_rows - 1) / slab_rows);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(q.grid, g));
+    a.rc = (a.m + grid - 1) / grid;
+    const size_t smem = (size_t)w * a.rc * sizeof(double);
+    void *args[] = {&a};
+    if (!ok_cuda(q, cudaLaunchCooperativeKernel((const void *)qr_leaf_kernel, dim3(grid), dim3(kQrNT),
+                                                args, smem, q.st),
+                 "qr_leaf_kernel"))
+      return false;
+    // T leaf = larft(V_leaf^T V_leaf, tau)
+    if (!ok_blas(q, cublasDgemm(q.h, CUBLAS_OP_T, CUBLAS_OP_N, (int)w, (int)w, (int)(mp - c), &one,
+                                Vc + c, (int)q.ldv, Vc + c, (int)q.ldv, &zero, q.S, (int)w),
+                 "leaf V^T V"))
+      return false;
+    qr_larft_kernel<<<1, kQrB, 0, q.st>>>(q.S, (int)w, tau + c, q.T + c * q.ldt + c, q.ldt);
+    return ok_cuda(q, cudaGetLastError(), "qr_larft_kernel");
+  }
+  const int64_t B = q.bleaf;
+  int64_t w1 = ((w / 2 + B - 1) / B) * B;
+  if (w1 >= w) w1 = w - B;
+  const int64_t w2 = w - w1;
+  if (!rec_panel(q, P, mp, c, w1, tau)) return false;
+  // right half rows [c, mp): C -= V1 T1^T V1^T C
+  double *C = P + (c + w1) * q.lda + c;
+  const double *V1 = Vc + c;  // rows [c, mp) of columns c..c+w1
+  const double *T1 = q.T + c * q.ldt + c;
+  const int k1 = (int)(mp - c);
+  if (!ok_blas(q, cublasDgemm(q.h, CUBLAS_OP_T, CUBLAS_OP_N, (int)w1, (int)w2, k1, &one, V1, (int)q.ldv,
+                              C, (int)q.lda, &zero, q.W, (int)w1), "panel V1^T C") ||
+      !ok_blas(q, cublasDtrmm(q.h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T,
+                              CUBLAS_DIAG_NON_UNIT, (int)w1, (int)w2, &one, T1, (int)q.ldt, q.W,
+                              (int)w1, q.W, (int)w1), "panel T1^T W") ||
+      !ok_blas(q, cublasDgemm(q.h, CUBLAS_OP_N, CUBLAS_OP_N, k1, (int)w2, (int)w1, &mone, V1, (int)q.ldv,
+                              q.W, (int)w1, &one, C, (int)q.lda), "panel C -= V1 W"))
+    return false;
+  if (!rec_panel(q, P, mp, c + w1, w2, tau)) return false;
+  // T12 = -T1 (V1^T V2) T2 over rows [c + w1, mp) (V2 is zero above its diagonal)
+  double *T12 = q.T + (c + w1) * q.ldt + c;
+  const double *T2 = q.T + (c + w1) * q.ldt + (c + w1);
+  const int k2 = (int)(mp - c - w1);
+  return ok_blas(q, cublasDgemm(q.h, CUBLAS_OP_T, CUBLAS_OP_N, (int)w1, (int)w2, k2, &one,
+                                Vc + c + w1, (int)q.ldv, q.V + (c + w1) * q.ldv + c + w1, (int)q.ldv,
+                                &zero, T12, (int)q.ldt), "T12 gemm") &&
+         ok_blas(q, cublasDtrmm(q.h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                                CUBLAS_DIAG_NON_UNIT, (int)w1, (int)w2, &mone, T1, (int)q.ldt, T12,
+                                (int)q.ldt, T12, (int)q.ldt), "T12 left trmm") &&
+         ok_blas(q, cublasDtrmm(q.h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                                CUBLAS_DIAG_NON_UNIT, (int)w1, (int)w2, &one, T2, (int)q.ldt, T12,
+                                (int)q.ldt, T12, (int)q.ldt), "T12 right trmm");
+}
+
+}  // namespace
+
+int64_t qr_leaf_rows() {
+  static int64_t r = 0;
+  if (!r) {
+    r = 256;
+    if (const char *s = getenv("FLS_QR_LEAF_ROWS")) {  // tuning sweeps only
+      const int64_t v = atoll(s);
+      if (v >= 32) r = v;
+    }
+  }
+  return r;
+}
+
+int64_t qr_blocked_max_rows() {
+  static int64_t mx = 0;
+  if (!mx) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    mx = (int64_t)std::max(1, std::min(sms, kQrMaxGrid)) * (kQrSlab / (kQrMinLeaf * sizeof(double)));
+  }
+  return mx;
+}
+
+int qr_panel_width() {
+  static int nb = 0;
+  if (!nb) {
+    nb = 256;
+    if (const char *s = getenv("FLS_QR_NB")) {  // tuning sweeps only
+      const int v = atoi(s);
+      if (v >= kQrB) nb = (v / kQrB) * kQrB;
+    }
+  }
+  return nb;
+}
+
+// A (m x n, lda) -> R / V / tau in place.  Returns 0 or a message (static string).
+const char *qr_blocked(cublasHandle_t h, cudaStream_t st, double *A, int64_t m, int64_t n,
+                       int64_t lda, double *tau, cudaError_t *cerr, cublasStatus_t *berr) {
+  *cerr = cudaSuccess;
+  *berr = CUBLAS_STATUS_SUCCESS;
+  const int64_t k = m < n ? m : n;
+  if (k <= 0) return nullptr;
+  const int64_t nb = qr_panel_width();
+  QrCtx q;
+  q.h = h;
+  q.st = st;
+  q.A = A;
+  q.lda = lda;
+  q.ldv = (m + 3) / 4 * 4;
+  q.ldt = nb;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  q.grid = std::max(1, std::min(sms, kQrMaxGrid));
+  if (m > qr_blocked_max_rows()) {
+    *cerr = cudaErrorInvalidValue;
+    return "rows exceed the leaf slab capacity";
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(qr_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQrSlab);
+    attr = true;
+  }
+  const size_t nV = (size_t)q.ldv * nb, nT = (size_t)nb * nb, nW = (size_t)nb * (n > nb ? n : nb);
+  const size_t nS = (size_t)kQrB * kQrB, nP = (size_t)2 * q.grid * (kQrB + 1), nR = 2 * (kQrB + 1);
+  double *ws = nullptr;
+  cudaError_t e = cudaMallocAsync((void **)&ws, (nV + nT + nW + nS + nP + nR) * sizeof(double), st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *cerr = e;
+    return "qr workspace allocation";
+  }
+  q.V = ws;
+  q.T = q.V + nV;
+  q.W = q.T + nT;
+  q.S = q.W + nW;
+  q.part = q.S + nS;
+  q.rowb = q.part + nP;
+  const double one = 1.0, zero = 0.0, mone = -1.0;
+  bool good = ok_blas(q, cublasSetStream(h, st), "cublasSetStream");
+  for (int64_t j = 0; good && j < k; j += nb) {
+    const int64_t w = nb < k - j ? nb : k - j;
+    const int64_t mp = m - j;
+    double *P = A + j * lda + j;
+    const int64_t rc = (mp + q.grid - 1) / q.grid;
+    q.bleaf = (int)std::min<int64_t>(kQrB, (int64_t)kQrSlab / (rc * (int64_t)sizeof(double)));
+    good = rec_panel(q, P, mp, 0, w, tau + j);
+    const int64_t nt = n - j - w;
+    if (good && nt > 0) {  // trailing update C -= V T^T V^T C
+      double *C = P + w * lda;
+      good = ok_blas(q, cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)w, (int)nt, (int)mp, &one, q.V,
+                                    (int)q.ldv, C, (int)lda, &zero, q.W, (int)w), "trailing V^T C") &&
+             ok_blas(q, cublasDtrmm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T,
+                                    CUBLAS_DIAG_NON_UNIT, (int)w, (int)nt, &one, q.T, (int)q.ldt, q.W,
+                                    (int)w, q.W, (int)w), "trailing T^T W") &&
+             ok_blas(q, cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)mp, (int)nt, (int)w, &mone, q.V,
+                                    (int)q.ldv, q.W, (int)w, &one, C, (int)lda), "trailing C -= V W");
+    }
+  }
+  cudaFreeAsync(ws, st);
+  *cerr = q.cerr;
+  *berr = q.berr;
+  return good ? nullptr : q.fail;
+}
+
+}  // namespace fls

@@ -4,7 +4,7 @@ Assembly needs no collective: rank r owns global rows
 [floor(r R / P), floor((r+1) R / P)) and every rank regenerates W, b from the seed.
 The solve has one real exchange step (TSQR, "QR or SVD"; Tikhonov form P:L158):
 
-    local:  [A_r | b_r] = Q_r R_r                      (fls_qr_r, cuSOLVER geqrf on each GPU)
+    local:  [A_r | b_r] = Q_r R_r                      (fls_qr_r, Householder QR on each GPU)
     gather: R_0 .. R_{P-1} -> root                      (torch.distributed / NCCL over NVLink)
     root:   [R_0; ...; R_{P-1}; sqrt(mu) I | 0] = Q R   (fls_solve: geqrf + trsv)
     bcast:  beta

@@ -25,7 +25,7 @@ from ._abi import FLS_COL_MAJOR, FLS_ROW_MAJOR, FlsError, check
 Term = Tuple[Sequence[int], float, int]   # (alpha, coef, field)
 
 __all__ = ["Context", "Block", "fls_features", "fls_assemble", "fls_features_assemble", "fls_solve", "fls_qr_r",
-           "fls_frob2", "fls_eval", "fls_sync", "fls_ctx_timing", "fls_ctx_timing_read",
+           "fls_frob2", "fls_geqrf", "fls_eval", "fls_sync", "fls_ctx_timing", "fls_ctx_timing_read",
            "fls_assemble_host", "HostBlockSet", "BlockSet", "fls_features_blocks", "QRFactor",
            "make_nonlinearity", "fls_nl_residual", "fls_axpy", "fls_features_transform",
            "fls_bandwidth_grad", "fls_sample_box", "fls_sample_faces", "FlsError", "FLS_COL_MAJOR", "FLS_ROW_MAJOR",
@@ -457,6 +457,18 @@ def fls_solve(ctx: Context, Ab: torch.Tensor, n_rows: int, lda: int, n_features:
     check(_abi.load().fls_solve(ctx.handle, _ptr(Ab), int(n_rows), int(lda), int(n_features),
                                 float(sqrt_mu), _ptr(beta), C.byref(res)))
     return beta, res.value
+
+
+def fls_geqrf(ctx: Context, M: torch.Tensor, n_rows: int, lda: int, n_cols: int,
+              tau: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Householder QR of the flat column-major block M in place (geqrf format); returns tau"""
+    _dev_f64(M, "M")
+    if M.numel() < lda * (n_cols - 1) + n_rows:
+        raise ValueError("M too small for n_rows x n_cols at lda")
+    k = min(n_rows, n_cols)
+    tau = torch.empty((k,), dtype=torch.float64, device=M.device) if tau is None else tau
+    check(_abi.load().fls_geqrf(ctx.handle, _ptr(M), int(n_rows), int(lda), int(n_cols), _ptr(tau)))
+    return tau
 
 
 def fls_qr_r(ctx: Context, M: torch.Tensor, n_rows: int, lda: int, n_cols: int,

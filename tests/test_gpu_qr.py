@@ -1,0 +1,125 @@
+"""libfls's blocked Householder QR (fls_geqrf; the factorisation behind fls_solve, fls_qr_factor,
+fls_qr_r) against the mathematics: Q R = A and Q^T Q = I to rounding, |diag R| equal to
+cuSOLVER geqrf's (torch.geqrf) on full-rank inputs, tau = 0 for an already-zero column, and the
+LAPACK storage format (torch.linalg.householder_product rebuilds Q from it)."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2602_10541_b200 import fls
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return fls.Context()
+
+
+@pytest.fixture(params=["blocked", "cusolver"], autouse=True)
+def method(request, monkeypatch):
+    """every test runs on libfls's blocked QR and on the cuSOLVER path (same storage format)"""
+    monkeypatch.setenv("FLS_QR", request.param)
+    return request.param
+
+
+def _factor(ctx, A, pad=3):
+    m, n = A.shape
+    lda = m + pad
+    M = torch.zeros((n, lda), dtype=torch.float64, device="cuda")
+    M[:, :m] = A.T
+    tau = fls.fls_geqrf(ctx, M.view(-1), m, lda, n)
+    torch.cuda.synchronize()
+    assert torch.all(M[:, m:] == 0), "rows past n_rows (lda padding) were written"
+    return M[:, :m].T.contiguous(), tau
+
+
+def _check(A, a, tau, tol=1e-13):
+    m, n = A.shape
+    k = min(m, n)
+    Q = torch.linalg.householder_product(a[:, :k], tau)          # m x k
+    R = torch.triu(a[:k, :])
+    nA = torch.linalg.norm(A)
+    assert float(torch.linalg.norm(Q @ R - A) / nA) <= tol
+    assert float(torch.linalg.norm(Q.T @ Q - torch.eye(k, dtype=A.dtype, device=A.device))) <= tol * k ** 0.5
+
+
+@pytest.mark.parametrize("m,n", [(100, 37), (1000, 300), (3000, 700), (777, 513), (20000, 1100),
+                                 (64, 64), (33, 1), (1, 5), (300, 520), (40, 100)])
+def test_geqrf_reconstructs_and_matches_cusolver_diag(ctx, m, n):
+    g = torch.Generator(device="cuda").manual_seed(m * 1000 + n)
+    A = torch.randn((m, n), dtype=torch.float64, device="cuda", generator=g)
+    a, tau = _factor(ctx, A)
+    _check(A, a, tau)
+    a_ref, _ = torch.geqrf(A)
+    k = min(m, n)
+    d, d_ref = a.diagonal()[:k].abs(), a_ref.diagonal()[:k].abs()
+    assert float(((d - d_ref).abs() / d_ref).max()) <= 1e-10
+
+
+def test_geqrf_rank_deficient_and_zero_columns(ctx):
+    g = torch.Generator(device="cuda").manual_seed(7)
+    m, n = 2500, 600
+    B = torch.randn((m, 150), dtype=torch.float64, device="cuda", generator=g)
+    A = B @ torch.randn((150, n), dtype=torch.float64, device="cuda", generator=g)  # rank 150
+    A[:, 5] = 0.0                      # zero column: tau_5 = 0, H_5 = I
+    A[:, 300] = A[:, 299]              # duplicate column
+    a, tau = _factor(ctx, A)
+    _check(A, a, tau, tol=1e-12)
+    assert float(tau[5]) == 0.0
+    d = a.diagonal().abs()
+    nA = float(torch.linalg.norm(A))
+    assert float(d[160:].max()) <= 1e-11 * nA          # numerical rank shows on the diagonal
+
+
+def test_geqrf_solves_least_squares_like_lstsq(ctx):
+    """[A | b] factored together: R beta = (Q^T b)[0:n] is the LAPACK least-squares solution and
+    |R(n, n)| the residual norm (how fls_solve uses it)"""
+    g = torch.Generator(device="cuda").manual_seed(11)
+    m, n = 5000, 800
+    A = torch.randn((m, n), dtype=torch.float64, device="cuda", generator=g)
+    b = torch.randn((m, 1), dtype=torch.float64, device="cuda", generator=g)
+    a, _ = _factor(ctx, torch.cat([A, b], 1))
+    beta = torch.linalg.solve_triangular(torch.triu(a[:n, :n]), a[:n, n:], upper=True)
+    ref = torch.linalg.lstsq(A.cpu(), b.cpu()).solution.cuda()
+    assert float(torch.linalg.norm(beta - ref) / torch.linalg.norm(ref)) <= 1e-11
+    res = float(torch.linalg.norm(A @ ref - b))
+    assert abs(abs(float(a[n, n])) - res) <= 1e-10 * res
+
+
+def test_geqrf_errors(ctx):
+    M = torch.zeros(100, dtype=torch.float64, device="cuda")
+    with pytest.raises(fls.FlsError):
+        fls.fls_geqrf(ctx, M, 10, 5, 3)                 # lda < n_rows
+    with pytest.raises(fls.FlsError):
+        fls.fls_geqrf(ctx, M, 0, 10, 3)
+
+
+@pytest.mark.parametrize("name,size", [("c1_poisson1d", "full"), ("c2_poisson2d", "full"),
+                                       ("c5_biharm3d", "mini")])
+def test_solve_parity_with_oracle_on_both_qr_paths(ctx, name, size):
+    """fls_solve (assembly -> QR -> trsv) on numerically rank-deficient systems (C1: rank ~41 of
+    500) and with the relative ridge (C5): fitted u vs the oracle chain <= 1e-6 on either path"""
+    import math
+
+    import numpy as np
+
+    import oracle
+    import workloads as wl
+    from gpu_common import U_TOL, dev_blocks
+    p = wl.make_problem(name, size)
+    W, b = p.parity_features()
+    Wd, bd = torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda()
+    F, R = p.n_features, p.n_rows
+    ridge = p.ridge_rel > 0
+    Ab, lda = fls.fls_assemble(ctx, Wd, bd, dev_blocks(p), extra_rows=F if ridge else 0)
+    sq = p.ridge_rel * math.sqrt(fls.fls_frob2(ctx, Ab, R, lda, F)) if ridge else 0.0
+    beta, _ = fls.fls_solve(ctx, Ab, R, lda, F, sq)
+    Xt = p.test_points(10_000)
+    u_gpu = fls.fls_eval(ctx, Wd, bd, beta, torch.from_numpy(Xt).cuda()).cpu().numpy()
+    Ao, ro, _ = oracle.assemble(W, b, p.blocks, want_scale=False)
+    beta_o, _, _ = oracle.lstsq(Ao, ro, ridge_rel=p.ridge_rel)
+    u_orc = oracle.evaluate(W, b, beta_o, Xt)
+    assert np.linalg.norm(u_gpu - u_orc) / np.linalg.norm(u_orc) <= U_TOL
