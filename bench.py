@@ -353,6 +353,7 @@ def solve_measure(args, world, rank, local):
            "method": "Householder QR (fls_geqrf: blocked compact-WY on cuBLAS DGEMM + cooperative leaf kernel) + trsv" + (" / TSQR over ranks" if world > 1 else ""),
            "qr_flops": 2.0 * (R + extra) * (F + 1) ** 2 - 2.0 / 3.0 * (F + 1) ** 3,
            "resid_norm": res}
+    out["qr_tflops"] = out["qr_flops"] / (ph[2] / 1e3) / 1e12
     if args.workload != "c5_biharm3d":   # C5 has no BC rows: u* is not the LS solution (A12)
         out["rel_l2_vs_u_star"] = float(np.linalg.norm(uh - us) / np.linalg.norm(us))
     return out

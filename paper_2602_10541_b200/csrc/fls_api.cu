@@ -24,6 +24,8 @@ struct fls_ctx {
   double *d_scratch = nullptr;        // small device scratch (min diag, frob partials)
   double *ws = nullptr;               // per-feature prefactor records
   size_t ws_bytes = 0;
+  double *qws = nullptr;              // blocked-QR workspace (grow-only; + tau scratch)
+  size_t qws_bytes = 0;
   cusolverDnHandle_t solver = nullptr;
   cublasHandle_t blas = nullptr;
   // optional per-launch timing of the assembly kernels (fls_ctx_timing)
@@ -213,6 +215,7 @@ fls_status fls_ctx_destroy(fls_ctx *ctx) {
   cudaFree(ctx->hin);
   cudaFree(ctx->hout);
   cudaFree(ctx->ws);
+  cudaFree(ctx->qws);
   cudaFree(ctx->d_err);
   cudaFree(ctx->d_scratch);
   delete ctx;
@@ -711,15 +714,22 @@ static fls_status geqrf_inplace(fls_ctx *ctx, double *M, int64_t m, int64_t lda,
   // small problems (C1: 1,002 x 501) are launch-latency bound: one cuSOLVER call is faster
   const int method = qr_method();
   if (method != 1 && m <= qr_blocked_max_rows() && (method == 2 || n >= kQrBlockedMinCols)) {
-    double *tau = tau_out;
-    if (!tau && cudaMallocAsync((void **)&tau, (size_t)(k > 0 ? k : 1) * sizeof(double), ctx->stream) != cudaSuccess) {
-      cudaGetLastError();
-      return fail(FLS_ENOMEM, "qr tau");
+    const size_t need = (qr_blocked_ws(m, n) + (size_t)(k > 0 ? k : 1)) * sizeof(double);
+    if (need > ctx->qws_bytes) {  // grow-only: repeated solves (Newton, RHS sweeps) reuse it
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(ctx->qws);
+      ctx->qws = nullptr;
+      ctx->qws_bytes = 0;
+      if (cudaMalloc((void **)&ctx->qws, need) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(FLS_ENOMEM, "blocked QR workspace of %zu bytes", need);
+      }
+      ctx->qws_bytes = need;
     }
+    double *tau = tau_out ? tau_out : ctx->qws + qr_blocked_ws(m, n);
     cudaError_t ce;
     cublasStatus_t be;
-    const char *msg = qr_blocked(ctx->blas, ctx->stream, M, m, n, lda, tau, &ce, &be);
-    if (!tau_out) cudaFreeAsync(tau, ctx->stream);
+    const char *msg = qr_blocked(ctx->blas, ctx->stream, M, m, n, lda, tau, ctx->qws, &ce, &be);
     cudaError_t e = cudaStreamSynchronize(ctx->stream);
     if (msg) {
       if (ce == cudaErrorMemoryAllocation) return fail(FLS_ENOMEM, "blocked QR: %s", msg);

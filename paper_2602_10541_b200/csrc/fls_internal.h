@@ -184,7 +184,9 @@ cudaError_t launch_frob2(const double *A, int64_t lda, int64_t m, int64_t n, dou
 
 // blocked Householder QR (fls_qr.cu), geqrf output format; nullptr or a failure message
 const char *qr_blocked(cublasHandle_t h, cudaStream_t st, double *A, int64_t m, int64_t n,
-                       int64_t lda, double *tau, cudaError_t *cerr, cublasStatus_t *berr);
+                       int64_t lda, double *tau, double *ws, cudaError_t *cerr,
+                       cublasStatus_t *berr);
+size_t qr_blocked_ws(int64_t m, int64_t n);  // doubles of ws (incl. nothing for tau)
 int qr_panel_width();
 int64_t qr_blocked_max_rows();  // taller blocks use cusolverDnDgeqrf
 

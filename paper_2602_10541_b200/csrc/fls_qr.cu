@@ -352,9 +352,30 @@ int qr_panel_width() {
   return nb;
 }
 
-// A (m x n, lda) -> R / V / tau in place.  Returns 0 or a message (static string).
+static int qr_grid() {
+  static int g = 0;
+  if (!g) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    g = std::max(1, std::min(sms, kQrMaxGrid));
+  }
+  return g;
+}
+
+// workspace (doubles) qr_blocked needs for an m x n block: panel V, T, W, leaf S, partials
+size_t qr_blocked_ws(int64_t m, int64_t n) {
+  const int64_t nb = qr_panel_width();
+  const int64_t ldv = (m + 3) / 4 * 4;
+  return (size_t)ldv * nb + (size_t)nb * nb + (size_t)nb * (n > nb ? n : nb) + (size_t)kQrB * kQrB +
+         (size_t)2 * qr_grid() * (kQrB + 1) + 2 * (kQrB + 1);
+}
+
+// A (m x n, lda) -> R / V / tau in place, ws = qr_blocked_ws(m, n) doubles (caller-owned, so
+// repeated solves do not allocate).  Returns 0 or a message (static string).
 const char *qr_blocked(cublasHandle_t h, cudaStream_t st, double *A, int64_t m, int64_t n,
-                       int64_t lda, double *tau, cudaError_t *cerr, cublasStatus_t *berr) {
+                       int64_t lda, double *tau, double *ws, cudaError_t *cerr,
+                       cublasStatus_t *berr) {
   *cerr = cudaSuccess;
   *berr = CUBLAS_STATUS_SUCCESS;
   const int64_t k = m < n ? m : n;
@@ -367,10 +388,7 @@ const char *qr_blocked(cublasHandle_t h, cudaStream_t st, double *A, int64_t m, 
   q.lda = lda;
   q.ldv = (m + 3) / 4 * 4;
   q.ldt = nb;
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  q.grid = std::max(1, std::min(sms, kQrMaxGrid));
+  q.grid = qr_grid();
   if (m > qr_blocked_max_rows()) {
     *cerr = cudaErrorInvalidValue;
     return "rows exceed the leaf slab capacity";
@@ -381,14 +399,7 @@ const char *qr_blocked(cublasHandle_t h, cudaStream_t st, double *A, int64_t m, 
     attr = true;
   }
   const size_t nV = (size_t)q.ldv * nb, nT = (size_t)nb * nb, nW = (size_t)nb * (n > nb ? n : nb);
-  const size_t nS = (size_t)kQrB * kQrB, nP = (size_t)2 * q.grid * (kQrB + 1), nR = 2 * (kQrB + 1);
-  double *ws = nullptr;
-  cudaError_t e = cudaMallocAsync((void **)&ws, (nV + nT + nW + nS + nP + nR) * sizeof(double), st);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    *cerr = e;
-    return "qr workspace allocation";
-  }
+  const size_t nS = (size_t)kQrB * kQrB, nP = (size_t)2 * q.grid * (kQrB + 1);
   q.V = ws;
   q.T = q.V + nV;
   q.W = q.T + nT;
@@ -416,7 +427,6 @@ const char *qr_blocked(cublasHandle_t h, cudaStream_t st, double *A, int64_t m, 
                                     (int)q.ldv, q.W, (int)w, &one, C, (int)lda), "trailing C -= V W");
     }
   }
-  cudaFreeAsync(ws, st);
   *cerr = q.cerr;
   *berr = q.berr;
   return good ? nullptr : q.fail;
