@@ -33,7 +33,7 @@ namespace cg = cooperative_groups;
 namespace fls {
 
 constexpr int kQrB = 32;    // leaf width (columns per cooperative kernel)
-constexpr int kQrNT = 256;  // threads per CTA of the leaf kernel
+constexpr int kQrNT = 512;  // threads per CTA of the leaf kernel
 constexpr int kQrW = kQrNT / 32;
 constexpr size_t kQrSlab = 216 * 1024;  // shared-memory slab budget per CTA (one CTA per SM)
 constexpr int kQrMaxGrid = 256;         // leaf CTAs at most (one per SM)
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(kQrNT) qr_leaf_kernel(const QrLeafArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double slab[];  // [b][rc], column-major
   __shared__ double red[kQrW][kQrB + 1];
-  __shared__ double tot[kQrB + 1], rowv[kQrB + 1];
+  __shared__ double tot[kQrB + 1];
   __shared__ double s_tau, s_scale, s_beta;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t rc = a.rc;
@@ -109,43 +109,51 @@ __global__ void __launch_bounds__(kQrNT) qr_leaf_kernel(const QrLeafArgs a) {
     if (jj >= r_lo && jj < r_lo + nr && threadIdx.x < nc)
       rowb[threadIdx.x] = xs[threadIdx.x * rc + (jj - r_lo)];
     grid.sync();
-    // ---- totals (warp q sums slot q over the CTAs; same order in every CTA), then dlarfg;
-    // the diagonal row is fetched in the same round trip
-    if (threadIdx.x >= kQrNT - 32 && threadIdx.x - (kQrNT - 32) < nc)
-      rowv[threadIdx.x - (kQrNT - 32)] = rowb[threadIdx.x - (kQrNT - 32)];
-    for (int q = warp; q < nc; q += kQrW) {
-      double v[kQrMaxGrid / 32];  // all loads in flight before the adds (one L2 round trip)
+    // ---- every warp: total of slot 0 (same order in every CTA) -> dlarfg, redundantly, then
+    // the totals of its slots q: tot[q] = tau * v^T a_{jj+q} (v_jj = 1); one round trip to L2
+    {
+      double v0[kQrMaxGrid / 32];
 #pragma unroll
       for (int t = 0; t < kQrMaxGrid / 32; ++t) {
         const unsigned k = lane + 32 * t;
-        v[t] = k < gridDim.x ? part[(int64_t)k * (kQrB + 1) + q] : 0.0;
+        v0[t] = k < gridDim.x ? part[(int64_t)k * (kQrB + 1)] : 0.0;
       }
-      double s = 0.0;
+      const double alpha = rowb[0];
+      double s0 = 0.0;
 #pragma unroll
-      for (int t = 0; t < kQrMaxGrid / 32; ++t) s += v[t];
+      for (int t = 0; t < kQrMaxGrid / 32; ++t) s0 += v0[t];
 #pragma unroll
-      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) tot[q] = s;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const double alpha = rowv[0];
+      for (int o = 16; o; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o);
       double tau = 0.0, scale = 0.0, beta = alpha;
-      if (tot[0] > 0.0) {
-        beta = -copysign(hypot(alpha, sqrt(tot[0])), alpha);
+      if (s0 > 0.0) {
+        beta = -copysign(hypot(alpha, sqrt(s0)), alpha);
         tau = (beta - alpha) / beta;
         scale = 1.0 / (alpha - beta);
       }
-      s_tau = tau;
-      s_scale = scale;
-      s_beta = beta;
+      if (threadIdx.x == 0) {
+        s_tau = tau;
+        s_scale = scale;
+        s_beta = beta;
+        if (blockIdx.x == 0) a.tau[jj] = tau;
+      }
+      for (int q = warp > 0 ? warp : kQrW; q < nc; q += kQrW) {
+        double v[kQrMaxGrid / 32];
+#pragma unroll
+        for (int t = 0; t < kQrMaxGrid / 32; ++t) {
+          const unsigned k = lane + 32 * t;
+          v[t] = k < gridDim.x ? part[(int64_t)k * (kQrB + 1) + q] : 0.0;
+        }
+        const double rq = rowb[q];
+        double sq = 0.0;
+#pragma unroll
+        for (int t = 0; t < kQrMaxGrid / 32; ++t) sq += v[t];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) tot[q] = tau * fma(scale, sq, rq);
+      }
     }
     __syncthreads();
     const double tau = s_tau, scale = s_scale;
-    // tau * (v^T a_c), v_jj = 1
-    if (threadIdx.x >= 1 && threadIdx.x < nc)
-      tot[threadIdx.x] = tau * fma(scale, tot[threadIdx.x], rowv[threadIdx.x]);
-    __syncthreads();
     // ---- apply H_jj to my rows of the remaining columns (v overwrites x below the diagonal)
     double *xw = slab + jj * rc;
     const int rd = jj - r_lo >= 0 ? (int)(jj - r_lo) : -1;  // my row index of the diagonal
@@ -163,7 +171,6 @@ __global__ void __launch_bounds__(kQrNT) qr_leaf_kernel(const QrLeafArgs a) {
           if (q < nc) xw[q * rc + r] -= tot[q];
       }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.tau[jj] = tau;
     __syncthreads();
   }
   // write back R / v and the explicit V (zeros above, ones on the diagonal)
