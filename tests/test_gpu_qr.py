@@ -47,7 +47,8 @@ def _check(A, a, tau, tol=1e-13):
 
 
 @pytest.mark.parametrize("m,n", [(100, 37), (1000, 300), (3000, 700), (777, 513), (20000, 1100),
-                                 (64, 64), (33, 1), (1, 5), (300, 520), (40, 100)])
+                                 (64, 64), (33, 1), (1, 5), (300, 520), (40, 100),
+                                 (300000, 100)])   # tall: leaves narrower than 32 (slab budget)
 def test_geqrf_reconstructs_and_matches_cusolver_diag(ctx, m, n):
     g = torch.Generator(device="cuda").manual_seed(m * 1000 + n)
     A = torch.randn((m, n), dtype=torch.float64, device="cuda", generator=g)
