@@ -400,10 +400,19 @@ const char *qr_blocked(cublasHandle_t h, cudaStream_t st, double *A, int64_t m, 
     *cerr = cudaErrorInvalidValue;
     return "rows exceed the leaf slab capacity";
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(qr_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQrSlab);
-    attr = true;
+  {  // the shared-memory opt-in is a per-device function attribute
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr[dev]) {
+      cudaError_t e = cudaFuncSetAttribute(qr_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)kQrSlab);
+      if (e != cudaSuccess) {
+        *cerr = e;
+        return "qr_leaf_kernel shared-memory attribute";
+      }
+      if (dev >= 0 && dev < 64) attr[dev] = true;
+    }
   }
   const size_t nV = (size_t)q.ldv * nb, nT = (size_t)nb * nb, nW = (size_t)nb * (n > nb ? n : nb);
   const size_t nS = (size_t)kQrB * kQrB, nP = (size_t)2 * q.grid * (kQrB + 1);
