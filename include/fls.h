@@ -356,6 +356,17 @@ FLS_API fls_status fls_eval(fls_ctx *ctx, const double *W, const double *b, int3
                     int64_t n_features, int32_t normalize, const double *beta,
                     const fls_operator *op, const double *X, int64_t n_points, double *out);
 
+/* out_i = sum_j A_ij beta_j for the rows of one row block, with A_ij exactly as fls_assemble
+ * defines them (s, the block weight, its operator including coefficient fields, Eq. 2 / Eq. 3,
+ * P:L95-121) -- i.e. A_block beta without materialising A (PDE residuals of variable-
+ * coefficient operators such as C5's, Newton residuals).  block->values is ignored.
+ *   block: host descriptor of device arrays (X n_points x dim, coef_fields n_points x
+ *   n_fields).  out: device, n_points.  Errors as fls_eval (FLS_EINVAL also for a field id
+ *   >= n_fields or fields used with coef_fields NULL).  Asynchronous. */
+FLS_API fls_status fls_eval_block(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
+                                  int64_t n_features, int32_t normalize, const double *beta,
+                                  const fls_block *block, double *out);
+
 #ifdef __cplusplus
 }
 #endif

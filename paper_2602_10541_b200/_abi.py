@@ -107,6 +107,8 @@ _SIGS = {
                            C.c_int64]),
     "fls_frob2": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
                             C.POINTER(C.c_double)]),
+    "fls_eval_block": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int32,
+                                 C.c_void_p, C.POINTER(fls_block), C.c_void_p]),
     "fls_eval": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int32,
                            C.c_void_p, C.POINTER(fls_operator), C.c_void_p, C.c_int64, C.c_void_p]),
 }

@@ -1190,26 +1190,31 @@ fls_status fls_frob2(fls_ctx *ctx, const double *A, int64_t n_rows, int64_t lda,
 }
 
 // ---------------------------------------------------------------------------------------------
-fls_status fls_eval(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
-                    int64_t n_features, int32_t normalize, const double *beta,
-                    const fls_operator *op, const double *X, int64_t n_points, double *out) {
+static fls_status eval_common(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
+                              int64_t n_features, int32_t normalize, const double *beta,
+                              const fls_operator *op, const double *X, int64_t n_points,
+                              const double *fields, int32_t n_fields, double weight, double *out,
+                              bool allow_fields) {
   if (fls_status s = check_ctx(ctx)) return s;
   if (dim < 1 || dim > FLS_MAX_DIM) return fail(FLS_EINVAL, "dim %d not in 1..%d", dim, FLS_MAX_DIM);
   if (n_features < 1) return fail(FLS_EINVAL, "n_features < 1");
   if (!W || !b || !beta) return fail(FLS_EINVAL, "W, b or beta is NULL");
   if (n_points < 0) return fail(FLS_EINVAL, "n_points < 0");
   if (n_points > 0 && (!X || !out)) return fail(FLS_EINVAL, "X or out is NULL");
+  if (!std::isfinite(weight)) return fail(FLS_EINVAL, "weight not finite");
   fls_term ident;
   std::memset(&ident, 0, sizeof ident);
   ident.coef = 1.0;
   ident.field = -1;
   fls_operator idop{dim, 1, &ident};
   OpPlan pl;
-  if (fls_status s = plan_operator(op ? op : &idop, dim, 0, false, pl, "eval operator")) return s;
+  if (fls_status s = plan_operator(op ? op : &idop, dim, n_fields, allow_fields, pl, "eval operator"))
+    return s;
+  if (pl.G > 0 && n_points > 0 && !fields)
+    return fail(FLS_EINVAL, "eval operator uses coefficient fields but coef_fields is NULL");
   if (n_points == 0) return FLS_OK;
   DeviceGuard g(ctx->device);
-  const int S = pf_stride(dim, 0, KM_SINCOS);
-  // eval records live after the largest assemble layout we may have (separate region)
+  const int S = pf_stride(dim, pl.G, KM_SINCOS);
   const int Smax = pf_stride(FLS_MAX_DIM, FLS_MAX_FIELDS, KM_SINCOS);
   if (fls_status s = ensure_ws(ctx, (size_t)n_features * Smax * sizeof(double))) return s;
   PrefArgs pa;
@@ -1219,16 +1224,17 @@ fls_status fls_eval(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
   pa.F = n_features;
   pa.D = dim;
   pa.n_terms = pl.n_terms;
-  pa.G = 0;
+  pa.G = pl.G;
   pa.pmode = PM_SINCOS;
   pa.S = S;
-  pa.scale = normalize ? 1.0 / std::sqrt((double)n_features) : 1.0;
+  pa.scale = (normalize ? 1.0 / std::sqrt((double)n_features) : 1.0) * weight;
   pa.pf = ctx->ws;
   pa.err = ctx->d_err;
   std::memcpy(pa.terms, pl.terms, sizeof pl.terms);
   cudaError_t e = launch_prefactor(pa, ctx->stream);
   if (e != cudaSuccess) return cuda_fail(e, "prefactor_kernel");
   EvalArgs ea;
+  std::memset(&ea, 0, sizeof ea);
   ea.pf = pa.pf;
   ea.S = S;
   ea.F = n_features;
@@ -1237,9 +1243,30 @@ fls_status fls_eval(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
   ea.n = n_points;
   ea.out = out;
   ea.err = ctx->d_err;
+  ea.fields = fields;
+  ea.nf = n_fields;
+  ea.G = pl.G;
+  for (int q = 0; q < pl.G; ++q) ea.gfield[q] = pl.gfield[q];
   e = launch_eval(dim, ea, ctx->stream);
   if (e != cudaSuccess) return cuda_fail(e, "eval_kernel");
   return FLS_OK;
+}
+
+fls_status fls_eval(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
+                    int64_t n_features, int32_t normalize, const double *beta,
+                    const fls_operator *op, const double *X, int64_t n_points, double *out) {
+  return eval_common(ctx, W, b, dim, n_features, normalize, beta, op, X, n_points, nullptr, 0, 1.0,
+                     out, false);
+}
+
+fls_status fls_eval_block(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
+                          int64_t n_features, int32_t normalize, const double *beta,
+                          const fls_block *block, double *out) {
+  if (!block) return fail(FLS_EINVAL, "block is NULL");
+  if (!block->op) return fail(FLS_EINVAL, "block operator is NULL");
+  if (block->n_fields < 0 || block->n_fields > 64) return fail(FLS_EINVAL, "n_fields out of range");
+  return eval_common(ctx, W, b, dim, n_features, normalize, beta, block->op, block->X,
+                     block->n_points, block->coef_fields, block->n_fields, block->weight, out, true);
 }
 
 }  // extern "C"

@@ -82,7 +82,7 @@ struct AsmArgs {
 };
 
 struct EvalArgs {
-  const double *pf;  // PM_SINCOS layout, G = 0: [W'_0..W'_{D-1}, b', Ps, Pc] (+pad)
+  const double *pf;  // PM_SINCOS layout: [W'_0..W'_{D-1}, b', Ps_0, Pc_0, .., Ps_G, Pc_G] (+pad)
   int32_t S;
   int64_t F;
   const double *beta;
@@ -90,6 +90,10 @@ struct EvalArgs {
   int64_t n;
   double *out;
   unsigned *err;
+  const double *fields;           // n x nf coefficient fields (G > 0), row-major
+  int32_t nf;
+  int32_t G;                      // field groups (0: constant coefficients)
+  int32_t gfield[FLS_MAX_FIELDS]; // field id of group g+1
 };
 
 // layout helper shared by host and kernels

@@ -253,7 +253,8 @@ cudaError_t launch_prefactor_batch(const PrefBatch &b, int64_t F, cudaStream_t s
 
 // ------------------------------------------------------------------------------------------
 // a10 eval (Alg. 1 line 6):  out_i = sum_j beta_j (Ps_j sin z_ij + Pc_j cos z_ij),
-// with Ps = s, Pc = 0 for u_N itself (identity operator) -- A is never materialised.
+// with Ps = s, Pc = 0 for u_N itself (identity operator) -- A is never materialised.  With
+// coefficient fields (fls_eval_block): Ps = Ps_0 + sum_g c_g(x_i) Ps_g, likewise Pc.
 // One warp per 4 rows; lanes stride over features; fixed-order warp reduction.
 // ------------------------------------------------------------------------------------------
 template <int D>
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(256) eval_kernel(const EvalArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r0 = ((int64_t)blockIdx.x * 8 + warp) * 4;
   double x[4][D];
+  double cf[4][FLS_MAX_FIELDS];  // per-row coefficient of group g+1
   bool bad = false;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -270,6 +272,11 @@ __global__ void __launch_bounds__(256) eval_kernel(const EvalArgs a) {
       x[q][k] = r < a.n ? a.X[r * D + k] : 0.0;
       bad |= !finite(x[q][k]);
     }
+#pragma unroll
+    for (int g = 0; g < FLS_MAX_FIELDS; ++g) {
+      cf[q][g] = (g < a.G && r < a.n) ? a.fields[r * a.nf + a.gfield[g]] : 0.0;
+      bad |= !finite(cf[q][g]);
+    }
   }
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   for (int64_t j = lane; j < a.F; j += 32) {
@@ -277,7 +284,13 @@ __global__ void __launch_bounds__(256) eval_kernel(const EvalArgs a) {
     double w[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) w[k] = p[k];
-    const double bp = p[D], ps = p[D + 1], pc = p[D + 2];
+    const double bp = p[D], ps0 = p[D + 1], pc0 = p[D + 2];
+    double psg[FLS_MAX_FIELDS], pcg[FLS_MAX_FIELDS];
+#pragma unroll
+    for (int g = 0; g < FLS_MAX_FIELDS; ++g) {
+      psg[g] = g < a.G ? p[D + 3 + 2 * g] : 0.0;
+      pcg[g] = g < a.G ? p[D + 4 + 2 * g] : 0.0;
+    }
     const double bt = a.beta[j];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -288,6 +301,14 @@ __global__ void __launch_bounds__(256) eval_kernel(const EvalArgs a) {
       const double f = halfturn(h, sgn);
       const double u = f * f;
       const double s = sinpi_core(f, u), c = cospi_core(u);
+      double ps = ps0, pc = pc0;
+#pragma unroll
+      for (int g = 0; g < FLS_MAX_FIELDS; ++g) {
+        if (g < a.G) {
+          ps = fma(cf[q][g], psg[g], ps);
+          pc = fma(cf[q][g], pcg[g], pc);
+        }
+      }
       acc[q] = fma(bt, flipsign(fma(ps, s, pc * c), sgn), acc[q]);
     }
   }

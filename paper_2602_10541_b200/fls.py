@@ -25,7 +25,7 @@ from ._abi import FLS_COL_MAJOR, FLS_ROW_MAJOR, FlsError, check
 Term = Tuple[Sequence[int], float, int]   # (alpha, coef, field)
 
 __all__ = ["Context", "Block", "fls_features", "fls_assemble", "fls_features_assemble", "fls_solve", "fls_qr_r",
-           "fls_frob2", "fls_geqrf", "fls_eval", "fls_sync", "fls_ctx_timing", "fls_ctx_timing_read",
+           "fls_frob2", "fls_geqrf", "fls_eval", "fls_eval_block", "fls_sync", "fls_ctx_timing", "fls_ctx_timing_read",
            "fls_assemble_host", "HostBlockSet", "BlockSet", "fls_features_blocks", "QRFactor",
            "make_nonlinearity", "fls_nl_residual", "fls_axpy", "fls_features_transform",
            "fls_bandwidth_grad", "fls_sample_box", "fls_sample_faces", "FlsError", "FLS_COL_MAJOR", "FLS_ROW_MAJOR",
@@ -487,6 +487,21 @@ def fls_frob2(ctx: Context, A: torch.Tensor, n_rows: int, lda: int, n_cols: int)
     check(_abi.load().fls_frob2(ctx.handle, _ptr(A), int(n_rows), int(lda), int(n_cols),
                                 C.byref(out)))
     return out.value
+
+
+def fls_eval_block(ctx: Context, W: torch.Tensor, b: torch.Tensor, beta: torch.Tensor, block: Block,
+                   normalize: bool = True, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """A_block @ beta for one row block (its operator, coefficient fields and weight), without
+    materialising A"""
+    for t, nm in ((W, "W"), (b, "b"), (beta, "beta")):
+        _dev_f64(t, nm)
+    F, dim = int(W.shape[0]), int(W.shape[1])
+    bs = BlockSet([block], dim)
+    if out is None:
+        out = torch.empty((block.n,), dtype=torch.float64, device=W.device)
+    check(_abi.load().fls_eval_block(ctx.handle, _ptr(W), _ptr(b), dim, F, int(bool(normalize)),
+                                     _ptr(beta), bs.arr, _ptr(out)))
+    return out
 
 
 def fls_eval(ctx: Context, W: torch.Tensor, b: torch.Tensor, beta: torch.Tensor, X: torch.Tensor,

@@ -420,6 +420,49 @@ def test_eval_with_operator_matches_assembled_rows(ctx):
     assert np.abs(Lu - ref).max() <= 1e-12 * (S @ np.abs(beta.cpu().numpy())).max()
 
 
+@pytest.mark.parametrize("name", ["c5_biharm3d", "c4_heat2d", "c2_poisson2d"])
+def test_eval_block_matches_oracle_rows(ctx, name):
+    """fls_eval_block = A_block beta with the block's weight and coefficient fields (C5: the
+    16 (1 + x1) u term), A never materialised; every block of the problem"""
+    p = wl.make_problem(name, "mini")
+    W, b, Wd, bd = _parity_feats(p)
+    F = p.n_features
+    beta_h = np.random.default_rng(1).normal(size=F)
+    beta = torch.from_numpy(beta_h).cuda()
+    for blk, dblk in zip(p.blocks, dev_blocks(p)):
+        got = fls.fls_eval_block(ctx, Wd, bd, beta, dblk).cpu().numpy()
+        Ao, _, S = oracle.assemble(W, b, [blk])
+        ref = Ao @ beta_h
+        assert np.abs(got - ref).max() <= 1e-12 * (S @ np.abs(beta_h)).max(), blk.name
+
+
+def test_eval_block_two_fields_mixed_parity(ctx):
+    """mixed-parity operator with two coefficient fields (the sin+cos eval path)"""
+    rng = np.random.default_rng(5)
+    d, F, n = 3, 211, 777
+    W = rng.normal(0, 2.0, size=(F, d))
+    b = rng.uniform(0, 2 * np.pi, size=F)
+    X = rng.uniform(0, 1, size=(n, d))
+    fields = rng.normal(size=(n, 3))
+    terms = [((2, 0, 0), 1.0, -1), ((0, 1, 0), -0.5, 2), ((0, 0, 0), 3.0, 0), ((1, 1, 1), 0.25, 2)]
+
+    class B:
+        pass
+    h = B()
+    h.X, h.terms, h.weight, h.values, h.fields = X, terms, 7.0, None, fields
+    Ao, _, S = oracle.assemble(W, b, [h])
+    beta_h = rng.normal(size=F)
+    blk = fls.Block(torch.from_numpy(X).cuda(), terms, 7.0, None, torch.from_numpy(fields).cuda())
+    got = fls.fls_eval_block(ctx, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(),
+                             torch.from_numpy(beta_h).cuda(), blk).cpu().numpy()
+    assert np.abs(got - Ao @ beta_h).max() <= 1e-12 * (S @ np.abs(beta_h)).max()
+    bad = fls.Block(torch.from_numpy(X).cuda(), [((0, 0, 0), 1.0, 5)], 1.0, None,
+                    torch.from_numpy(fields).cuda())
+    with pytest.raises(fls.FlsError):
+        fls.fls_eval_block(ctx, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(),
+                           torch.from_numpy(beta_h).cuda(), bad)
+
+
 # ------------------------------------------------------------------------------------- host path
 @pytest.mark.parametrize("chunk", [0, 1000, 4096])
 def test_assemble_host_matches_device(ctx, chunk):
