@@ -17,7 +17,6 @@
 //     instead of several kernel launches and no global-memory pass.
 // Householder vector per column (LAPACK dlarfg): beta = -sign(alpha) ||[alpha; x]||,
 // tau = (beta - alpha) / beta, v = x / (alpha - beta); ||x|| = 0 gives tau = 0 (H = I).
-#include <cooperative_groups.h>
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -28,7 +27,6 @@
 
 #include "fls_internal.h"
 
-namespace cg = cooperative_groups;
 
 namespace fls {
 
@@ -48,15 +46,33 @@ struct QrLeafArgs {
   double *V;     // explicit V (zeros above, ones on the diagonal), same row origin as A
   int64_t ldv;
   double *tau;
-  double *part;  // [2][gridDim.x][kQrB + 1] per-CTA partial sums
+  double *part;  // [2][kQrB + 1][gridDim.x] per-CTA partial sums (slot-major)
   double *rowb;  // [2][kQrB + 1] the diagonal row a_jj.. at the start of column jj
+  unsigned *bar; // grid-barrier arrival counter (zeroed before the launch)
 };
+
+// grid-wide barrier of a cooperative launch (all CTAs co-resident): monotonically increasing
+// arrival counter, release-add by one thread per CTA, acquire-poll until every CTA of round
+// `round` has arrived
+__device__ __forceinline__ void qr_grid_barrier(unsigned *bar, unsigned round) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned target = (round + 1) * gridDim.x;
+    // release: the CTA's writes before the __syncthreads above are visible to any CTA that
+    // acquires the counter value (PTX memory model: bar.sync + release is cumulative)
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
 
 // One leaf (b <= 32 columns, m rows) of the recursive QR.  CTA k owns rows [k rc, (k+1) rc)
 // and keeps them (b columns) in shared memory for the whole leaf: the global memory traffic is
 // one read and one write of the leaf plus the per-column partial sums.
 __global__ void __launch_bounds__(kQrNT) qr_leaf_kernel(const QrLeafArgs a) {
-  cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double slab[];  // [b][rc], column-major
   __shared__ double red[kQrW][kQrB + 1];
   __shared__ double tot[kQrB + 1];
@@ -103,12 +119,12 @@ __global__ void __launch_bounds__(kQrNT) qr_leaf_kernel(const QrLeafArgs a) {
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < kQrW; ++w) s += red[w][threadIdx.x];
-      part[(int64_t)blockIdx.x * (kQrB + 1) + threadIdx.x] = s;
+      part[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = s;  // slot-major: coalesced reads
     }
     // the owner of row jj publishes it before the barrier
     if (jj >= r_lo && jj < r_lo + nr && threadIdx.x < nc)
       rowb[threadIdx.x] = xs[threadIdx.x * rc + (jj - r_lo)];
-    grid.sync();
+    qr_grid_barrier(a.bar, (unsigned)jj);
     // ---- every warp: total of slot 0 (same order in every CTA) -> dlarfg, redundantly, then
     // the totals of its slots q: tot[q] = tau * v^T a_{jj+q} (v_jj = 1); one round trip to L2
     {
@@ -116,7 +132,7 @@ __global__ void __launch_bounds__(kQrNT) qr_leaf_kernel(const QrLeafArgs a) {
 #pragma unroll
       for (int t = 0; t < kQrMaxGrid / 32; ++t) {
         const unsigned k = lane + 32 * t;
-        v0[t] = k < gridDim.x ? part[(int64_t)k * (kQrB + 1)] : 0.0;
+        v0[t] = k < gridDim.x ? part[k] : 0.0;   // the barrier's acquire invalidated L1
       }
       const double alpha = rowb[0];
       double s0 = 0.0;
@@ -141,7 +157,7 @@ __global__ void __launch_bounds__(kQrNT) qr_leaf_kernel(const QrLeafArgs a) {
 #pragma unroll
         for (int t = 0; t < kQrMaxGrid / 32; ++t) {
           const unsigned k = lane + 32 * t;
-          v[t] = k < gridDim.x ? part[(int64_t)k * (kQrB + 1) + q] : 0.0;
+          v[t] = k < gridDim.x ? part[(int64_t)q * gridDim.x + k] : 0.0;
         }
         const double rq = rowb[q];
         double sq = 0.0;
@@ -225,6 +241,7 @@ struct QrCtx {
   double *W;     // nb x n scratch
   double *S;     // kQrB x kQrB
   double *part, *rowb;
+  unsigned *bar;   // leaf grid-barrier counter
   int grid;        // CTAs of a leaf launch (one per SM)
   int bleaf;       // leaf width for the current panel (slab fits shared memory)
   const char *fail = nullptr;
@@ -267,6 +284,8 @@ bool rec_panel(QrCtx &q, double *P, int64_t mp, int64_t c, int64_t w, double *ta
     a.tau = tau + c;
     a.part = q.part;
     a.rowb = q.rowb;
+    a.bar = q.bar;
+    if (!ok_cuda(q, cudaMemsetAsync(q.bar, 0, sizeof(unsigned), q.st), "barrier reset")) return false;
     // fewest CTAs that hold the leaf in shared memory, but about qr_leaf_rows() rows each:
     // fewer CTAs make the per-column grid barrier and partial-sum reduction cheaper
     const int64_t slab_rows = (int64_t)kQrSlab / (w * (int64_t)sizeof(double));
@@ -375,7 +394,7 @@ size_t qr_blocked_ws(int64_t m, int64_t n) {
   const int64_t nb = qr_panel_width();
   const int64_t ldv = (m + 3) / 4 * 4;
   return (size_t)ldv * nb + (size_t)nb * nb + (size_t)nb * (n > nb ? n : nb) + (size_t)kQrB * kQrB +
-         (size_t)2 * qr_grid() * (kQrB + 1) + 2 * (kQrB + 1);
+         (size_t)2 * qr_grid() * (kQrB + 1) + 2 * (kQrB + 1) + 1;  // + barrier counter
 }
 
 // A (m x n, lda) -> R / V / tau in place, ws = qr_blocked_ws(m, n) doubles (caller-owned, so
@@ -422,6 +441,7 @@ const char *qr_blocked(cublasHandle_t h, cudaStream_t st, double *A, int64_t m, 
   q.S = q.W + nW;
   q.part = q.S + nS;
   q.rowb = q.part + nP;
+  q.bar = reinterpret_cast<unsigned *>(q.rowb + 2 * (kQrB + 1));
   const double one = 1.0, zero = 0.0, mone = -1.0;
   bool good = ok_blas(q, cublasSetStream(h, st), "cublasSetStream");
   for (int64_t j = 0; good && j < k; j += nb) {
