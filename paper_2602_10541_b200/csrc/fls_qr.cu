@@ -31,7 +31,7 @@
 namespace fls {
 
 constexpr int kQrB = 32;    // leaf width (columns per cooperative kernel)
-constexpr int kQrNT = 512;  // threads per CTA of the leaf kernel
+constexpr int kQrNT = 256;  // threads per CTA of the leaf kernel
 constexpr int kQrW = kQrNT / 32;
 constexpr size_t kQrSlab = 216 * 1024;  // shared-memory slab budget per CTA (one CTA per SM)
 constexpr int kQrMaxGrid = 256;         // leaf CTAs at most (one per SM)
@@ -69,9 +69,39 @@ __device__ __forceinline__ void qr_grid_barrier(unsigned *bar, unsigned round) {
   __syncthreads();
 }
 
+// block-reduce the per-thread partial sums of column jj (slot 0: ||x||^2, slot q: x^T a_{jj+q})
+// and publish them (slot-major) plus, from the owner CTA, the diagonal row a_{jj, jj..}
+__device__ __forceinline__ void qr_publish(double (&acc)[kQrB], double (*red)[kQrB + 1],
+                                           const double *slab, int64_t rc, int64_t r_lo, int nr,
+                                           int jj, int nc, double *part, double *rowb) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // 32 warp sums in 31 shuffles (recursive halving): afterwards lane l holds sum of acc[l]
+#pragma unroll
+  for (int sh = 16; sh >= 1; sh >>= 1) {
+    const bool up = lane & sh;
+#pragma unroll
+    for (int t = 0; t < sh; ++t) {
+      const double send = up ? acc[t] : acc[t + sh];
+      const double keep = up ? acc[t + sh] : acc[t];
+      acc[t] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
+    }
+  }
+  red[warp][lane] = acc[0];
+  __syncthreads();  // also orders the slab updates before the row publication below
+  if (threadIdx.x < nc) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kQrW; ++w) s += red[w][threadIdx.x];
+    part[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = s;  // slot-major: coalesced reads
+  }
+  if (jj >= r_lo && jj < r_lo + nr && threadIdx.x < nc)
+    rowb[threadIdx.x] = slab[(jj + threadIdx.x) * rc + (jj - r_lo)];
+}
+
 // One leaf (b <= 32 columns, m rows) of the recursive QR.  CTA k owns rows [k rc, (k+1) rc)
 // and keeps them (b columns) in shared memory for the whole leaf: the global memory traffic is
-// one read and one write of the leaf plus the per-column partial sums.
+// one read and one write of the leaf plus the per-column partial sums.  The update of column
+// jj's reflector and the partial sums of column jj+1 share one pass over the slab.
 __global__ void __launch_bounds__(kQrNT) qr_leaf_kernel(const QrLeafArgs a) {
   extern __shared__ __align__(16) double slab[];  // [b][rc], column-major
   __shared__ double red[kQrW][kQrB + 1];
@@ -85,45 +115,24 @@ __global__ void __launch_bounds__(kQrNT) qr_leaf_kernel(const QrLeafArgs a) {
   for (int q = 0; q < b; ++q)
     for (int r = threadIdx.x; r < nr; r += kQrNT) slab[q * rc + r] = a.A[(int64_t)q * a.lda + r_lo + r];
   __syncthreads();
-  for (int jj = 0; jj < b; ++jj) {
-    const int nc = b - jj;  // slot 0: ||x||^2, slot q: x^T a_{jj+q}
-    double *part = a.part + (size_t)(jj & 1) * gridDim.x * (kQrB + 1);
-    double *rowb = a.rowb + (jj & 1) * (kQrB + 1);
-    const double *xs = slab + jj * rc;
-    // ---- partial sums over my rows below the diagonal
-    double acc[kQrB];
+  double acc[kQrB];
+  {  // partial sums of column 0 over my rows below the diagonal
 #pragma unroll
     for (int q = 0; q < kQrB; ++q) acc[q] = 0.0;
-    const int r0 = jj + 1 - r_lo > 0 ? (int)(jj + 1 - r_lo) : 0;
+    const int r0 = 1 - r_lo > 0 ? (int)(1 - r_lo) : 0;
     for (int r = r0 + threadIdx.x; r < nr; r += kQrNT) {
-      const double x = xs[r];
+      const double x = slab[r];
       acc[0] = fma(x, x, acc[0]);
 #pragma unroll
       for (int q = 1; q < kQrB; ++q)
-        if (q < nc) acc[q] = fma(x, xs[q * rc + r], acc[q]);
+        if (q < b) acc[q] = fma(x, slab[q * rc + r], acc[q]);
     }
-    // 32 warp sums in 31 shuffles (recursive halving): afterwards lane l holds sum of acc[l]
-#pragma unroll
-    for (int sh = 16; sh >= 1; sh >>= 1) {
-      const bool up = lane & sh;
-#pragma unroll
-      for (int t = 0; t < sh; ++t) {
-        const double send = up ? acc[t] : acc[t + sh];
-        const double keep = up ? acc[t + sh] : acc[t];
-        acc[t] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
-      }
-    }
-    red[warp][lane] = acc[0];
-    __syncthreads();
-    if (threadIdx.x < nc) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < kQrW; ++w) s += red[w][threadIdx.x];
-      part[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = s;  // slot-major: coalesced reads
-    }
-    // the owner of row jj publishes it before the barrier
-    if (jj >= r_lo && jj < r_lo + nr && threadIdx.x < nc)
-      rowb[threadIdx.x] = xs[threadIdx.x * rc + (jj - r_lo)];
+    qr_publish(acc, red, slab, rc, r_lo, nr, 0, b, a.part, a.rowb);
+  }
+  for (int jj = 0; jj < b; ++jj) {
+    const int nc = b - jj;
+    const double *part = a.part + (size_t)(jj & 1) * gridDim.x * (kQrB + 1);
+    const double *rowb = a.rowb + (jj & 1) * (kQrB + 1);
     qr_grid_barrier(a.bar, (unsigned)jj);
     // ---- every warp: total of slot 0 (same order in every CTA) -> dlarfg, redundantly, then
     // the totals of its slots q: tot[q] = tau * v^T a_{jj+q} (v_jj = 1); one round trip to L2
@@ -171,15 +180,32 @@ __global__ void __launch_bounds__(kQrNT) qr_leaf_kernel(const QrLeafArgs a) {
     __syncthreads();
     const double tau = s_tau, scale = s_scale;
     // ---- apply H_jj to my rows of the remaining columns (v overwrites x below the diagonal)
+    // and accumulate column jj+1's partial sums over rows below ITS diagonal
+#pragma unroll
+    for (int q = 0; q < kQrB; ++q) acc[q] = 0.0;
     double *xw = slab + jj * rc;
     const int rd = jj - r_lo >= 0 ? (int)(jj - r_lo) : -1;  // my row index of the diagonal
     for (int r = (rd > 0 ? rd : 0) + threadIdx.x; r < nr; r += kQrNT) {
       if (r > rd) {
         const double v = tau != 0.0 ? xw[r] * scale : xw[r];
         xw[r] = v;
+        const bool below = r_lo + r > jj + 1;  // contributes to column jj+1's sums
+        double xn = 0.0;
 #pragma unroll
-        for (int q = 1; q < kQrB; ++q)
-          if (q < nc) xw[q * rc + r] -= v * tot[q];
+        for (int q = 1; q < kQrB; ++q) {
+          if (q < nc) {
+            const double nv = xw[q * rc + r] - v * tot[q];
+            xw[q * rc + r] = nv;
+            if (below) {
+              if (q == 1) {
+                xn = nv;
+                acc[0] = fma(nv, nv, acc[0]);
+              } else {
+                acc[q - 1] = fma(xn, nv, acc[q - 1]);
+              }
+            }
+          }
+        }
       } else {  // r == rd: the diagonal row
         xw[r] = s_beta;
 #pragma unroll
@@ -187,8 +213,12 @@ __global__ void __launch_bounds__(kQrNT) qr_leaf_kernel(const QrLeafArgs a) {
           if (q < nc) xw[q * rc + r] -= tot[q];
       }
     }
-    __syncthreads();
+    if (jj + 1 < b)
+      qr_publish(acc, red, slab, rc, r_lo, nr, jj + 1, nc - 1,
+                 a.part + (size_t)((jj + 1) & 1) * gridDim.x * (kQrB + 1),
+                 a.rowb + ((jj + 1) & 1) * (kQrB + 1));
   }
+  __syncthreads();
   // write back R / v and the explicit V (zeros above, ones on the diagonal)
   for (int q = 0; q < b; ++q)
     for (int r = threadIdx.x; r < nr; r += kQrNT) {
