@@ -250,12 +250,13 @@ FLS_API fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t l
 /* Cholesky factor).  The outer loss is  Lout = ||A(L) beta* - b||^2, beta* the     */
 /* least-squares optimum; by optimality of beta* its gradient needs no differentiation of   */
 /* the solve:  dLout/dL_kl = 2 sum_i r_i sum_j beta_j dA_ij/dW_jk W^_jl,  r = A beta* - b,    */
-/* with dA_ij/dW_jk = w s sum_t c_t [alpha_tk prod W^(alpha_t - e_k) Phi_p(z_ij)              */
-/*                                   + prod W^alpha_t x_ik Phi_{p+1}(z_ij)]  (Eq. 2 + chain). */
+/* with dA_ij/dW_jk = w s sum_t c_t(x_i) [alpha_tk prod W^(alpha_t - e_k) Phi_p(z_ij)         */
+/*                                   + prod W^alpha_t x_ik Phi_{p+1}(z_ij)]  (Eq. 2 + chain), */
+/* c_t(x_i) = coef_t, times the block's coefficient field for field terms.                   */
 /* fls_features_transform: W (F x dim) = rows L W^_j (L host, dim x dim row-major).          */
-/* fls_bandwidth_grad: blocks as for fls_assemble but values = the block's rows of r (device) */
-/*   (constant-coefficient operators only: FLS_EUNSUPPORTED with coefficient fields);       */
-/*   G (host, dim x dim row-major) receives dLout/dL; deterministic; blocking.               */
+/* fls_bandwidth_grad: blocks as for fls_assemble (coefficient fields allowed) but values =  */
+/*   the block's rows of r (device); G (host, dim x dim row-major) receives dLout/dL;        */
+/*   deterministic; blocking.                                                                */
 /* ---------------------------------------------------------------------------------------- */
 FLS_API fls_status fls_features_transform(fls_ctx *ctx, int32_t dim, int64_t n_features,
                                           const double *L, const double *W_hat, double *W);

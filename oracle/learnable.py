@@ -2,7 +2,8 @@
 
 Outer loss Lout(L) = ||A(L) beta* - b||^2 with W = L W^, A by the oracle's
 term-by-term assembly, beta* by its Householder lstsq.  The gradient is written out from the
-definition: for each term c prod W^e Phi_p(W.x + b) (e, p from the symbolic differentiator),
+definition: for each term c(x) prod W^e Phi_p(W.x + b) (e, p from the symbolic differentiator;
+c(x) = coef, or coef times a coefficient field),
     d/dW_k = c e_k prod W^(e - e_k) Phi_p(z) + c prod W^e x_k Phi_{p+1}(z),
     dLout/dL_kl = 2 sum_ij r_i beta_j dA_ij/dW_jk W^_jl      (beta* optimal: envelope)
 evaluated with numpy sin / cos on the full (rows x features) grid -- small inputs only.
@@ -44,8 +45,10 @@ def outer_grad(Lmat, W_hat, b, blocks, sqrt_mu=0.0, normalize=True):
         ri = r[off:off + n]
         off += n
         Z = X @ W.T + b                              # (n, F)
+        fields = getattr(blk, "fields", None)
         for alpha, coef, field in blk.terms:
-            assert field < 0, "constant coefficients only"
+            # per-row coefficient c_t(x_i): coef, times the coefficient field for field terms
+            rc = ri * (fields[:, field] if field >= 0 else 1.0)
             e, p = diff(alpha)
             mono = np.ones(F)
             for k in range(d):
@@ -58,8 +61,8 @@ def outer_grad(Lmat, W_hat, b, blocks, sqrt_mu=0.0, normalize=True):
                     m_k = np.ones(F)
                     for l in range(d):
                         m_k = m_k * W[:, l] ** (e[l] - (1 if l == k else 0))
-                    V[:, k] += blk.weight * s * coef * e[k] * m_k * (ri @ phase_p)
+                    V[:, k] += blk.weight * s * coef * e[k] * m_k * (rc @ phase_p)
                 # c prod W^e x_k Phi_{p+1}(z)
-                V[:, k] += blk.weight * s * coef * mono * ((ri * X[:, k]) @ phase_p1)
+                V[:, k] += blk.weight * s * coef * mono * ((rc * X[:, k]) @ phase_p1)
     G = 2.0 * np.einsum("jk,j,jl->kl", V, beta, W_hat)
     return loss, G, beta

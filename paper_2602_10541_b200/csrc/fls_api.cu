@@ -1042,8 +1042,6 @@ fls_status fls_bandwidth_grad(fls_ctx *ctx, const double *W, const double *W_hat
                                        n_features, FLS_ROW_MAJOR, ap))
     return s;
   for (int q = 0; q < n_blocks; ++q) {
-    if (blocks[q].n_fields > 0 || ap.plans[q].G > 0)
-      return fail(FLS_EUNSUPPORTED, "block %d: coefficient fields in the bandwidth gradient", q);
     if (blocks[q].n_points > 0 && !blocks[q].values)
       return fail(FLS_EINVAL, "block %d: values (the residual rows) is NULL", q);
   }
@@ -1078,7 +1076,8 @@ fls_status fls_bandwidth_grad(fls_ctx *ctx, const double *W, const double *W_hat
     pa.F = F;
     pa.D = dim;
     pa.n_terms = ap.plans[q].n_terms;
-    pa.S = kGradRec;
+    pa.G = ap.plans[q].G;
+    pa.S = grad_stride(dim, pa.G);
     pa.scale = s_norm * B.weight;
     pa.pf = ctx->ws + (size_t)q * F * kGradRec;
     pa.err = ctx->d_err;
@@ -1088,7 +1087,10 @@ fls_status fls_bandwidth_grad(fls_ctx *ctx, const double *W, const double *W_hat
     GradArgs ga;
     std::memset(&ga, 0, sizeof ga);
     ga.pf = pa.pf;
-    ga.S = kGradRec;
+    ga.S = pa.S;
+    ga.fields = B.coef_fields;
+    ga.nf = B.n_fields;
+    for (int g2 = 0; g2 < pa.G; ++g2) ga.gfield[g2] = ap.plans[q].gfield[g2];
     ga.F = F;
     ga.X = B.X;
     ga.r = B.values;
@@ -1098,7 +1100,7 @@ fls_status fls_bandwidth_grad(fls_ctx *ctx, const double *W, const double *W_hat
     ga.slot0 = slot0;
     ga.partials = partials;
     ga.err = ctx->d_err;
-    e = launch_grad_reduce(dim, ga, slots_q[q], ctx->stream);
+    e = launch_grad_reduce(dim, pa.G, ga, slots_q[q], ctx->stream);
     slot0 += slots_q[q];
   }
   if (e == cudaSuccess) {

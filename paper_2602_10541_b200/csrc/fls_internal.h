@@ -163,13 +163,19 @@ cudaError_t launch_nl_residual(const NlArgs &a, int nblk, double *stats, cudaStr
 struct TransformArgs {
   double L[FLS_MAX_DIM * FLS_MAX_DIM];
 };
-constexpr int kGradRec = 3 * FLS_MAX_DIM + 4;  // record stride upper bound (doubles)
+// gradient record per feature: [W/pi (D), b/pi, then per field group g = 0..G: Ps (D), Pc (D),
+// Qs, Qc]; stride bound for D = FLS_MAX_DIM, G = FLS_MAX_FIELDS
+__host__ __device__ constexpr int grad_stride(int D, int G) { return D + 1 + (G + 1) * (2 * D + 2); }
+constexpr int kGradRec = grad_stride(FLS_MAX_DIM, FLS_MAX_FIELDS);
 struct GradArgs {
   const double *pf;
   int32_t S;
   int64_t F;
   const double *X;
   const double *r;
+  const double *fields;            // n x nf coefficient fields (G > 0)
+  int32_t nf;
+  int32_t gfield[FLS_MAX_FIELDS];  // field id of group g+1
   int64_t row0, row1, rows_per_slot;
   int32_t slot0;
   double *partials;
@@ -178,7 +184,7 @@ struct GradArgs {
 cudaError_t launch_transform(int32_t D, int64_t F, const TransformArgs &t, const double *Wh,
                              double *W, cudaStream_t st);
 cudaError_t launch_grad_prefactor(const PrefArgs &a, cudaStream_t st);
-cudaError_t launch_grad_reduce(int D, const GradArgs &a, int slots, cudaStream_t st);
+cudaError_t launch_grad_reduce(int D, int G, const GradArgs &a, int slots, cudaStream_t st);
 cudaError_t launch_grad_final(int D, int64_t F, int nslots, const double *partials,
                               const double *beta, const double *Wh, double *G, cudaStream_t st);
 cudaError_t launch_axpy(int64_t n, double alpha, const double *x, const double *y, double *out,

@@ -29,21 +29,14 @@ def outer_loss_and_grad(ctx, L, W_hat, b, blocks: Sequence[fls.Block], sqrt_mu: 
     extra = F if sqrt_mu > 0 else 0
     Ab, lda = fls.fls_assemble(ctx, W, b, blocks, normalize=normalize, extra_rows=extra)
     beta, _ = fls.fls_solve(ctx, Ab, R, lda, F, sqrt_mu)
-    zero = fls.make_nonlinearity("poly", [0.0])
     loss = 0.0
     rblocks = []
-    zeros = None
     for blk in blocks:
-        if blk.fields is not None:
-            raise NotImplementedError("coefficient fields in the bandwidth gradient")
-        Lu = fls.fls_eval(ctx, W, b, beta, blk.X, terms=blk.terms, normalize=normalize)
-        vals = blk.values if blk.values is not None else torch.zeros_like(Lu)
-        neg, _, st = fls.fls_nl_residual(ctx, zero, Lu, Lu, vals)          # v - L[u]
-        if zeros is None or zeros.numel() != neg.numel():
-            zeros = torch.zeros_like(neg)
-        r = fls.fls_axpy(ctx, -blk.weight, neg, zeros)                     # w (L[u] - v)
-        loss += blk.weight ** 2 * st[0]
-        rblocks.append(fls.Block(blk.X, blk.terms, blk.weight, r))
+        Abeta = fls.fls_eval_block(ctx, W, b, beta, blk, normalize=normalize)   # w L[u_N](x_i)
+        vals = blk.values if blk.values is not None else torch.zeros_like(Abeta)
+        r = fls.fls_axpy(ctx, -blk.weight, vals, Abeta)                        # w (L[u] - v)
+        loss += fls.fls_frob2(ctx, r, r.numel(), max(r.numel(), 1), 1) if r.numel() else 0.0
+        rblocks.append(fls.Block(blk.X, blk.terms, blk.weight, r, blk.fields))
     G = fls.fls_bandwidth_grad(ctx, W, W_hat, b, rblocks, beta, normalize=normalize)
     return loss, G, beta
 

@@ -49,6 +49,19 @@ def test_bandwidth_gradient_matches_oracle(ctx, L):
     assert np.abs(G - G_o).max() <= 1e-7 * np.abs(G_o).max(), (G, G_o)
 
 
+@pytest.mark.parametrize("L", [[[5.0, 0.0], [0.0, 5.0]], [[4.0, 0.0], [0.5, 5.0]]])
+def test_bandwidth_gradient_with_coefficient_field_matches_oracle(ctx, L):
+    """variable-coefficient Helmholtz (k^2 (1 + x_1) u as a coefficient field)"""
+    p = wl.make_helmholtz2d_var(n_int=300, per_edge=20, n_features=60)
+    W_hat, b = p.parity_features()
+    loss_o, G_o, _ = ol.outer_grad(np.array(L), W_hat, b, p.blocks)
+    loss, G, _ = outer_loss_and_grad(ctx, L, torch.from_numpy(W_hat).cuda(),
+                                     torch.from_numpy(b).cuda(), dev_blocks(p))
+    G = np.array(G)
+    assert abs(loss - loss_o) <= 1e-8 * loss_o
+    assert np.abs(G - G_o).max() <= 1e-7 * np.abs(G_o).max(), (G, G_o)
+
+
 def test_adamw_trajectory_matches_oracle(ctx):
     p, W_hat, b = _setup()
     steps, lr = 6, 0.05

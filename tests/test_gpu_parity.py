@@ -357,8 +357,12 @@ def test_error_paths_extended(ctx):
     b = torch.rand(7, dtype=torch.float64, device=dev)
     blk = fls.Block(X, [((0, 0), 1.0, 0)], 1.0, torch.zeros(20, dtype=torch.float64, device=dev),
                     torch.ones((20, 1), dtype=torch.float64, device=dev))
-    with pytest.raises(FlsError, match="EUNSUPPORTED"):
-        fls.fls_bandwidth_grad(ctx, W, W, b, [blk], torch.zeros(7, dtype=torch.float64, device=dev))
+    G = fls.fls_bandwidth_grad(ctx, W, W, b, [blk], torch.zeros(7, dtype=torch.float64, device=dev))
+    assert np.all(np.array(G) == 0.0)                                    # r = 0: fields allowed
+    blk_bad = fls.Block(X, [((0, 0), 1.0, 1)], 1.0, torch.zeros(20, dtype=torch.float64, device=dev),
+                        torch.ones((20, 1), dtype=torch.float64, device=dev))
+    with pytest.raises(FlsError, match="EINVAL"):                        # field id >= n_fields
+        fls.fls_bandwidth_grad(ctx, W, W, b, [blk_bad], torch.zeros(7, dtype=torch.float64, device=dev))
     with pytest.raises(FlsError, match="EINVAL"):                        # eval op with a field
         fls.fls_eval(ctx, W, b, torch.zeros(7, dtype=torch.float64, device=dev), X,
                      terms=[((0, 0), 1.0, 0)])

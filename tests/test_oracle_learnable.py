@@ -39,3 +39,24 @@ def test_cholesky_gradient_matches_fd():
         Lm[k, l] -= h
         fd = (ol.outer_loss(Lp, W_hat, b, p.blocks)[0] - ol.outer_loss(Lm, W_hat, b, p.blocks)[0]) / (2 * h)
         assert abs(G[k, l] - fd) <= 1e-5 * max(abs(fd), abs(G).max()), (k, l, G[k, l], fd)
+
+
+def test_gradient_with_coefficient_field_matches_fd():
+    """variable-coefficient operator (k^2 (1 + x_1) u term as a coefficient field)"""
+    p = wl.make_helmholtz2d_var(n_int=300, per_edge=20, n_features=60)
+    W_hat, b = p.parity_features()
+    L = np.array([[4.0, 0.0], [0.5, 5.0]])
+    loss, G, _ = ol.outer_grad(L, W_hat, b, p.blocks)
+    for (k, l) in [(0, 0), (1, 0), (1, 1)]:
+        h = 1e-5
+        Lp, Lm = L.copy(), L.copy()
+        Lp[k, l] += h
+        Lm[k, l] -= h
+        fd = (ol.outer_loss(Lp, W_hat, b, p.blocks)[0] - ol.outer_loss(Lm, W_hat, b, p.blocks)[0]) / (2 * h)
+        assert abs(G[k, l] - fd) <= 1e-5 * max(abs(fd), abs(G).max()), (k, l, G[k, l], fd)
+    # the field matters: dropping it changes the gradient
+    import dataclasses
+    const = [dataclasses.replace(p.blocks[0], terms=p.blocks[0].terms[:-1] + [((0, 0), 100.0, -1)],
+                                 fields=None), p.blocks[1]]
+    _, G0, _ = ol.outer_grad(L, W_hat, b, const)
+    assert np.abs(G0 - G).max() > 1e-3 * np.abs(G).max()

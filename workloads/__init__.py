@@ -349,6 +349,27 @@ def make_helmholtz2d(n_int: int = 600, per_edge: int = 40, n_features: int = 120
     return Problem("helmholtz2d", 2, n_features, 1.0, blocks, u, lo, hi, 0.0, seed)
 
 
+def make_helmholtz2d_var(n_int: int = 600, per_edge: int = 40, n_features: int = 120,
+                         k: float = 10.0, seed: int = 0) -> Problem:
+    """Variable-coefficient Helmholtz 2D: Lap u + k^2 (1 + x_1) u = f on [0,1]^2 (coefficient
+    field c(x) = 1 + x_1 on the zeroth-order term, as in config 5's reading A11), Dirichlet
+    (lambda = 100), u* = sin(4 pi x) sin(4 pi y), f = (k^2 (1 + x_1) - 32 pi^2) u*.  For the
+    learnable-bandwidth gradient with coefficient fields."""
+    gi, gb = rng(seed, STREAM_INTERIOR), rng(seed, STREAM_BOUNDARY)
+    lo, hi = np.zeros(2), np.ones(2)
+    Xi = _uniform_box(gi, n_int, lo, hi)
+    Xb = _faces(gb, 2, per_edge, lo, hi, axes=[1, 0])
+
+    def u(X):
+        return np.sin(4 * PI * X[:, 0]) * np.sin(4 * PI * X[:, 1])
+    cf = 1.0 + Xi[:, 0]
+    f = (k * k * cf - 32 * PI * PI) * u(Xi)
+    blocks = [Block("pde", _c(Xi), op_laplacian(2, 1.0) + [((0, 0), k * k, 0)], 1.0, _c(f),
+                    fields=_c(cf[:, None])),
+              Block("bc", _c(Xb), op_identity(2), 100.0, _c(u(Xb)))]
+    return Problem("helmholtz2d_var", 2, n_features, 1.0, blocks, u, lo, hi, 0.0, seed)
+
+
 def sample_rows(n_rows: int, n_shards: int = 8, stride: int = 256) -> np.ndarray:
     """Deterministic sampled global rows: every stride-th row plus the first and last
     row of every shard of an n_shards-way split."""
