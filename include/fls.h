@@ -59,7 +59,7 @@ extern "C" {
 #define FLS_API
 #endif
 
-#define FLS_API_VERSION 1
+#define FLS_API_VERSION 2  /* 2: fls_features_assemble, fls_geqrf, fls_eval_block; fields in fls_bandwidth_grad */
 #define FLS_MAX_DIM 8      /* spatial / space-time dimension d <= 8 */
 #define FLS_MAX_TERMS 64   /* terms per operator */
 #define FLS_MAX_FIELDS 4   /* coefficient fields per block */

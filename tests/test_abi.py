@@ -68,3 +68,12 @@ def test_product_package_never_imports_oracle():
     # and the oracle never includes the product headers
     orc = open(os.path.join(root, "oracle", "oracle.c")).read()
     assert "fls.h" not in orc and "fls_device" not in orc
+
+
+def test_api_version_matches_header():
+    """the library reports the FLS_API_VERSION its header declares"""
+    import re
+    from paper_2602_10541_b200 import _abi
+    hdr = open(_abi.HEADER).read()
+    v = int(re.search(r"#define FLS_API_VERSION (\d+)", hdr).group(1))
+    assert _abi.load().fls_api_version() == v
