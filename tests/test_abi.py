@@ -30,7 +30,7 @@ def test_library_exports_every_header_symbol(lib):
 
 
 def test_api_version_and_status_strings(lib):
-    assert lib.fls_api_version() == 1
+    assert lib.fls_api_version() == 2
     for k, v in _abi.STATUS.items():
         assert lib.fls_status_string(k).decode() == v
 
