@@ -503,6 +503,23 @@ def main():
                 pk = sms * 64 * mhz * 1e6 / 1e12
                 fp64[f"peak_tops_{tag}"] = pk
                 fp64[f"frac_{tag}"] = ach / pk
+    # the binding roofline under sustained load: board power (profiles/r01_power_model.json,
+    # tools/power_model.py: idle power + measured energy per entry of the store pattern and of the
+    # per-entry arithmetic, each probed alone) -> entries/s <= (P_limit - P_idle) / (E_st + E_alu)
+    power = None
+    pm = os.path.join(ROOT, "profiles", "r01_power_model.json")
+    if os.path.exists(pm) and p.name == "c5_biharm3d":
+        try:
+            m = json.load(open(pm))["model"]
+            bound = m["power_bound_entries_per_s"]
+            power = {"bound": "board power", "limit_w": m["power_limit_w"], "idle_w": m["idle_w"],
+                     "nj_per_entry": m["store_nj_per_entry"] + m["alu_nj_per_entry"],
+                     "bound_entries_per_s_per_gpu": bound,
+                     "achieved_entries_per_s_per_gpu": n_local * F / (k_ms_step / 1e3),
+                     "frac": n_local * F / (k_ms_step / 1e3) / bound,
+                     "source": "profiles/r01_power_model.json (tools/power_model.py)"}
+        except Exception:
+            power = None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -517,7 +534,7 @@ def main():
                      "frac": achieved / hbm_peak, "traffic": traffic,
                      "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
                      "kernel": "assemble_rm_kernel" if row_major else "assemble_cm_kernel",
-                     "kernel_ms_avg": k_avg_ms, "fp64_pipe": fp64,
+                     "kernel_ms_avg": k_avg_ms, "fp64_pipe": fp64, "power": power,
                      "scope": "rank 0's GPU (per-GPU kernel roofline)"},
         "gpu_launches": launches_per_step_fixed * args.steps + k_launches,
         "clocks": clocks,
