@@ -350,7 +350,8 @@ def solve_measure(args, world, rank, local):
     ctx.close()
     out = {"ms": sum(ph), "features_ms": ph[0], "assemble_ms": ph[1], "lstsq_ms": ph[2],
            "eval_ms": ph[3], "rows": R, "features": F, "ridge_rel": p.ridge_rel,
-           "method": "Householder QR (fls_geqrf: blocked compact-WY on cuBLAS DGEMM + cooperative leaf kernel) + trsv" + (" / TSQR over ranks" if world > 1 else ""),
+           "method": "Householder QR (fls_geqrf: blocked compact-WY on cuBLAS DGEMM + cooperative leaf kernel) + trsv"
+                     + (f" / TSQR over ranks ({fdist.LAST_TRANSPORT} transport)" if world > 1 else ""),
            "qr_flops": 2.0 * (R + extra) * (F + 1) ** 2 - 2.0 / 3.0 * (F + 1) ** 3,
            "resid_norm": res}
     out["qr_tflops"] = out["qr_flops"] / (ph[2] / 1e3) / 1e12

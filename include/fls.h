@@ -59,7 +59,7 @@ extern "C" {
 #define FLS_API
 #endif
 
-#define FLS_API_VERSION 2  /* 2: fls_features_assemble, fls_geqrf, fls_eval_block; fields in fls_bandwidth_grad */
+#define FLS_API_VERSION 2  /* 2: fls_features_assemble, fls_geqrf, fls_eval_block, fls_ipc_*; fields in fls_bandwidth_grad */
 #define FLS_MAX_DIM 8      /* spatial / space-time dimension d <= 8 */
 #define FLS_MAX_TERMS 64   /* terms per operator */
 #define FLS_MAX_FIELDS 4   /* coefficient fields per block */
@@ -341,6 +341,20 @@ FLS_API fls_status fls_qr_r(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda
  *   FLS_ECUSOLVER (cuBLAS failure).  Blocking. */
 FLS_API fls_status fls_geqrf(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda, int64_t n_cols,
                              double *tau);
+
+/* CUDA IPC for the TSQR exchange over peer memory (NVLink / NVSwitch): the root exports its
+ * stacking buffer, every rank maps it and fls_qr_r writes its R factor straight into the
+ * root's memory (the R-extraction kernel's stores ARE the transfer; no staging, no NCCL
+ * gather).  fls_ipc_handle: handle (host, FLS_IPC_HANDLE_BYTES) of the allocation that
+ * CONTAINS dev_ptr, and *offset = dev_ptr - that allocation's base (caching allocators
+ * sub-allocate).  fls_ipc_open maps a handle exported by ANOTHER process (same or peer
+ * device) and returns the allocation's base in this process (add the offset);
+ * fls_ipc_close unmaps it.  Errors: FLS_EINVAL (NULL), FLS_ECUDA (CUDA IPC failure, e.g.
+ * no peer access). */
+#define FLS_IPC_HANDLE_BYTES 64
+FLS_API fls_status fls_ipc_handle(fls_ctx *ctx, void *dev_ptr, void *handle, int64_t *offset);
+FLS_API fls_status fls_ipc_open(fls_ctx *ctx, const void *handle, void **dev_ptr);
+FLS_API fls_status fls_ipc_close(fls_ctx *ctx, void *dev_ptr);
 
 /* sum of squares of the n_rows x n_cols column-major block (for ||A||_F^2).  out: host.
  * Blocking. */

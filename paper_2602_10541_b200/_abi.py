@@ -20,6 +20,7 @@ FLS_MAX_TERMS = 64
 FLS_MAX_FIELDS = 4
 FLS_COL_MAJOR = 0
 FLS_ROW_MAJOR = 1
+FLS_IPC_HANDLE_BYTES = 64
 
 STATUS = {0: "FLS_OK", 1: "FLS_EINVAL", 2: "FLS_ENOMEM", 3: "FLS_ECUDA", 4: "FLS_ECUSOLVER",
           5: "FLS_ENCCL", 6: "FLS_ENONFINITE", 7: "FLS_ERANK", 8: "FLS_EUNSUPPORTED"}
@@ -103,6 +104,9 @@ _SIGS = {
     "fls_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_double,
                             C.c_void_p, C.POINTER(C.c_double)]),
     "fls_geqrf": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p]),
+    "fls_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
+    "fls_ipc_open": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "fls_ipc_close": (C.c_int, [C.c_void_p, C.c_void_p]),
     "fls_qr_r": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
                            C.c_int64]),
     "fls_frob2": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,

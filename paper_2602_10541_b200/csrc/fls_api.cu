@@ -3,6 +3,7 @@
 //
 // Product code.  Paper = PAPER.md (arxiv 2602.10541), cited P:L<line>.
 #include <cublas_v2.h>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 
@@ -932,6 +933,53 @@ fls_status fls_geqrf(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda, int64
   if (fls_status s = fls_sync(ctx)) return s;
   if (fls_status s = ensure_handles(ctx)) return s;
   return geqrf_inplace(ctx, M, n_rows, lda, n_cols, tau);
+}
+
+fls_status fls_ipc_handle(fls_ctx *ctx, void *dev_ptr, void *handle, int64_t *offset) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!dev_ptr || !handle || !offset) return fail(FLS_EINVAL, "dev_ptr, handle or offset is NULL");
+  static_assert(sizeof(cudaIpcMemHandle_t) <= FLS_IPC_HANDLE_BYTES, "IPC handle size");
+  DeviceGuard g(ctx->device);
+  // allocation base through the driver entry point (no link-time libcuda dependency)
+  typedef CUresult (*range_fn)(CUdeviceptr *, size_t *, CUdeviceptr);
+  static range_fn get_range = nullptr;
+  if (!get_range) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(FLS_ECUDA, "cuMemGetAddressRange entry point unavailable");
+    get_range = reinterpret_cast<range_fn>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(FLS_EINVAL, "dev_ptr is not device memory");
+  *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  cudaIpcMemHandle_t h;
+  FLS_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base)));
+  std::memset(handle, 0, FLS_IPC_HANDLE_BYTES);
+  std::memcpy(handle, &h, sizeof h);
+  return FLS_OK;
+}
+
+fls_status fls_ipc_open(fls_ctx *ctx, const void *handle, void **dev_ptr) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!handle || !dev_ptr) return fail(FLS_EINVAL, "handle or dev_ptr is NULL");
+  DeviceGuard g(ctx->device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  *dev_ptr = nullptr;
+  FLS_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return FLS_OK;
+}
+
+fls_status fls_ipc_close(fls_ctx *ctx, void *dev_ptr) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!dev_ptr) return fail(FLS_EINVAL, "dev_ptr is NULL");
+  DeviceGuard g(ctx->device);
+  FLS_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return FLS_OK;
 }
 
 fls_status fls_qr_r(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda, int64_t n_cols,

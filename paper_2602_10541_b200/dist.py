@@ -5,7 +5,9 @@ Assembly needs no collective: rank r owns global rows
 The solve has one real exchange step (TSQR, "QR or SVD"; Tikhonov form P:L158):
 
     local:  [A_r | b_r] = Q_r R_r                      (fls_qr_r, Householder QR on each GPU)
-    gather: R_0 .. R_{P-1} -> root                      (torch.distributed / NCCL over NVLink)
+    gather: R_0 .. R_{P-1} -> root   (default on GPUs: each rank's R-extraction kernel stores
+                                      straight into the root's buffer over CUDA IPC peer
+                                      memory; else a torch.distributed gather)
     root:   [R_0; ...; R_{P-1}; sqrt(mu) I | 0] = Q R   (fls_solve: geqrf + trsv)
     bcast:  beta
 
@@ -17,10 +19,14 @@ can be tested on CPU with gloo (tests/test_dist_gloo.py).
 from __future__ import annotations
 
 import math
+import os
 from typing import Callable, Optional, Tuple
 
 import torch
 import torch.distributed as dist
+
+
+LAST_TRANSPORT = None   # transport the last multi-rank tsqr_solve used ("p2p" / "collective")
 
 
 def shard_range(n_rows: int, rank: int, world: int) -> Tuple[int, int]:
@@ -44,6 +50,19 @@ class _FlsOps:
 
     def solve(self, M, n_rows, lda, F, sqrt_mu):
         return self.fls.fls_solve(self.ctx, M, n_rows, lda, F, sqrt_mu)
+
+    # peer-memory transport (CUDA IPC over NVLink / NVSwitch)
+    def qr_r_into(self, Ab, n_rows, lda, ncols, dst_ptr, ldr):
+        self.fls.fls_qr_r(self.ctx, Ab, n_rows, lda, ncols, ldr=ldr, R_ptr=dst_ptr)
+
+    def ipc_handle(self, t):
+        return self.fls.fls_ipc_handle(self.ctx, t)
+
+    def ipc_open(self, handle):
+        return self.fls.fls_ipc_open(self.ctx, handle)
+
+    def ipc_close(self, ptr):
+        self.fls.fls_ipc_close(self.ctx, ptr)
 
 
 def _combine(ops, Rs, ks, F, sqrt_mu, dev):
@@ -83,11 +102,63 @@ def tsqr_local(blocks, F: int, *, ridge_rel: float = 0.0, ctx=None, ops=None):
     return _combine(ops, Rs, ks, F, sqrt_mu, dev)
 
 
+def _tsqr_p2p(ops, Ab, n_local, lda, F, sqrt_mu, group, root, world, rank, dev, cdev):
+    """TSQR exchange over peer memory: the root allocates the stacking buffer S (rank r's R
+    factor at rows [r kmax, r kmax + k_r), zero rows elsewhere, ridge rows after), exports it
+    by CUDA IPC, and every rank's fls_qr_r writes its R straight into S (the copy kernel's
+    remote stores over NVLink are the transfer).  Host barrier, then the root solves."""
+    nc = F + 1
+    k = min(n_local, nc)
+    ks = torch.tensor([k], dtype=torch.int64, device=cdev)
+    all_k = [torch.zeros_like(ks) for _ in range(world)]
+    dist.all_gather(all_k, ks, group=group)
+    kmax = max(int(t.item()) for t in all_k)
+    K = world * kmax
+    ldm = ((K + (F if sqrt_mu > 0.0 else 0) + 3) // 4) * 4
+    S = None
+    obj = [None]
+    if rank == root:
+        S = torch.zeros((nc * ldm,), dtype=torch.float64, device=dev)
+        torch.cuda.synchronize(dev)
+        obj = [ops.ipc_handle(S)]
+    dist.broadcast_object_list(obj, src=root, group=group)
+    handle, off = obj[0]
+    base, ok = None, 1
+    try:
+        base = S.data_ptr() if rank == root else ops.ipc_open(handle) + off
+    except Exception:            # e.g. no peer access between these GPUs
+        ok = 0
+    flag = torch.tensor([ok], dtype=torch.int64, device=cdev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    if int(flag.item()) == 0:    # every rank falls back to the collective transport
+        if base is not None and rank != root:
+            ops.ipc_close(base - off)
+        return None
+    try:
+        if k > 0:
+            ops.qr_r_into(Ab, n_local, lda, nc, base + 8 * rank * kmax, ldm)   # blocking
+        dist.barrier(group=group)
+    finally:
+        if rank != root:
+            ops.ipc_close(base - off)
+    beta = torch.empty((F,), dtype=torch.float64, device=cdev)
+    res = 0.0
+    if rank == root:
+        b_root, res = ops.solve(S, K, ldm, F, sqrt_mu)
+        beta.copy_(b_root)
+    dist.broadcast(beta, src=root, group=group)
+    return beta.to(dev), res
+
+
 def tsqr_solve(Ab: torch.Tensor, n_local: int, lda: int, F: int, *, ridge_rel: float = 0.0,
-               ctx=None, ops=None, group=None, root: int = 0) -> Tuple[torch.Tensor, float]:
+               ctx=None, ops=None, group=None, root: int = 0,
+               transport: str = "auto") -> Tuple[torch.Tensor, float]:
     """beta = argmin ||A beta - b||^2 + mu ||beta||^2 for [A | b] row-sharded over the ranks.
 
     Ab: this rank's column-major [A_r | b_r] (flat, (F+1) * lda, destroyed).
+    transport: "p2p" (R factors written into the root's buffer over CUDA IPC peer memory),
+    "collective" (gather through torch.distributed), "auto" = p2p for NCCL process groups on
+    CUDA unless FLS_TSQR_TRANSPORT=collective.
     Returns (beta replicated on every rank, residual norm on root / 0.0 elsewhere)."""
     ops = ops if ops is not None else _FlsOps(ctx)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -110,7 +181,19 @@ def tsqr_solve(Ab: torch.Tensor, n_local: int, lda: int, F: int, *, ridge_rel: f
         beta, res = ops.solve(Ab, n_local, lda, F, sqrt_mu)
         return beta, res
 
-    # local R factor, padded to kmax rows (zero rows change nothing)
+    if transport == "auto":
+        transport = os.environ.get("FLS_TSQR_TRANSPORT", "")
+        if transport not in ("p2p", "collective"):
+            transport = "p2p" if (dev.type == "cuda" and dist.get_backend(group) == "nccl") else "collective"
+    global LAST_TRANSPORT
+    if transport == "p2p":
+        out = _tsqr_p2p(ops, Ab, n_local, lda, F, sqrt_mu, group, root, world, rank, dev, cdev)
+        if out is not None:
+            LAST_TRANSPORT = "p2p"
+            return out
+    LAST_TRANSPORT = "collective"
+
+    # collective transport: local R factor, padded to kmax rows (zero rows change nothing)
     k = min(n_local, nc)
     if k > 0:
         R, ldr = ops.qr_r(Ab, n_local, lda, nc)

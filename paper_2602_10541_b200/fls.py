@@ -25,7 +25,8 @@ from ._abi import FLS_COL_MAJOR, FLS_ROW_MAJOR, FlsError, check
 Term = Tuple[Sequence[int], float, int]   # (alpha, coef, field)
 
 __all__ = ["Context", "Block", "fls_features", "fls_assemble", "fls_features_assemble", "fls_solve", "fls_qr_r",
-           "fls_frob2", "fls_geqrf", "fls_eval", "fls_eval_block", "fls_sync", "fls_ctx_timing", "fls_ctx_timing_read",
+           "fls_frob2", "fls_geqrf", "fls_eval", "fls_eval_block", "fls_ipc_handle", "fls_ipc_open",
+           "fls_ipc_close", "fls_sync", "fls_ctx_timing", "fls_ctx_timing_read",
            "fls_assemble_host", "HostBlockSet", "BlockSet", "fls_features_blocks", "QRFactor",
            "make_nonlinearity", "fls_nl_residual", "fls_axpy", "fls_features_transform",
            "fls_bandwidth_grad", "fls_sample_box", "fls_sample_faces", "FlsError", "FLS_COL_MAJOR", "FLS_ROW_MAJOR",
@@ -472,14 +473,37 @@ def fls_geqrf(ctx: Context, M: torch.Tensor, n_rows: int, lda: int, n_cols: int,
 
 
 def fls_qr_r(ctx: Context, M: torch.Tensor, n_rows: int, lda: int, n_cols: int,
-             R: Optional[torch.Tensor] = None, ldr: Optional[int] = None):
+             R: Optional[torch.Tensor] = None, ldr: Optional[int] = None, R_ptr: Optional[int] = None):
+    """local Householder QR, R (upper trapezoid) into R -- or into raw device memory R_ptr (e.g.
+    a peer process's buffer mapped by fls_ipc_open: the copy kernel's stores are the transfer)"""
     k = min(n_rows, n_cols)
     ldr = k if ldr is None else ldr
-    if R is None:
+    if R_ptr is None and R is None:
         R = torch.empty((n_cols * ldr,), dtype=torch.float64, device=M.device)
-    check(_abi.load().fls_qr_r(ctx.handle, _ptr(M), int(n_rows), int(lda), int(n_cols), _ptr(R),
+    dst = C.c_void_p(R_ptr) if R_ptr is not None else _ptr(R)
+    check(_abi.load().fls_qr_r(ctx.handle, _ptr(M), int(n_rows), int(lda), int(n_cols), dst,
                                int(ldr)))
     return R, ldr
+
+
+def fls_ipc_handle(ctx: Context, t: torch.Tensor):
+    """(CUDA IPC handle of the allocation holding device tensor t, byte offset of t in it)"""
+    buf = (C.c_char * _abi.FLS_IPC_HANDLE_BYTES)()
+    off = C.c_int64(0)
+    check(_abi.load().fls_ipc_handle(ctx.handle, C.c_void_p(t.data_ptr()), buf, C.byref(off)))
+    return bytes(buf), int(off.value)
+
+
+def fls_ipc_open(ctx: Context, handle: bytes) -> int:
+    """map another process's exported allocation; returns its base device address here"""
+    buf = (C.c_char * _abi.FLS_IPC_HANDLE_BYTES).from_buffer_copy(handle)
+    out = C.c_void_p()
+    check(_abi.load().fls_ipc_open(ctx.handle, buf, C.byref(out)))
+    return int(out.value)
+
+
+def fls_ipc_close(ctx: Context, ptr: int):
+    check(_abi.load().fls_ipc_close(ctx.handle, C.c_void_p(ptr)))
 
 
 def fls_frob2(ctx: Context, A: torch.Tensor, n_rows: int, lda: int, n_cols: int) -> float:
