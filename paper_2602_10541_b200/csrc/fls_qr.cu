@@ -151,9 +151,13 @@ __global__ void __launch_bounds__(kQrNT) qr_leaf_kernel(const QrLeafArgs a) {
       for (int o = 16; o; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o);
       double tau = 0.0, scale = 0.0, beta = alpha;
       if (s0 > 0.0) {
-        beta = -copysign(hypot(alpha, sqrt(s0)), alpha);
-        tau = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
+        // ||[alpha; x]|| without hypot's rescaling (entries here are far from over/underflow)
+        // and one division for both tau = (beta - alpha) / beta and 1 / (alpha - beta)
+        beta = -copysign(sqrt(fma(alpha, alpha, s0)), alpha);
+        const double d = alpha - beta;
+        const double inv = 1.0 / (beta * d);
+        tau = -d * d * inv;
+        scale = beta * inv;
       }
       if (threadIdx.x == 0) {
         s_tau = tau;
