@@ -102,7 +102,10 @@ inline dim3 asm_grid(AsmArgs &a) {
   const int64_t rt = (span + kRowsCTA - 1) / kRowsCTA;
   const int64_t resident = (int64_t)sms * asm_min_blocks<D, G, KM>();
   const bool big_x = span * (D + G + 1) * 8 > ((int64_t)32 << 20);
-  const int64_t min_fpc = big_x ? (a.F < kFC ? a.F : kFC) : (a.F < 16 ? a.F : 16);
+  int64_t min_fpc = big_x ? (a.F < kFC ? a.F : kFC) : (a.F < 16 ? a.F : 16);
+  // small blocks (C1, C2): 16-feature CTAs cannot fill the waves -> narrower CTAs (>= 2, the
+  // features-per-iteration granularity) so the launch spreads over the SMs
+  if (!big_x && rt * ((a.F + 15) / 16) < waves * resident) min_fpc = a.F < 2 ? a.F : 2;
   const int64_t gmax = (a.F + min_fpc - 1) / min_fpc;
   int64_t g0 = (waves * resident + rt - 1) / rt;
   g0 = g0 < 1 ? 1 : (g0 > gmax ? gmax : g0);
