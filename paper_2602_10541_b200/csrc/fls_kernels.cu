@@ -149,40 +149,53 @@ __device__ void prefactor_one(const PrefArgs &a, int64_t j) {
   prefactor_core(a, j, w, bj);
 }
 
-// a1 + a2 fused (fls_features_assemble): one thread per feature draws W_j, b_j exactly as
-// features_kernel does (same Philox words, same Box-Muller arithmetic -> bit-identical), writes
-// them, and folds every block's prefactor record from the registers.
-__global__ void features_prefactor_kernel(int32_t D, int64_t F, const FeatBlocks fb,
-                                          uint64_t seed, double *W, double *b, const PrefBatch pb) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= F) return;
+// a1 + a2 fused (fls_features_assemble).  A CTA covers kFpFeat features: first one thread per
+// NORMAL (feature j, axis k; normal index m = j*D + k) draws it exactly as features_kernel does
+// (same Philox words, same Box-Muller arithmetic -> bit-identical W) into shared memory -- the
+// transcendental chains run in parallel instead of D deep per thread -- then one thread per
+// feature draws b_j and folds every block's prefactor record from the shared W row.
+constexpr int kFpFeat = 64;
+__global__ void __launch_bounds__(kFpFeat * FLS_MAX_DIM)
+features_prefactor_kernel(int32_t D, int64_t F, const FeatBlocks fb, uint64_t seed, double *W,
+                          double *b, const PrefBatch pb) {
+  __shared__ double ws[kFpFeat * FLS_MAX_DIM];
+  const int64_t j0 = (int64_t)blockIdx.x * kFpFeat;
   const double two_pi = 6.283185307179586476925286766559;
-  const double sig = block_sigma(fb, j);
-  double w[FLS_MAX_DIM];
-  for (int k = 0; k < D; ++k) {
-    const int64_t m = j * D + k;          // normal index; pair m/2 uses raw words m&~1, m|1
-    const int64_t word0 = m & ~int64_t(1);
-    uint64_t c[4] = {(uint64_t)(word0 / 4) + 1, 0, 0, 0};
-    philox4x64(c, seed, 1);
-    const int o = (int)(word0 % 4);
-    const double u1 = u01(c[o]), u2 = u01(c[o + 1]);
-    const double rad = sqrt(-2.0 * log(1.0 - u1));
-    const double th = two_pi * u2;
-    double sn, cs;
-    sincos(th, &sn, &cs);
-    w[k] = sig * (rad * ((m & 1) ? sn : cs));
-    W[m] = w[k];
+  const int t = threadIdx.x;
+  if (t < kFpFeat * D) {
+    const int64_t m = j0 * D + t;         // normal index; pair m/2 uses raw words m&~1, m|1
+    if (m < F * D) {
+      const int64_t word0 = m & ~int64_t(1);
+      uint64_t c[4] = {(uint64_t)(word0 / 4) + 1, 0, 0, 0};
+      philox4x64(c, seed, 1);
+      const int o = (int)(word0 % 4);
+      const double u1 = u01(c[o]), u2 = u01(c[o + 1]);
+      const double rad = sqrt(-2.0 * log(1.0 - u1));
+      const double th = two_pi * u2;
+      double sn, cs;
+      sincos(th, &sn, &cs);
+      const double w = block_sigma(fb, m / D) * (rad * ((m & 1) ? sn : cs));
+      ws[t] = w;
+      W[m] = w;
+    }
   }
+  __syncthreads();
+  if (t >= kFpFeat) return;
+  const int64_t j = j0 + t;
+  if (j >= F) return;
   uint64_t c[4] = {(uint64_t)(j / 4) + 1, 0, 0, 0};
   philox4x64(c, seed, 2);
   const double bj = two_pi * u01(c[j % 4]);
   b[j] = bj;
+  double w[FLS_MAX_DIM];
+  for (int k = 0; k < D; ++k) w[k] = ws[t * D + k];
   for (int q = 0; q < pb.n; ++q) prefactor_core(pb.blk[q], j, w, bj);
 }
 
 cudaError_t launch_features_prefactor(int32_t dim, int64_t F, const FeatBlocks &fb, uint64_t seed,
                                       double *W, double *b, const PrefBatch &pb, cudaStream_t st) {
-  features_prefactor_kernel<<<(unsigned)((F + 127) / 128), 128, 0, st>>>(dim, F, fb, seed, W, b, pb);
+  const int nt = ((kFpFeat * (dim > 1 ? dim : 1) + 31) / 32) * 32;
+  features_prefactor_kernel<<<(unsigned)((F + kFpFeat - 1) / kFpFeat), nt, 0, st>>>(dim, F, fb, seed, W, b, pb);
   return cudaGetLastError();
 }
 
