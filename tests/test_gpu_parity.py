@@ -250,7 +250,7 @@ def test_mode_sin_two_fields_high_order(ctx):
     _mode_case(ctx, terms, fields)
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(32))
 def test_random_operator_fuzz(ctx, seed):
     """random linear operators: 1..8 terms, |alpha| <= 6 per term, d in 1..8, 0..3 coefficient
     fields, random weights, with and without the 1/sqrt(N) normalisation (Table 3 ablation)"""
@@ -291,6 +291,11 @@ def test_random_operator_fuzz(ctx, seed):
     Arm, rrm = fls.fls_assemble(ctx, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(), [dv],
                                 normalize=normalize, layout=fls.FLS_ROW_MAJOR)
     assert np.array_equal(Arm[:, :F].cpu().numpy(), Ag) and np.array_equal(rrm.cpu().numpy(), rg)
+    # A beta without materialising A (fls_eval_block) for the same operator family
+    beta_h = g.normal(size=F)
+    got = fls.fls_eval_block(ctx, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(),
+                             torch.from_numpy(beta_h).cuda(), dv, normalize=normalize).cpu().numpy()
+    assert np.abs(got - Ao @ beta_h).max() <= 1e-12 * max((S @ np.abs(beta_h)).max(), 1e-300)
 
 
 @pytest.mark.parametrize("d", [1, 2, 4, 6, 8])
