@@ -1,0 +1,42 @@
+"""bench.py's own arm on the GPU (config 3, so it runs in seconds): one JSON line with the
+contract's keys, a positive value, the roofline / clocks / launch-count objects, and e2e +
+solve blocks when enabled."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(*extra):
+    r = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--no-cpu",
+                        *extra], cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return lines[0]
+
+
+def test_bench_line_contract_small():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    j = _run("--workload", "c3_poisson5d", "--e2e-steps", "1", "--e2e-ring-rows", "8192")
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "gpu_launches", "clocks", "e2e", "solve"):
+        assert k in j, k
+    assert j["value"] > 0 and j["n_gpus"] == 1 and j["steps"] == 3 and j["warmup"] == 3
+    rf = j["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in rf, k
+    assert 0 < rf["frac"] < 1.5 and rf["bound"] == "hbm"
+    assert j["gpu_launches"] >= 2 * j["steps"]
+    assert j["e2e"]["value"] > 0 and j["e2e"]["d2h_bytes_per_step"] > 0
+    assert j["solve"]["ms"] > 0
+    assert "sm_mhz" in j["clocks"] and "reasons" in j["clocks"]
