@@ -27,6 +27,8 @@ struct fls_ctx {
   size_t ws_bytes = 0;
   double *qws = nullptr;              // blocked-QR workspace (grow-only; + tau scratch)
   size_t qws_bytes = 0;
+  double *gws = nullptr;              // bandwidth-gradient partials (grow-only)
+  size_t gws_bytes = 0;
   cusolverDnHandle_t solver = nullptr;
   cublasHandle_t blas = nullptr;
   // optional per-launch timing of the assembly kernels (fls_ctx_timing)
@@ -217,6 +219,7 @@ fls_status fls_ctx_destroy(fls_ctx *ctx) {
   cudaFree(ctx->hout);
   cudaFree(ctx->ws);
   cudaFree(ctx->qws);
+  cudaFree(ctx->gws);
   cudaFree(ctx->d_err);
   cudaFree(ctx->d_scratch);
   delete ctx;
@@ -697,6 +700,22 @@ static fls_status ensure_handles(fls_ctx *ctx) {
 // cusolverDnDgeqrf call below that.  tau_out (k = min(m, n) doubles) may be NULL.
 constexpr int64_t kQrBlockedMinCols = 1024;
 
+// per-context solver scratch (grow-only): repeated solves (Newton, AdamW, RHS sweeps) never
+// allocate -- per-call stream-ordered allocations stalled the host sporadically
+static fls_status ensure_qws(fls_ctx *ctx, size_t bytes) {
+  if (bytes <= ctx->qws_bytes) return FLS_OK;
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->qws);
+  ctx->qws = nullptr;
+  ctx->qws_bytes = 0;
+  if (cudaMalloc((void **)&ctx->qws, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FLS_ENOMEM, "solver workspace of %zu bytes", bytes);
+  }
+  ctx->qws_bytes = bytes;
+  return FLS_OK;
+}
+
 // FLS_QR: "cusolver" / "blocked" force a method (A/B timing, tests); unset = by size.  Read
 // per call so a test can switch it.
 static int qr_method() {
@@ -716,17 +735,7 @@ static fls_status geqrf_inplace(fls_ctx *ctx, double *M, int64_t m, int64_t lda,
   const int method = qr_method();
   if (method != 1 && m <= qr_blocked_max_rows() && (method == 2 || n >= kQrBlockedMinCols)) {
     const size_t need = (qr_blocked_ws(m, n) + (size_t)(k > 0 ? k : 1)) * sizeof(double);
-    if (need > ctx->qws_bytes) {  // grow-only: repeated solves (Newton, RHS sweeps) reuse it
-      cudaStreamSynchronize(ctx->stream);
-      cudaFree(ctx->qws);
-      ctx->qws = nullptr;
-      ctx->qws_bytes = 0;
-      if (cudaMalloc((void **)&ctx->qws, need) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(FLS_ENOMEM, "blocked QR workspace of %zu bytes", need);
-      }
-      ctx->qws_bytes = need;
-    }
+    if (fls_status s = ensure_qws(ctx, need)) return s;
     double *tau = tau_out ? tau_out : ctx->qws + qr_blocked_ws(m, n);
     cudaError_t ce;
     cublasStatus_t be;
@@ -744,19 +753,16 @@ static fls_status geqrf_inplace(fls_ctx *ctx, double *M, int64_t m, int64_t lda,
   if (cusolverDnDgeqrf_bufferSize(ctx->solver, (int)m, (int)n, M, (int)lda, &lwork) !=
       CUSOLVER_STATUS_SUCCESS)
     return fail(FLS_ECUSOLVER, "cusolverDnDgeqrf_bufferSize failed");
-  double *work = nullptr;
   size_t bytes = ((size_t)lwork + (size_t)k + 2) * sizeof(double);
-  if (cudaMallocAsync((void **)&work, bytes, ctx->stream) != cudaSuccess) {
-    cudaGetLastError();
-    return fail(FLS_ENOMEM, "geqrf workspace of %zu bytes", bytes);
-  }
+  if (fls_status s = ensure_qws(ctx, bytes)) return s;
+  double *work = ctx->qws;
   double *tau = tau_out ? tau_out : work + lwork;
   int *info = reinterpret_cast<int *>(work + lwork + k);
   cusolverStatus_t st = cusolverDnDgeqrf(ctx->solver, (int)m, (int)n, M, (int)lda, tau, work,
                                          lwork, info);
   int h_info = 0;
   cudaMemcpyAsync(&h_info, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
-  cudaFreeAsync(work, ctx->stream);
+  
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return cuda_fail(e, "geqrf");
   if (st != CUSOLVER_STATUS_SUCCESS || h_info != 0)
@@ -888,10 +894,8 @@ fls_status fls_qr_solve(fls_ctx *ctx, const fls_qr *q, const double *B, int64_t 
       CUSOLVER_STATUS_SUCCESS)
     return fail(FLS_ECUSOLVER, "ormqr_bufferSize");
   const size_t cbytes = sizeof(double) * ldc * nrhs;
-  if (cudaMallocAsync((void **)&C, cbytes + sizeof(double) * (lwork + 2), ctx->stream) != cudaSuccess) {
-    cudaGetLastError();
-    return fail(FLS_ENOMEM, "qr_solve workspace");
-  }
+  if (fls_status s = ensure_qws(ctx, cbytes + sizeof(double) * (lwork + 2))) return s;
+  C = ctx->qws;
   double *work = C + ldc * nrhs;
   int *info = reinterpret_cast<int *>(work + lwork);
   FLS_CUDA(cudaMemsetAsync(C, 0, cbytes, ctx->stream));
@@ -906,7 +910,6 @@ fls_status fls_qr_solve(fls_ctx *ctx, const fls_qr *q, const double *B, int64_t 
                                   (int)q->ld, C, (int)ldc);
   cudaMemcpy2DAsync(Beta, sizeof(double) * ldbeta, C, sizeof(double) * ldc, sizeof(double) * q->n,
                     nrhs, cudaMemcpyDeviceToDevice, ctx->stream);
-  cudaFreeAsync(C, ctx->stream);
   FLS_CUDA(cudaStreamSynchronize(ctx->stream));
   if (st != CUSOLVER_STATUS_SUCCESS) return fail(FLS_ECUSOLVER, "ormqr status %d", (int)st);
   if (bs != CUBLAS_STATUS_SUCCESS) return fail(FLS_ECUSOLVER, "trsm status %d", (int)bs);
@@ -1104,12 +1107,20 @@ fls_status fls_bandwidth_grad(fls_ctx *ctx, const double *W, const double *W_hat
     slots_q[q] = n == 0 ? 0 : (int)std::min<int64_t>(16, (n + 255) / 256);
     nslots += slots_q[q];
   }
-  double *partials = nullptr;
+  // partial sums: grow-only per-context buffer (repeated calls in the AdamW loop)
   const size_t pbytes = sizeof(double) * ((size_t)std::max(nslots, 1) * F * dim + (size_t)dim * dim);
-  if (cudaMallocAsync((void **)&partials, pbytes, ctx->stream) != cudaSuccess) {
-    cudaGetLastError();
-    return fail(FLS_ENOMEM, "bandwidth_grad workspace");
+  if (pbytes > ctx->gws_bytes) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->gws);
+    ctx->gws = nullptr;
+    ctx->gws_bytes = 0;
+    if (cudaMalloc((void **)&ctx->gws, pbytes) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(FLS_ENOMEM, "bandwidth_grad workspace");
+    }
+    ctx->gws_bytes = pbytes;
   }
+  double *partials = ctx->gws;
   double *Gd = partials + (size_t)std::max(nslots, 1) * F * dim;
   const double s_norm = normalize ? 1.0 / std::sqrt((double)F) : 1.0;
   int slot0 = 0;
@@ -1157,7 +1168,6 @@ fls_status fls_bandwidth_grad(fls_ctx *ctx, const double *W, const double *W_hat
   }
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(G, Gd, sizeof(double) * dim * dim, cudaMemcpyDeviceToHost, ctx->stream);
-  cudaFreeAsync(partials, ctx->stream);
   if (e != cudaSuccess) return cuda_fail(e, "bandwidth_grad");
   FLS_CUDA(cudaStreamSynchronize(ctx->stream));
   return FLS_OK;
