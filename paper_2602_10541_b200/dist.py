@@ -120,8 +120,13 @@ def _tsqr_p2p(ops, Ab, n_local, lda, F, sqrt_mu, group, root, world, rank, dev, 
     if rank == root:
         S = torch.zeros((nc * ldm,), dtype=torch.float64, device=dev)
         torch.cuda.synchronize(dev)
-        obj = [ops.ipc_handle(S)]
+        try:
+            obj = [ops.ipc_handle(S)]
+        except Exception:        # e.g. an allocator whose memory cannot be exported (VMM)
+            obj = [None]
     dist.broadcast_object_list(obj, src=root, group=group)
+    if obj[0] is None:           # every rank falls back to the collective transport
+        return None
     handle, off = obj[0]
     base, ok = None, 1
     try:
