@@ -119,7 +119,8 @@ def _tsqr_p2p(ops, Ab, n_local, lda, F, sqrt_mu, group, root, world, rank, dev, 
     obj = [None]
     if rank == root:
         S = torch.zeros((nc * ldm,), dtype=torch.float64, device=dev)
-        torch.cuda.synchronize(dev)
+        if dev.type == "cuda":
+            torch.cuda.synchronize(dev)
         try:
             obj = [ops.ipc_handle(S)]
         except Exception:        # e.g. an allocator whose memory cannot be exported (VMM)

@@ -45,6 +45,50 @@ def _free_port():
     return p
 
 
+class NoIpcOps(NumpyOps):
+    """the root cannot export its buffer (e.g. VMM allocations): every rank must fall back"""
+
+    def ipc_handle(self, t):
+        raise RuntimeError("no CUDA IPC here")
+
+
+def _worker_p2p_fallback(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2602_10541_b200 import dist as fdist
+        R, F = 120, 16
+        g = np.random.default_rng(7)
+        A = g.normal(size=(R, F))
+        b = g.normal(size=R)
+        a, e = shard_range(R, rank, world)
+        n = e - a
+        lda = ((n + 3) // 4) * 4
+        Ab = torch.zeros((F + 1) * lda, dtype=torch.float64)
+        V = Ab.view(F + 1, lda)
+        V[:F, :n] = torch.from_numpy(A[a:e].T.copy())
+        V[F, :n] = torch.from_numpy(b[a:e].copy())
+        beta, _ = tsqr_solve(Ab, n, lda, F, ops=NoIpcOps(), transport="p2p")
+        out[rank] = (beta.numpy().tolist(), fdist.LAST_TRANSPORT)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_tsqr_p2p_falls_back_to_collective_on_every_rank():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_p2p_fallback, args=(2, _free_port(), out), nprocs=2, join=True)
+    g = np.random.default_rng(7)
+    A = g.normal(size=(120, 16))
+    b = g.normal(size=120)
+    ref, *_ = np.linalg.lstsq(A, b, rcond=None)
+    for r in range(2):
+        beta, used = out[r]
+        assert used == "collective"
+        assert np.allclose(beta, ref, rtol=1e-9, atol=1e-9 * np.abs(ref).max())
+
+
 def _worker(rank, world, port, case, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
