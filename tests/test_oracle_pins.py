@@ -378,3 +378,44 @@ def test_config_recovery(name, tol):
     u = oracle.evaluate(W, b, beta, Xt)
     us = p.u_star(Xt)
     assert np.linalg.norm(u - us) / np.linalg.norm(us) <= tol
+
+
+# ----------------------------------------------------------------------------- SPEC identities
+def test_zero_phase_rows():
+    """pin: at zero phase (x = 0, b = 0) the identity row is sin(0) = 0 and a
+    first-derivative row is W_j cos(0) = W_j (scaled by s = 1/sqrt(N))."""
+    d, F = 2, 9
+    W, _ = rand_basis(d, F, 2.0, 11)
+    b = np.zeros(F)
+    X = np.zeros((1, d))
+    H, _ = col(W, b, X, wl.op_identity(d), normalize=True)
+    assert np.all(H == 0.0)
+    Dx, _ = col(W, b, X, [((1, 0), 1.0, -1)], normalize=True)
+    assert np.allclose(Dx[0], W[:, 0] / math.sqrt(F), rtol=1e-15, atol=0)
+
+
+def test_axis_permutation_symmetry():
+    """pin: permuting the coordinate axes of X, W and every multi-index together
+    leaves A unchanged, exactly (same products in the same order up to commutation)."""
+    d, F = 3, 23
+    W, b = rand_basis(d, F, 2.0, 12)
+    X = np.random.default_rng(13).random((17, d))
+    terms = [((2, 1, 0), 1.5, -1), ((0, 0, 3), -0.25, -1), ((1, 0, 1), 2.0, -1)]
+    perm = [2, 0, 1]
+    A, _ = col(W, b, X, terms)
+    tp = [(tuple(a[p] for p in perm), c, f) for a, c, f in terms]
+    Ap, _ = col(W[:, perm], b, X[:, perm], tp)
+    assert np.allclose(A, Ap, rtol=1e-14, atol=1e-14 * np.abs(A).max())
+
+
+def test_zero_source_gives_zero_beta_and_mu0_is_lstsq():
+    """pins: a zero right-hand side gives beta = 0 exactly (Q^T 0 = 0); the Tikhonov
+    solve with mu = 0 is the plain least-squares solve."""
+    g = np.random.default_rng(14)
+    A = g.normal(size=(40, 12))
+    beta, res, _ = oracle.lstsq(A, np.zeros(40))
+    assert np.all(beta == 0.0) and res == 0.0
+    bv = g.normal(size=40)
+    b1, r1, _ = oracle.lstsq(A, bv)
+    b2, r2, _ = oracle.lstsq_mu(A, bv, 0.0)
+    assert np.allclose(b1, b2, rtol=1e-13, atol=1e-13) and abs(r1 - r2) <= 1e-13 * max(r1, 1.0)
