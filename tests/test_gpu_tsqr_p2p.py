@@ -87,3 +87,16 @@ def test_tsqr_p2p_matches_oracle_and_collective(name):
         assert np.linalg.norm(u - u_o) / np.linalg.norm(u_o) <= 1e-6
         assert np.linalg.norm(u - col[r][0]) / np.linalg.norm(u_o) <= 1e-9
     assert abs(p2p[0][1] - col[0][1]) <= 1e-9 * max(abs(col[0][1]), 1e-300)
+
+
+def test_ipc_errors():
+    """an invalid IPC handle maps to FLS_ECUDA; NULL arguments to FLS_EINVAL"""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_10541_b200 import fls
+    ctx = fls.Context(0)
+    with pytest.raises(fls.FlsError, match="ECUDA"):
+        fls.fls_ipc_open(ctx, bytes(64))
+    t = torch.zeros(1000, dtype=torch.float64, device="cuda")
+    h, off = fls.fls_ipc_handle(ctx, t[10:])
+    assert len(h) == 64 and off >= 80 and off % 8 == 0      # offset of t[10:] in its allocation
