@@ -10,7 +10,9 @@ static cudaError_t go_sin(AsmArgs *blks, int n, cudaStream_t st) {
   const size_t smem = (size_t)kFC * S * sizeof(double);
   AsmBatch bt;
   bt.n = n;
-  int64_t total = 0;
+  int64_t total = 0, span = 0;
+  for (int q = 0; q < n; ++q) span += blks[q].lr1 - (blks[q].lr0 & ~int64_t(kRowAlign - 1));
+  for (int q = 0; q < n; ++q) blks[q].batch_span = span;
   for (int q = 0; q < n; ++q) {
     const dim3 g = asm_grid<D, G, KM_SIN>(blks[q]);  // sets blks[q].fpc
     bt.blk[q] = blks[q];

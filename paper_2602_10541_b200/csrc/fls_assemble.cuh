@@ -104,10 +104,17 @@ inline dim3 asm_grid(AsmArgs &a) {
   const bool big_x = span * (D + G + 1) * 8 > ((int64_t)32 << 20);
   int64_t min_fpc = big_x ? (a.F < kFC ? a.F : kFC) : (a.F < 16 ? a.F : 16);
   // small blocks (C1, C2): 16-feature CTAs cannot fill the waves -> narrower CTAs (>= 2, the
-  // features-per-iteration granularity) so the launch spreads over the SMs
-  if (!big_x && rt * ((a.F + 15) / 16) < waves * resident) min_fpc = a.F < 2 ? a.F : 2;
+  // features-per-iteration granularity) so the launch spreads over the SMs, each block of the
+  // batch getting CTAs in proportion to its rows
+  int64_t target = waves * resident;
+  if (!big_x && rt * ((a.F + 15) / 16) < waves * resident) {
+    min_fpc = a.F < 2 ? a.F : 2;
+    if (a.batch_span > span) target = (target * span + a.batch_span - 1) / a.batch_span;
+    const int64_t floor16 = rt * ((a.F + 15) / 16);  // never wider than 16 features per CTA
+    if (target < floor16) target = floor16;
+  }
   const int64_t gmax = (a.F + min_fpc - 1) / min_fpc;
-  int64_t g0 = (waves * resident + rt - 1) / rt;
+  int64_t g0 = (target + rt - 1) / rt;
   g0 = g0 < 1 ? 1 : (g0 > gmax ? gmax : g0);
   int64_t best = g0;
   double best_eff = -1.0;

@@ -78,6 +78,7 @@ struct AsmArgs {
   int32_t nf;                    // n_fields of the block (row stride of fields)
   int32_t vec;                   // 16-byte vector stores allowed
   int64_t fpc;                   // features per CTA (set by the launcher)
+  int64_t batch_span;            // rows of all blocks in this launch (set by the launcher)
   int32_t gfield[FLS_MAX_FIELDS];// field id of group g+1
 };
 
