@@ -77,3 +77,16 @@ def test_api_version_matches_header():
     hdr = open(_abi.HEADER).read()
     v = int(re.search(r"#define FLS_API_VERSION (\d+)", hdr).group(1))
     assert _abi.load().fls_api_version() == v
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """no CPU fallback: pointing the binding at a missing libfls raises at first use"""
+    import subprocess
+    import sys
+    code = ("import os, sys; sys.path.insert(0, %r)\n"
+            "from paper_2602_10541_b200 import _abi\n"
+            "try:\n    _abi.load()\nexcept Exception as e:\n    print('RAISED', type(e).__name__)\n"
+            "else:\n    print('LOADED')\n") % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FLS_LIB=str(tmp_path / "libfls_missing.so"))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=120)
+    assert "RAISED FlsError" in r.stdout, r.stdout + r.stderr
