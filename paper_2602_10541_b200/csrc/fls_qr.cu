@@ -134,26 +134,44 @@ __global__ void __launch_bounds__(kQrNT) qr_leaf_kernel(const QrLeafArgs a) {
     const double *part = a.part + (size_t)(jj & 1) * gridDim.x * (kQrB + 1);
     const double *rowb = a.rowb + (jj & 1) * (kQrB + 1);
     qr_grid_barrier(a.bar, (unsigned)jj);
-    // ---- every warp: total of slot 0 (same order in every CTA) -> dlarfg, redundantly, then
-    // the totals of its slots q: tot[q] = tau * v^T a_{jj+q} (v_jj = 1); one round trip to L2
+    // ---- every warp: totals of slot 0 and of its own slots q (same order in every CTA; all
+    // loads issued before any use: one L2 round trip), then dlarfg redundantly, then
+    // tot[q] = tau * v^T a_{jj+q} (v_jj = 1)
     {
-      double v0[kQrMaxGrid / 32];
+      constexpr int NS = (kQrB + kQrW - 1) / kQrW;  // own slots per warp
+      const int q0 = warp > 0 ? warp : kQrW;
+      double v0 = 0.0, vs[NS], rq[NS];
+#pragma unroll
+      for (int i = 0; i < NS; ++i) vs[i] = rq[i] = 0.0;
 #pragma unroll
       for (int t = 0; t < kQrMaxGrid / 32; ++t) {
         const unsigned k = lane + 32 * t;
-        v0[t] = k < gridDim.x ? part[k] : 0.0;   // the barrier's acquire invalidated L1
+        if (k < gridDim.x) {
+          v0 += part[k];                         // the barrier's acquire invalidated L1
+#pragma unroll
+          for (int i = 0; i < NS; ++i) {
+            const int q = q0 + kQrW * i;
+            if (q < nc) vs[i] += part[(int64_t)q * gridDim.x + k];
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NS; ++i) {
+        const int q = q0 + kQrW * i;
+        if (q < nc) rq[i] = rowb[q];
       }
       const double alpha = rowb[0];
-      double s0 = 0.0;
 #pragma unroll
-      for (int t = 0; t < kQrMaxGrid / 32; ++t) s0 += v0[t];
+      for (int o = 16; o; o >>= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, o);
 #pragma unroll
-      for (int o = 16; o; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        for (int i = 0; i < NS; ++i) vs[i] += __shfl_xor_sync(0xffffffffu, vs[i], o);
+      }
       double tau = 0.0, scale = 0.0, beta = alpha;
-      if (s0 > 0.0) {
+      if (v0 > 0.0) {
         // ||[alpha; x]|| without hypot's rescaling (entries here are far from over/underflow)
         // and one division for both tau = (beta - alpha) / beta and 1 / (alpha - beta)
-        beta = -copysign(sqrt(fma(alpha, alpha, s0)), alpha);
+        beta = -copysign(sqrt(fma(alpha, alpha, v0)), alpha);
         const double d = alpha - beta;
         const double inv = 1.0 / (beta * d);
         tau = -d * d * inv;
@@ -165,20 +183,10 @@ __global__ void __launch_bounds__(kQrNT) qr_leaf_kernel(const QrLeafArgs a) {
         s_beta = beta;
         if (blockIdx.x == 0) a.tau[jj] = tau;
       }
-      for (int q = warp > 0 ? warp : kQrW; q < nc; q += kQrW) {
-        double v[kQrMaxGrid / 32];
 #pragma unroll
-        for (int t = 0; t < kQrMaxGrid / 32; ++t) {
-          const unsigned k = lane + 32 * t;
-          v[t] = k < gridDim.x ? part[(int64_t)q * gridDim.x + k] : 0.0;
-        }
-        const double rq = rowb[q];
-        double sq = 0.0;
-#pragma unroll
-        for (int t = 0; t < kQrMaxGrid / 32; ++t) sq += v[t];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-        if (lane == 0) tot[q] = tau * fma(scale, sq, rq);
+      for (int i = 0; i < NS; ++i) {
+        const int q = q0 + kQrW * i;
+        if (q < nc && lane == 0) tot[q] = tau * fma(scale, vs[i], rq[i]);
       }
     }
     __syncthreads();
