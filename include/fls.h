@@ -59,7 +59,7 @@ extern "C" {
 #define FLS_API
 #endif
 
-#define FLS_API_VERSION 2  /* 2: fls_features_assemble, fls_geqrf, fls_eval_block, fls_ipc_*; fields in fls_bandwidth_grad */
+#define FLS_API_VERSION 2  /* 2: fls_features_assemble, fls_geqrf, fls_eval_block, fls_ipc_*, fls_solve_stacked; fields in fls_bandwidth_grad */
 #define FLS_MAX_DIM 8      /* spatial / space-time dimension d <= 8 */
 #define FLS_MAX_TERMS 64   /* terms per operator */
 #define FLS_MAX_FIELDS 4   /* coefficient fields per block */
@@ -322,6 +322,20 @@ FLS_API fls_status fls_qr_factor(fls_ctx *ctx, const double *A, int64_t n_rows, 
 FLS_API fls_status fls_qr_solve(fls_ctx *ctx, const fls_qr *qr, const double *B, int64_t ldb,
                                 int64_t nrhs, double *Beta, int64_t ldbeta);
 FLS_API fls_status fls_qr_destroy(fls_qr *qr);
+
+/* TSQR root step (P:L124 solve of the stacked factors): S holds n_blocks upper-triangular or
+ * -trapezoidal factors [R_r | c_r] in block order -- block r = rows [r kb, (r+1) kb) of the
+ * column-major S (lds >= n_blocks kb, n_features + 1 columns), zero-padded to kb rows -- and
+ * the solve appends [sqrt_mu I | 0] rows when sqrt_mu > 0, then returns beta (device,
+ * n_features) and |R(F, F)| (host, may be NULL) exactly as fls_solve on the stacked matrix.
+ * The triangular structure is exploited: the rows are permuted (block 0, then row i of every
+ * other block and of the ridge, for i = 0, 1, ...) so that for the columns [j, j + w) only the
+ * first kb + G (j + w) rows can be nonzero, and the blocked QR stops each panel there (about
+ * half the flops of a dense QR of the stack at P = 8).  S is not modified.  Blocking.
+ *   Errors: FLS_EINVAL (sizes, NULL, underdetermined), FLS_ENOMEM, FLS_ECUSOLVER, FLS_ERANK. */
+FLS_API fls_status fls_solve_stacked(fls_ctx *ctx, const double *S, int32_t n_blocks, int64_t kb,
+                                     int64_t lds, int64_t n_features, double sqrt_mu, double *beta,
+                                     double *resid_norm);
 
 /* TSQR building block:Householder QR of the local column-major block M (n_rows x n_cols,
  * destroyed) and copy of its upper-trapezoidal R (min(n_rows, n_cols) x n_cols, zeros below

@@ -103,6 +103,8 @@ _SIGS = {
                                     C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]),
     "fls_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_double,
                             C.c_void_p, C.POINTER(C.c_double)]),
+    "fls_solve_stacked": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_int64,
+                                    C.c_double, C.c_void_p, C.POINTER(C.c_double)]),
     "fls_geqrf": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p]),
     "fls_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
     "fls_ipc_open": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),

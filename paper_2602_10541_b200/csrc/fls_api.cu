@@ -29,6 +29,8 @@ struct fls_ctx {
   size_t qws_bytes = 0;
   double *gws = nullptr;              // bandwidth-gradient partials (grow-only)
   size_t gws_bytes = 0;
+  double *sws = nullptr;              // permuted stack of the TSQR root solve (grow-only)
+  size_t sws_bytes = 0;
   cusolverDnHandle_t solver = nullptr;
   cublasHandle_t blas = nullptr;
   // optional per-launch timing of the assembly kernels (fls_ctx_timing)
@@ -220,6 +222,7 @@ fls_status fls_ctx_destroy(fls_ctx *ctx) {
   cudaFree(ctx->ws);
   cudaFree(ctx->qws);
   cudaFree(ctx->gws);
+  cudaFree(ctx->sws);
   cudaFree(ctx->d_err);
   cudaFree(ctx->d_scratch);
   delete ctx;
@@ -678,6 +681,9 @@ fls_status fls_assemble_host(fls_ctx *ctx, const double *W, const double *b, int
 
 }  // extern "C"
 
+static fls_status qr_trsv(fls_ctx *ctx, double *Ab, int64_t m, int64_t lda, int64_t n_features,
+                          double *beta, double *resid_norm, int64_t grp_base, int64_t grp_size);
+
 extern "C" {
 
 // ---------------------------------------------------------------------------------------------
@@ -726,7 +732,8 @@ static int qr_method() {
 }
 
 static fls_status geqrf_inplace(fls_ctx *ctx, double *M, int64_t m, int64_t lda, int64_t n,
-                                double *tau_out = nullptr) {
+                                double *tau_out = nullptr, int64_t grp_base = 0,
+                                int64_t grp_size = 0) {
   if (m > INT32_MAX || n > INT32_MAX || lda > INT32_MAX)
     return fail(FLS_EUNSUPPORTED, "geqrf: dimensions exceed int32 (m=%lld n=%lld lda=%lld)",
                 (long long)m, (long long)n, (long long)lda);
@@ -739,7 +746,8 @@ static fls_status geqrf_inplace(fls_ctx *ctx, double *M, int64_t m, int64_t lda,
     double *tau = tau_out ? tau_out : ctx->qws + qr_blocked_ws(m, n);
     cudaError_t ce;
     cublasStatus_t be;
-    const char *msg = qr_blocked(ctx->blas, ctx->stream, M, m, n, lda, tau, ctx->qws, &ce, &be);
+    const char *msg = qr_blocked(ctx->blas, ctx->stream, M, m, n, lda, tau, ctx->qws, &ce, &be,
+                                 grp_base, grp_size);
     cudaError_t e = cudaStreamSynchronize(ctx->stream);
     if (msg) {
       if (ce == cudaErrorMemoryAllocation) return fail(FLS_ENOMEM, "blocked QR: %s", msg);
@@ -790,8 +798,16 @@ fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int6
     cudaError_t e = launch_ridge_fill(Ab, lda, n_rows, n_features, n_features + 1, sqrt_mu, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "ridge_fill");
   }
+  return qr_trsv(ctx, Ab, m, lda, n_features, beta, resid_norm, 0, 0);
+}
+
+}  // extern "C"
+
+// [A | b] (m x (F+1), lda; ridge rows already in place) -> beta = R^-1 (Q^T b)[0:F], |R(F,F)|
+static fls_status qr_trsv(fls_ctx *ctx, double *Ab, int64_t m, int64_t lda, int64_t n_features,
+                          double *beta, double *resid_norm, int64_t grp_base, int64_t grp_size) {
   const int64_t n = n_features + 1;
-  if (fls_status s = geqrf_inplace(ctx, Ab, m, lda, n)) return s;
+  if (fls_status s = geqrf_inplace(ctx, Ab, m, lda, n, nullptr, grp_base, grp_size)) return s;
   // zero diagonal?
   cudaError_t e = launch_min_abs_diag(Ab, lda, n_features, ctx->d_scratch, ctx->stream);
   if (e != cudaSuccess) return cuda_fail(e, "min_abs_diag");
@@ -812,6 +828,46 @@ fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int6
   FLS_CUDA(cudaStreamSynchronize(ctx->stream));
   if (resid_norm) *resid_norm = std::fabs(rnn);
   return FLS_OK;
+}
+
+extern "C" {
+
+fls_status fls_solve_stacked(fls_ctx *ctx, const double *S, int32_t n_blocks, int64_t kb,
+                             int64_t lds, int64_t n_features, double sqrt_mu, double *beta,
+                             double *resid_norm) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!S || !beta) return fail(FLS_EINVAL, "S or beta is NULL");
+  if (n_features < 1 || n_blocks < 1 || kb < 1) return fail(FLS_EINVAL, "bad sizes");
+  if (lds < (int64_t)n_blocks * kb)
+    return fail(FLS_EINVAL, "lds %lld < n_blocks * kb = %lld", (long long)lds,
+                (long long)n_blocks * kb);
+  if (!(sqrt_mu >= 0.0) || !std::isfinite(sqrt_mu)) return fail(FLS_EINVAL, "sqrt_mu must be >= 0");
+  const int64_t F = n_features, n = F + 1;
+  const int64_t gq = (n_blocks - 1) + (sqrt_mu > 0.0 ? 1 : 0);
+  const int64_t groups = gq > 0 ? std::max<int64_t>(kb, sqrt_mu > 0.0 ? F : 0) : 0;
+  const int64_t m = kb + groups * gq;
+  if (m < F) return fail(FLS_EINVAL, "underdetermined: %lld rows < %lld features", (long long)m,
+                         (long long)F);
+  const int64_t ldm = (m + 3) / 4 * 4;
+  DeviceGuard g(ctx->device);
+  if (fls_status s = fls_sync(ctx)) return s;
+  if (fls_status s = ensure_handles(ctx)) return s;
+  const size_t need = sizeof(double) * (size_t)ldm * n;
+  if (need > ctx->sws_bytes) {  // grow-only scratch for the permuted stack
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->sws);
+    ctx->sws = nullptr;
+    ctx->sws_bytes = 0;
+    if (cudaMalloc((void **)&ctx->sws, need) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(FLS_ENOMEM, "stacked-solve workspace of %zu bytes", need);
+    }
+    ctx->sws_bytes = need;
+  }
+  cudaError_t e = launch_stack_permute(S, lds, n_blocks, kb, F, sqrt_mu, gq > 0 ? gq : 1, m, n,
+                                       ctx->sws, ldm, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "stack_permute");
+  return qr_trsv(ctx, ctx->sws, m, ldm, F, beta, resid_norm, kb, gq);
 }
 
 }  // extern "C"

@@ -196,7 +196,10 @@ cudaError_t launch_frob2(const double *A, int64_t lda, int64_t m, int64_t n, dou
 // blocked Householder QR (fls_qr.cu), geqrf output format; nullptr or a failure message
 const char *qr_blocked(cublasHandle_t h, cudaStream_t st, double *A, int64_t m, int64_t n,
                        int64_t lda, double *tau, double *ws, cudaError_t *cerr,
-                       cublasStatus_t *berr);
+                       cublasStatus_t *berr, int64_t grp_base = 0, int64_t grp_size = 0);
+cudaError_t launch_stack_permute(const double *S, int64_t lds, int32_t P, int64_t kb, int64_t F,
+                                 double sqrt_mu, int64_t gq, int64_t m_total, int64_t n, double *M,
+                                 int64_t ldm, cudaStream_t st);
 size_t qr_blocked_ws(int64_t m, int64_t n);  // doubles of ws (incl. nothing for tau)
 int qr_panel_width();
 int64_t qr_blocked_max_rows();  // taller blocks use cusolverDnDgeqrf

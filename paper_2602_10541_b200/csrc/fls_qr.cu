@@ -439,11 +439,48 @@ size_t qr_blocked_ws(int64_t m, int64_t n) {
          (size_t)2 * qr_grid() * (kQrB + 1) + 2 * (kQrB + 1) + 1;  // + barrier counter
 }
 
+// Row permutation of a block-order stack of P factors (block r = rows [r kb, (r+1) kb) of S)
+// into the order qr_blocked's grouped mode expects: block 0 first, then row group i = row i of
+// blocks 1..P-1 followed by ridge row i (sqrt_mu at column i), zeros where a source is absent.
+__global__ void stack_permute_kernel(const double *S, int64_t lds, int32_t P, int64_t kb, int64_t F,
+                                     double sqrt_mu, int64_t gq, int64_t m_total, int64_t n,
+                                     double *M, int64_t ldm) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= m_total * n) return;
+  const int64_t c = idx / m_total, t = idx % m_total;
+  double v = 0.0;
+  if (t < kb) {
+    v = S[c * lds + t];
+  } else {
+    const int64_t u = t - kb, i = u / gq, g = u % gq;
+    if (g < P - 1) {
+      if (i < kb) v = S[c * lds + (g + 1) * kb + i];
+    } else if (c == i && i < F) {
+      v = sqrt_mu;
+    }
+  }
+  M[c * ldm + t] = v;
+}
+
+cudaError_t launch_stack_permute(const double *S, int64_t lds, int32_t P, int64_t kb, int64_t F,
+                                 double sqrt_mu, int64_t gq, int64_t m_total, int64_t n, double *M,
+                                 int64_t ldm, cudaStream_t st) {
+  const int64_t tot = m_total * n;
+  if (tot == 0) return cudaSuccess;
+  stack_permute_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(S, lds, P, kb, F, sqrt_mu, gq,
+                                                                       m_total, n, M, ldm);
+  return cudaGetLastError();
+}
+
 // A (m x n, lda) -> R / V / tau in place, ws = qr_blocked_ws(m, n) doubles (caller-owned, so
 // repeated solves do not allocate).  Returns 0 or a message (static string).
+// grp_size > 0: A is a row-permuted stack of triangular factors (fls_solve_stacked): rows
+// [0, grp_base) are one upper-trapezoidal block and row group i (rows grp_base + i grp_size ..
+// + grp_size - 1) is zero left of column i -- so the rows of panel [j, j+w) that can be nonzero
+// end at grp_base + grp_size (j + w), and the panel and its trailing update stop there.
 const char *qr_blocked(cublasHandle_t h, cudaStream_t st, double *A, int64_t m, int64_t n,
                        int64_t lda, double *tau, double *ws, cudaError_t *cerr,
-                       cublasStatus_t *berr) {
+                       cublasStatus_t *berr, int64_t grp_base, int64_t grp_size) {
   *cerr = cudaSuccess;
   *berr = CUBLAS_STATUS_SUCCESS;
   const int64_t k = m < n ? m : n;
@@ -488,7 +525,8 @@ const char *qr_blocked(cublasHandle_t h, cudaStream_t st, double *A, int64_t m, 
   bool good = ok_blas(q, cublasSetStream(h, st), "cublasSetStream");
   for (int64_t j = 0; good && j < k; j += nb) {
     const int64_t w = nb < k - j ? nb : k - j;
-    const int64_t mp = m - j;
+    int64_t mp = m - j;
+    if (grp_size > 0) mp = std::min<int64_t>(mp, grp_base + grp_size * (j + w) - j);
     double *P = A + j * lda + j;
     const int64_t rc = (mp + q.grid - 1) / q.grid;
     q.bleaf = (int)std::min<int64_t>(kQrB, (int64_t)kQrSlab / (rc * (int64_t)sizeof(double)));

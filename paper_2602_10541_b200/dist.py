@@ -8,7 +8,8 @@ The solve has one real exchange step (TSQR, "QR or SVD"; Tikhonov form P
     gather: R_0 .. R_{P-1} -> root   (default on GPUs: each rank's R-extraction kernel stores
                                       straight into the root's buffer over CUDA IPC peer
                                       memory; else a torch.distributed gather)
-    root:   [R_0; ...; R_{P-1}; sqrt(mu) I | 0] = Q R   (fls_solve: geqrf + trsv)
+    root:   [R_0; ...; R_{P-1}; sqrt(mu) I | 0] = Q R   (fls_solve_stacked: the triangles' zeros
+                                                     skipped, blocked QR + trsv)
     bcast:  beta
 
 `ridge_rel` = tau of DESIGN.md reading A16: sqrt(mu) = tau ||A||_F with ||A||_F^2 summed over
@@ -51,6 +52,9 @@ class _FlsOps:
     def solve(self, M, n_rows, lda, F, sqrt_mu):
         return self.fls.fls_solve(self.ctx, M, n_rows, lda, F, sqrt_mu)
 
+    def solve_stacked(self, S, n_blocks, kb, lds, F, sqrt_mu):
+        return self.fls.fls_solve_stacked(self.ctx, S, n_blocks, kb, lds, F, sqrt_mu)
+
     # peer-memory transport (CUDA IPC over NVLink / NVSwitch)
     def qr_r_into(self, Ab, n_rows, lda, ncols, dst_ptr, ldr):
         self.fls.fls_qr_r(self.ctx, Ab, n_rows, lda, ncols, ldr=ldr, R_ptr=dst_ptr)
@@ -66,19 +70,17 @@ class _FlsOps:
 
 
 def _combine(ops, Rs, ks, F, sqrt_mu, dev):
-    """root step of TSQR: stack the (F+1) x k_r upper-trapezoidal factors, append the ridge rows,
-    QR + trsv (fls_solve)"""
+    """root step of TSQR: stack the (F+1) x k_r upper-trapezoidal factors in blocks of kmax rows
+    and solve the stack with its ridge rows (fls_solve_stacked exploits the triangles)"""
     nc = F + 1
-    K = sum(ks)
-    ldm = K + (F if sqrt_mu > 0.0 else 0)
-    ldm = ((ldm + 3) // 4) * 4
-    M = torch.zeros((nc * ldm,), dtype=torch.float64, device=dev)
-    Mv = M.view(nc, ldm)
-    off = 0
-    for R, k in zip(Rs, ks):
-        Mv[:, off:off + k] = R[:, :k]
-        off += k
-    return ops.solve(M, K, ldm, F, sqrt_mu)
+    kmax = max(ks)
+    P = len(Rs)
+    lds = ((P * kmax + 3) // 4) * 4
+    S = torch.zeros((nc * lds,), dtype=torch.float64, device=dev)
+    Sv = S.view(nc, lds)
+    for r, (R, k) in enumerate(zip(Rs, ks)):
+        Sv[:, r * kmax:r * kmax + k] = R[:, :k]
+    return ops.solve_stacked(S, P, kmax, lds, F, sqrt_mu)
 
 
 def tsqr_local(blocks, F: int, *, ridge_rel: float = 0.0, ctx=None, ops=None):
@@ -114,7 +116,7 @@ def _tsqr_p2p(ops, Ab, n_local, lda, F, sqrt_mu, group, root, world, rank, dev, 
     dist.all_gather(all_k, ks, group=group)
     kmax = max(int(t.item()) for t in all_k)
     K = world * kmax
-    ldm = ((K + (F if sqrt_mu > 0.0 else 0) + 3) // 4) * 4
+    ldm = ((K + 3) // 4) * 4
     S = None
     obj = [None]
     if rank == root:
@@ -150,7 +152,7 @@ def _tsqr_p2p(ops, Ab, n_local, lda, F, sqrt_mu, group, root, world, rank, dev, 
     beta = torch.empty((F,), dtype=torch.float64, device=cdev)
     res = 0.0
     if rank == root:
-        b_root, res = ops.solve(S, K, ldm, F, sqrt_mu)
+        b_root, res = ops.solve_stacked(S, world, kmax, ldm, F, sqrt_mu)
         beta.copy_(b_root)
     dist.broadcast(beta, src=root, group=group)
     return beta.to(dev), res

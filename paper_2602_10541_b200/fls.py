@@ -25,7 +25,7 @@ from ._abi import FLS_COL_MAJOR, FLS_ROW_MAJOR, FlsError, check
 Term = Tuple[Sequence[int], float, int]   # (alpha, coef, field)
 
 __all__ = ["Context", "Block", "fls_features", "fls_assemble", "fls_features_assemble", "fls_solve", "fls_qr_r",
-           "fls_frob2", "fls_geqrf", "fls_eval", "fls_eval_block", "fls_ipc_handle", "fls_ipc_open",
+           "fls_frob2", "fls_geqrf", "fls_solve_stacked", "fls_eval", "fls_eval_block", "fls_ipc_handle", "fls_ipc_open",
            "fls_ipc_close", "fls_sync", "fls_ctx_timing", "fls_ctx_timing_read",
            "fls_assemble_host", "HostBlockSet", "BlockSet", "fls_features_blocks", "QRFactor",
            "make_nonlinearity", "fls_nl_residual", "fls_axpy", "fls_features_transform",
@@ -457,6 +457,19 @@ def fls_solve(ctx: Context, Ab: torch.Tensor, n_rows: int, lda: int, n_features:
     res = C.c_double(0.0)
     check(_abi.load().fls_solve(ctx.handle, _ptr(Ab), int(n_rows), int(lda), int(n_features),
                                 float(sqrt_mu), _ptr(beta), C.byref(res)))
+    return beta, res.value
+
+
+def fls_solve_stacked(ctx: Context, S: torch.Tensor, n_blocks: int, kb: int, lds: int,
+                      n_features: int, sqrt_mu: float = 0.0, beta: Optional[torch.Tensor] = None):
+    """TSQR root step: beta of the stacked triangular factors [R_r | c_r] (block r at rows
+    [r kb, (r+1) kb) of the flat column-major S), structure-exploiting; S is not modified."""
+    _dev_f64(S, "S")
+    if beta is None:
+        beta = torch.empty((n_features,), dtype=torch.float64, device=S.device)
+    res = C.c_double(0.0)
+    check(_abi.load().fls_solve_stacked(ctx.handle, _ptr(S), int(n_blocks), int(kb), int(lds),
+                                        int(n_features), float(sqrt_mu), _ptr(beta), C.byref(res)))
     return beta, res.value
 
 

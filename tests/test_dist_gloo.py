@@ -36,6 +36,13 @@ class NumpyOps:
         res = abs(R[F, F]) if R.shape[0] > F else 0.0
         return torch.from_numpy(beta), float(res)
 
+    def solve_stacked(self, S, n_blocks, kb, lds, F, sqrt_mu):
+        # the stack in block order is a plain [A | b] of n_blocks * kb rows
+        M = torch.zeros((F + 1) * (n_blocks * kb + F), dtype=torch.float64)
+        ld = n_blocks * kb + F
+        M.view(F + 1, ld)[:, :n_blocks * kb] = S[: (F + 1) * lds].view(F + 1, lds)[:, :n_blocks * kb]
+        return self.solve(M, n_blocks * kb, ld, F, sqrt_mu)
+
 
 def _free_port():
     s = socket.socket()

@@ -124,3 +124,29 @@ def test_solve_parity_with_oracle_on_both_qr_paths(ctx, name, size):
     beta_o, _, _ = oracle.lstsq(Ao, ro, ridge_rel=p.ridge_rel)
     u_orc = oracle.evaluate(W, b, beta_o, Xt)
     assert np.linalg.norm(u_gpu - u_orc) / np.linalg.norm(u_orc) <= U_TOL
+
+
+@pytest.mark.parametrize("P,kb,n,ridge", [(4, 301, 300, 0.0), (8, 301, 300, 1e-3), (3, 150, 300, 1e-2),
+                                          (2, 1101, 1100, 0.0), (5, 1101, 1100, 1e-4)])
+def test_solve_stacked_matches_dense_solve(ctx, P, kb, n, ridge):
+    """fls_solve_stacked (row-permuted stack, panels stopped where the triangles end) == fls_solve
+    on the same stack in block order: beta and |R(F, F)| (full column rank inputs)"""
+    F = n - 1
+    g = torch.Generator(device="cuda").manual_seed(P * 1000 + kb)
+    lds = P * kb
+    S = torch.zeros(((F + 1) * lds,), dtype=torch.float64, device="cuda")
+    Sv = S.view(F + 1, lds)
+    for r in range(P):
+        k = min(kb, F + 1)
+        B = torch.randn((k, F + 1), dtype=torch.float64, device="cuda", generator=g)
+        Sv[:, r * kb:r * kb + k] = torch.triu(B).T        # upper-trapezoidal factor of block r
+    fro = float(torch.linalg.norm(Sv[:F, :]))
+    sq = ridge * fro
+    beta_s, res_s = fls.fls_solve_stacked(ctx, S, P, kb, lds, F, sq)
+    ld = ((lds + F + 3) // 4) * 4
+    M = torch.zeros(((F + 1) * ld,), dtype=torch.float64, device="cuda")
+    M.view(F + 1, ld)[:, :lds] = Sv
+    beta_d, res_d = fls.fls_solve(ctx, M, lds, ld, F, sq)
+    assert float(torch.linalg.norm(beta_s - beta_d) / torch.linalg.norm(beta_d)) <= 1e-10
+    assert abs(res_s - res_d) <= 1e-10 * max(res_d, 1e-300)
+    assert torch.equal(Sv[:, :1], S.view(F + 1, lds)[:, :1])   # S not modified (spot check)
