@@ -798,7 +798,10 @@ fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int6
     cudaError_t e = launch_ridge_fill(Ab, lda, n_rows, n_features, n_features + 1, sqrt_mu, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "ridge_fill");
   }
-  return qr_trsv(ctx, Ab, m, lda, n_features, beta, resid_norm, 0, 0);
+  // the ridge rows [sqrt_mu I | 0] below row n_rows: ridge row i is zero left of column i, so
+  // the blocked QR can stop each panel where the ridge rows still are (grouped mode, G = 1)
+  return qr_trsv(ctx, Ab, m, lda, n_features, beta, resid_norm, sqrt_mu > 0.0 ? n_rows : 0,
+                 sqrt_mu > 0.0 ? 1 : 0);
 }
 
 }  // extern "C"
