@@ -917,7 +917,10 @@ fls_status fls_qr_factor(fls_ctx *ctx, const double *A, int64_t n_rows, int64_t 
     fls_qr_destroy(q);
     return cuda_fail(e, "fls_qr_factor copy");
   }
-  if (fls_status s = geqrf_inplace(ctx, q->M, m, q->ld, n_features, q->tau)) {
+  // grouped mode for the ridge rows (zero left of their column); the stored reflectors are
+  // zero wherever a panel stopped, so ormqr applies them unchanged
+  if (fls_status s = geqrf_inplace(ctx, q->M, m, q->ld, n_features, q->tau,
+                                   sqrt_mu > 0.0 ? n_rows : 0, sqrt_mu > 0.0 ? 1 : 0)) {
     fls_qr_destroy(q);
     return s;
   }

@@ -150,3 +150,20 @@ def test_solve_stacked_matches_dense_solve(ctx, P, kb, n, ridge):
     assert float(torch.linalg.norm(beta_s - beta_d) / torch.linalg.norm(beta_d)) <= 1e-10
     assert abs(res_s - res_d) <= 1e-10 * max(res_d, 1e-300)
     assert torch.equal(Sv[:, :1], S.view(F + 1, lds)[:, :1])   # S not modified (spot check)
+
+
+@pytest.mark.parametrize("m,n,ridge", [(3000, 700, 1e-3), (5000, 1100, 1e-4), (2500, 1100, 0.0)])
+def test_cached_qr_with_ridge_matches_stacked_lstsq(ctx, m, n, ridge):
+    """fls_qr_factor + fls_qr_solve (ormqr on the stored reflectors, grouped mode for the ridge
+    rows on the blocked path) == LAPACK lstsq of [A; sqrt_mu I] for several right-hand sides"""
+    g = torch.Generator(device="cuda").manual_seed(m + n)
+    A = torch.randn((m, n), dtype=torch.float64, device="cuda", generator=g)
+    B = torch.randn((m, 3), dtype=torch.float64, device="cuda", generator=g)
+    sq = ridge * float(torch.linalg.norm(A))
+    qr = fls.QRFactor(ctx, A.T.contiguous().view(-1), m, m, n, sq)
+    Beta = qr.solve(B.T.contiguous().view(-1), m)                      # (3, n)
+    qr.close()
+    As = torch.cat([A, sq * torch.eye(n, dtype=torch.float64, device="cuda")]).cpu()
+    Bs = torch.cat([B, torch.zeros((n, 3), dtype=torch.float64, device="cuda")]).cpu()
+    ref = torch.linalg.lstsq(As, Bs).solution.T.cuda()
+    assert float(torch.linalg.norm(Beta - ref) / torch.linalg.norm(ref)) <= 1e-9
