@@ -1,5 +1,6 @@
+"""fls_solve on the full C1 system, 6 calls (first-call vs steady-state latency)."""
 import sys, time, torch
-sys.path.insert(0, ".")
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 import workloads as wl
 from paper_2602_10541_b200 import fls
 p = wl.make_problem("c1_poisson1d", "full")

@@ -1,5 +1,7 @@
+"""Run-to-run variance of one blocked QR (C4 shape, 10 calls) and per-kernel duration spread
+(torch.profiler): python tools/qr_variance.py"""
 import sys, os, json, torch
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2602_10541_b200 import fls
 from torch.profiler import profile, ProfilerActivity
 m, n = 65000, 8001
