@@ -1369,6 +1369,7 @@ static fls_status eval_common(fls_ctx *ctx, const double *W, const double *b, in
   ea.nf = n_fields;
   ea.G = pl.G;
   for (int q = 0; q < pl.G; ++q) ea.gfield[q] = pl.gfield[q];
+  ea.sin_only = pl.pmode == PM_SIN ? 1 : 0;   // all orders even (e.g. u_N itself)
   e = launch_eval(dim, ea, ctx->stream);
   if (e != cudaSuccess) return cuda_fail(e, "eval_kernel");
   return FLS_OK;

@@ -95,6 +95,7 @@ struct EvalArgs {
   int32_t nf;
   int32_t G;                      // field groups (0: constant coefficients)
   int32_t gfield[FLS_MAX_FIELDS]; // field id of group g+1
+  int32_t sin_only;               // every term of even order: Pc = 0, skip the cos polynomial
 };
 
 // layout helper shared by host and kernels

@@ -270,12 +270,13 @@ cudaError_t launch_prefactor_batch(const PrefBatch &b, int64_t F, cudaStream_t s
 // coefficient fields (fls_eval_block): Ps = Ps_0 + sum_g c_g(x_i) Ps_g, likewise Pc.
 // One warp per 4 rows; lanes stride over features; fixed-order warp reduction.
 // ------------------------------------------------------------------------------------------
-template <int D>
+// SINONLY: every term has even order (Pc = 0): no cos; NF: field groups handled (0 or FLS_MAX_FIELDS)
+template <int D, bool SINONLY, int NF>
 __global__ void __launch_bounds__(256) eval_kernel(const EvalArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r0 = ((int64_t)blockIdx.x * 8 + warp) * 4;
   double x[4][D];
-  double cf[4][FLS_MAX_FIELDS];  // per-row coefficient of group g+1
+  double cf[4][NF > 0 ? NF : 1];  // per-row coefficient of group g+1
   bool bad = false;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(256) eval_kernel(const EvalArgs a) {
       bad |= !finite(x[q][k]);
     }
 #pragma unroll
-    for (int g = 0; g < FLS_MAX_FIELDS; ++g) {
+    for (int g = 0; g < NF; ++g) {
       cf[q][g] = (g < a.G && r < a.n) ? a.fields[r * a.nf + a.gfield[g]] : 0.0;
       bad |= !finite(cf[q][g]);
     }
@@ -298,9 +299,9 @@ __global__ void __launch_bounds__(256) eval_kernel(const EvalArgs a) {
 #pragma unroll
     for (int k = 0; k < D; ++k) w[k] = p[k];
     const double bp = p[D], ps0 = p[D + 1], pc0 = p[D + 2];
-    double psg[FLS_MAX_FIELDS], pcg[FLS_MAX_FIELDS];
+    double psg[NF > 0 ? NF : 1], pcg[NF > 0 ? NF : 1];
 #pragma unroll
-    for (int g = 0; g < FLS_MAX_FIELDS; ++g) {
+    for (int g = 0; g < NF; ++g) {
       psg[g] = g < a.G ? p[D + 3 + 2 * g] : 0.0;
       pcg[g] = g < a.G ? p[D + 4 + 2 * g] : 0.0;
     }
@@ -313,10 +314,10 @@ __global__ void __launch_bounds__(256) eval_kernel(const EvalArgs a) {
       int sgn;
       const double f = halfturn(h, sgn);
       const double u = f * f;
-      const double s = sinpi_core(f, u), c = cospi_core(u);
+      const double s = sinpi_core(f, u), c = SINONLY ? 0.0 : cospi_core(u);
       double ps = ps0, pc = pc0;
 #pragma unroll
-      for (int g = 0; g < FLS_MAX_FIELDS; ++g) {
+      for (int g = 0; g < NF; ++g) {
         if (g < a.G) {
           ps = fma(cf[q][g], psg[g], ps);
           pc = fma(cf[q][g], pcg[g], pc);
@@ -341,8 +342,12 @@ __global__ void __launch_bounds__(256) eval_kernel(const EvalArgs a) {
 cudaError_t launch_eval(int D, const EvalArgs &a, cudaStream_t st) {
   const unsigned nb = (unsigned)((a.n + 31) / 32);
   switch (D) {
-#define FLS_EV(d) \
-  case d: eval_kernel<d><<<nb, 256, 0, st>>>(a); break;
+#define FLS_EV(d)                                                                       \
+  case d:                                                                               \
+    if (a.G > 0) eval_kernel<d, false, FLS_MAX_FIELDS><<<nb, 256, 0, st>>>(a);          \
+    else if (a.sin_only) eval_kernel<d, true, 0><<<nb, 256, 0, st>>>(a);                \
+    else eval_kernel<d, false, 0><<<nb, 256, 0, st>>>(a);                               \
+    break;
     FLS_EV(1) FLS_EV(2) FLS_EV(3) FLS_EV(4) FLS_EV(5) FLS_EV(6) FLS_EV(7) FLS_EV(8)
 #undef FLS_EV
     default: return cudaErrorInvalidValue;
