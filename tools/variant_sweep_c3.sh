@@ -10,6 +10,8 @@ VARIANTS=(
   "c3p1m4|-D FLS_PAIRS=1 -D FLS_MINB5=4"
   "c3p1m5|-D FLS_PAIRS=1 -D FLS_MINB5=5"
   "c3f1m4|-D FLS_FUNROLL=1 -D FLS_MINB5=4"
+  "c3f4m2|-D FLS_FUNROLL=4 -D FLS_MINB5=2"
+  "c3f4m3|-D FLS_FUNROLL=4 -D FLS_MINB5=3"
 )
 if [ "$1" = build ]; then
   for v in "${VARIANTS[@]}"; do
