@@ -1,0 +1,76 @@
+"""Command line: solve one of the BASELINE configurations end to end on cuda:0 (Algorithm 1,
+P:L130-143) and report the phase times and the error against the manufactured solution.
+
+    python -m paper_2602_10541_b200 c2_poisson2d [--size mini|full] [--features N] [--sigma S]
+
+Phases: features + assembly (fls_features_assemble), least squares (blocked Householder QR;
+C5 with its tau = 1e-10 relative ridge, reading A16), evaluation at 10,000 held-out
+points (fls_eval).  C5 has no boundary rows, so its u* error is not meaningful (reading A12).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def main(argv=None) -> int:
+    import numpy as np
+    import torch
+
+    import workloads as wl
+    from paper_2602_10541_b200 import fls
+
+    ap = argparse.ArgumentParser(prog="python -m paper_2602_10541_b200")
+    ap.add_argument("config", choices=wl.CONFIG_NAMES)
+    ap.add_argument("--size", choices=["mini", "full"], default="full")
+    ap.add_argument("--features", type=int, default=None, help="override the feature count N")
+    ap.add_argument("--sigma", type=float, default=None, help="override the bandwidth sigma")
+    ap.add_argument("--repeat", type=int, default=2, help="runs; the last one's times are reported")
+    args = ap.parse_args(argv)
+
+    kw = {"n_features": args.features} if args.features else {}
+    if args.config == "c5_biharm3d" and args.size == "full":
+        kw["n_int"] = 262_144                  # the solve subset of config 5 (J:configs[5])
+    p = wl.make_problem(args.config, args.size, **kw)
+    sigma = args.sigma if args.sigma else p.sigma
+    F, R, d = p.n_features, p.n_rows, p.dim
+    ctx = fls.Context()
+    blocks = [fls.Block(torch.from_numpy(b.X).cuda(), b.terms, b.weight, torch.from_numpy(b.values).cuda(),
+                        torch.from_numpy(b.fields).cuda() if b.fields is not None else None)
+              for b in p.blocks]
+    Xt = torch.from_numpy(p.test_points()).cuda()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    extra = F if p.ridge_rel > 0 else 0
+    for _ in range(max(1, args.repeat)):       # the last run is reported (the first loads kernels)
+        torch.cuda.synchronize()
+        ev[0].record()
+        W, b, Ab, lda = fls.fls_features_assemble(ctx, d, F, sigma, p.seed, blocks, extra_rows=extra)
+        ev[1].record()
+        sq = p.ridge_rel * math.sqrt(fls.fls_frob2(ctx, Ab, R, lda, F)) if p.ridge_rel > 0 else 0.0
+        beta, res = fls.fls_solve(ctx, Ab, R, lda, F, sq)
+        ev[2].record()
+        u = fls.fls_eval(ctx, W, b, beta, Xt)
+        ev[3].record()
+        torch.cuda.synchronize()
+        del Ab
+    us = p.u_star(Xt.cpu().numpy())
+    uh = u.cpu().numpy()
+    out = {"config": p.name, "rows": R, "features": F, "sigma": sigma,
+           "assemble_ms": ev[0].elapsed_time(ev[1]), "solve_ms": ev[1].elapsed_time(ev[2]),
+           "eval_ms": ev[2].elapsed_time(ev[3]), "residual_norm": res,
+           "rel_l2_vs_u_star": float(np.linalg.norm(uh - us) / np.linalg.norm(us))
+           if p.name != "c5_biharm3d" else None}
+    print(json.dumps(out, indent=1))
+    ctx.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -40,3 +40,16 @@ def test_bench_line_contract_small():
     assert j["e2e"]["value"] > 0 and j["e2e"]["d2h_bytes_per_step"] > 0
     assert j["solve"]["ms"] > 0
     assert "sm_mhz" in j["clocks"] and "reasons" in j["clocks"]
+
+
+def test_cli_solves_a_config():
+    """python -m paper_2602_10541_b200 <config>: Algorithm 1 end to end, u* recovered"""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    r = subprocess.run([sys.executable, "-m", "paper_2602_10541_b200", "c1_poisson1d"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = json.loads(r.stdout)
+    assert out["rows"] == 1002 and out["features"] == 500
+    assert out["rel_l2_vs_u_star"] < 1e-6 and out["solve_ms"] > 0
