@@ -2,6 +2,8 @@
 fls_qr_r) against the mathematics: Q R = A and Q^T Q = I to rounding, |diag R| equal to
 cuSOLVER geqrf's (torch.geqrf) on full-rank inputs, tau = 0 for an already-zero column, and the
 LAPACK storage format (torch.linalg.householder_product rebuilds Q from it)."""
+import math
+
 import pytest
 import torch
 
@@ -127,7 +129,8 @@ def test_solve_parity_with_oracle_on_both_qr_paths(ctx, name, size):
 
 
 @pytest.mark.parametrize("P,kb,n,ridge", [(4, 301, 300, 0.0), (8, 301, 300, 1e-3), (3, 150, 300, 1e-2),
-                                          (2, 1101, 1100, 0.0), (5, 1101, 1100, 1e-4)])
+                                          (2, 1101, 1100, 0.0), (5, 1101, 1100, 1e-4),
+                                          (1, 1101, 1100, 0.0), (1, 1101, 1100, 1e-3)])
 def test_solve_stacked_matches_dense_solve(ctx, P, kb, n, ridge):
     """fls_solve_stacked (row-permuted stack, panels stopped where the triangles end) == fls_solve
     on the same stack in block order: beta and |R(F, F)| (full column rank inputs)"""
@@ -139,6 +142,7 @@ def test_solve_stacked_matches_dense_solve(ctx, P, kb, n, ridge):
     for r in range(P):
         k = min(kb, F + 1)
         B = torch.randn((k, F + 1), dtype=torch.float64, device="cuda", generator=g)
+        B.diagonal().add_(4.0 * math.sqrt(F))      # well conditioned: random triangles are not
         Sv[:, r * kb:r * kb + k] = torch.triu(B).T        # upper-trapezoidal factor of block r
     fro = float(torch.linalg.norm(Sv[:F, :]))
     sq = ridge * fro
