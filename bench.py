@@ -438,11 +438,13 @@ def main():
     launches_per_step_fixed = 1 if len(blocks) <= 4 else 1 + (len(blocks) + 3) // 4
 
     def step():
+        torch.cuda.nvtx.range_push("fls step")   # NVTX: one range per step for nsys timelines
         if row_major:
             fls.fls_features_assemble(ctx, d, F, p.sigma, p.seed, bset, W=W, b=b, A=Ab, lda=lda,
                                       layout=fls.FLS_ROW_MAJOR, rhs=rhs)
         else:
             fls.fls_features_assemble(ctx, d, F, p.sigma, p.seed, bset, W=W, b=b, A=Ab, lda=lda)
+        torch.cuda.nvtx.range_pop()
 
     for _ in range(args.warmup):
         step()
