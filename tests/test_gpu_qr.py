@@ -171,3 +171,21 @@ def test_cached_qr_with_ridge_matches_stacked_lstsq(ctx, m, n, ridge):
     Bs = torch.cat([B, torch.zeros((n, 3), dtype=torch.float64, device="cuda")]).cpu()
     ref = torch.linalg.lstsq(As, Bs).solution.T.cuda()
     assert float(torch.linalg.norm(Beta - ref) / torch.linalg.norm(ref)) <= 1e-9
+
+
+def test_solve_zero_column_is_erank(ctx):
+    """an exactly zero column gives an exactly zero diagonal of R: fls_solve reports FLS_ERANK
+    (mu = 0) on either QR path, and solves with a ridge"""
+    m, n = 2000, 1100
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.randn((m, n), dtype=torch.float64, device="cuda", generator=g)
+    A[:, 17] = 0.0
+    ld = ((m + n + 3) // 4) * 4
+    M = torch.zeros(((n + 1) * ld,), dtype=torch.float64, device="cuda")
+    M.view(n + 1, ld)[:n, :m] = A.T
+    M.view(n + 1, ld)[n, :m] = torch.randn(m, dtype=torch.float64, device="cuda", generator=g)
+    M2 = M.clone()
+    with pytest.raises(fls.FlsError, match="ERANK"):
+        fls.fls_solve(ctx, M, m, ld, n, 0.0)
+    beta, _ = fls.fls_solve(ctx, M2, m, ld, n, 1e-6)
+    assert bool(torch.isfinite(beta).all()) and abs(float(beta[17])) <= 1e-6 * float(beta.abs().max())
