@@ -112,8 +112,17 @@ __global__ void __launch_bounds__(kQrNT) qr_leaf_kernel(const QrLeafArgs a) {
   const int64_t r_lo = (int64_t)blockIdx.x * rc;
   const int nr = (int)(r_lo >= a.m ? 0 : (a.m - r_lo < rc ? a.m - r_lo : rc));
   const int b = a.b;
-  for (int q = 0; q < b; ++q)
-    for (int r = threadIdx.x; r < nr; r += kQrNT) slab[q * rc + r] = a.A[(int64_t)q * a.lda + r_lo + r];
+  // all b loads of a row in flight before the first shared-memory store (one memory round trip
+  // per row instead of one per column)
+  for (int r = threadIdx.x; r < nr; r += kQrNT) {
+    double v[kQrB];
+#pragma unroll
+    for (int q = 0; q < kQrB; ++q)
+      if (q < b) v[q] = a.A[(int64_t)q * a.lda + r_lo + r];
+#pragma unroll
+    for (int q = 0; q < kQrB; ++q)
+      if (q < b) slab[q * rc + r] = v[q];
+  }
   __syncthreads();
   double acc[kQrB];
   {  // partial sums of column 0 over my rows below the diagonal
