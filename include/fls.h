@@ -34,7 +34,8 @@
  *     prefactors, O(n_blocks * n_features * (dim + 6)) doubles), grown on demand.
  *   - Streams: work is enqueued on the stream borrowed at fls_ctx_create (0 = legacy default
  *     stream).  fls_features / fls_assemble / fls_eval are ASYNCHRONOUS; fls_solve and
- *     fls_sync are blocking.
+ *     fls_sync are blocking.  A ctx is not thread-safe: use one ctx per host thread (or
+ *     serialise calls); several ctx may share a device and a stream.
  *   - Errors: every call returns fls_status.  Argument errors (FLS_EINVAL) are detected on
  *     the host before anything is enqueued.  Non-finite inputs (W, b, X, values, coefficient
  *     fields) are detected by the kernels themselves and reported asynchronously: the next
@@ -93,7 +94,9 @@ typedef struct fls_ctx fls_ctx;
 FLS_API fls_status fls_ctx_create(int device, void *cuda_stream, fls_ctx **out);
 /* frees the ctx workspace and library handles; NULL is a no-op. */
 FLS_API fls_status fls_ctx_destroy(fls_ctx *ctx);
-/* re-point the ctx at another stream (borrowed). */
+/* re-point the ctx at another stream (borrowed).  Work already enqueued on the old stream is
+ * ordered before anything later enqueued on the new one (an event wait, no host sync), so the
+ * ctx's workspace is never used by both streams at once.  Errors: FLS_EINVAL, FLS_ECUDA. */
 FLS_API fls_status fls_ctx_set_stream(fls_ctx *ctx, void *cuda_stream);
 /* block until the ctx stream is idle; returns FLS_ENONFINITE (and clears the flag) if a
  * kernel saw a non-finite input since the last check, FLS_ECUDA on an asynchronous fault. */

@@ -40,6 +40,7 @@ struct fls_ctx {
   // host-buffer path (fls_assemble_host): copy stream, events, device staging
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t hev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t switch_ev = nullptr;  // fls_ctx_set_stream ordering
   double *hin = nullptr, *hout = nullptr;
   size_t hin_bytes = 0, hout_bytes = 0;
 };
@@ -213,6 +214,7 @@ fls_status fls_ctx_destroy(fls_ctx *ctx) {
   for (cudaEvent_t ev : ctx->ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : ctx->hev)
     if (ev) cudaEventDestroy(ev);
+  if (ctx->switch_ev) cudaEventDestroy(ctx->switch_ev);
   if (ctx->copy_stream) {
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamDestroy(ctx->copy_stream);
@@ -231,7 +233,14 @@ fls_status fls_ctx_destroy(fls_ctx *ctx) {
 
 fls_status fls_ctx_set_stream(fls_ctx *ctx, void *cuda_stream) {
   if (fls_status s = check_ctx(ctx)) return s;
-  ctx->stream = (cudaStream_t)cuda_stream;
+  const cudaStream_t next = (cudaStream_t)cuda_stream;
+  if (next != ctx->stream) {  // the new stream waits for the old one's pending work
+    DeviceGuard g(ctx->device);
+    if (!ctx->switch_ev) FLS_CUDA(cudaEventCreateWithFlags(&ctx->switch_ev, cudaEventDisableTiming));
+    FLS_CUDA(cudaEventRecord(ctx->switch_ev, ctx->stream));
+    FLS_CUDA(cudaStreamWaitEvent(next, ctx->switch_ev, 0));
+  }
+  ctx->stream = next;
   if (ctx->solver) cusolverDnSetStream(ctx->solver, ctx->stream);
   if (ctx->blas) cublasSetStream(ctx->blas, ctx->stream);
   return FLS_OK;

@@ -130,6 +130,31 @@ def test_user_stream_and_timing_hook(ctx):
     c2.close()
 
 
+def test_set_stream_orders_pending_work(ctx):
+    """fls_ctx_set_stream: work enqueued on the old stream completes before the ctx's next call
+    on the new stream runs (include/fls.h) -- here the old stream is held up by a ~50 ms spin
+    before the assembly, and fls_frob2 on the new stream must still see the assembled A"""
+    p = wl.make_problem("c4_heat2d", "mini")
+    _, _, Wd, bd = _parity_feats(p)
+    blocks = fls.BlockSet(dev_blocks(p), 3)
+    ref, lda = fls.fls_assemble(ctx, Wd, bd, blocks)
+    fls.fls_sync(ctx)
+    F = p.n_features
+    want = float((ref.reshape(-1)[:F * lda].view(F, lda)[:, :p.n_rows] ** 2).sum())
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    A = torch.zeros_like(ref)
+    torch.cuda.synchronize()
+    c2 = fls.Context(stream=s1)
+    with torch.cuda.stream(s1):
+        torch.cuda._sleep(100_000_000)             # ~50 ms at 1.9 GHz on s1 only
+    fls.fls_assemble(c2, Wd, bd, blocks, A=A, lda=lda)
+    c2.set_stream(s2)
+    got = fls.fls_frob2(c2, A, p.n_rows, lda, F)
+    torch.cuda.synchronize()
+    assert got == pytest.approx(want, rel=1e-12)
+    c2.close()
+
+
 def test_unaligned_lda_and_pointer_scalar_path(ctx):
     p = wl.make_problem("c2_poisson2d", "mini")
     _, _, Wd, bd = _parity_feats(p)
