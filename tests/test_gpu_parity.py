@@ -84,6 +84,36 @@ def test_assemble_parity_full_size_sampled_rows(ctx, name):
     assert np.array_equal(rg, ro)
 
 
+@pytest.mark.parametrize("name", ["c3_poisson5d", "c5_biharm3d"])
+def test_bench_call_full_size_vs_oracle(ctx, name):
+    """bench.py's exact call (fls_features_assemble: W, b drawn on the device from the seed,
+    full BASELINE size, the bench's lda) against the oracle given ITS OWN features
+    (oracle.features, same seed) on sampled rows: W may differ by <= 8 ulp, which moves an
+    entry by well under the A14 bound."""
+    p = wl.make_problem(name, "full")
+    F, R, d = p.n_features, p.n_rows, p.dim
+    lda = wl_round4(R)
+    need = (F + 1) * lda * 8
+    free, _ = torch.cuda.mem_get_info()
+    if need + (2 << 30) > free:
+        pytest.skip(f"needs {need / 1e9:.1f} GB, {free / 1e9:.1f} GB free")
+    Ab = torch.empty(((F + 1) * lda,), dtype=torch.float64, device="cuda")
+    W = torch.empty((F, d), dtype=torch.float64, device="cuda")
+    b = torch.empty((F,), dtype=torch.float64, device="cuda")
+    bset = fls.BlockSet(dev_blocks(p), d)
+    fls.fls_features_assemble(ctx, d, F, p.sigma, p.seed, bset, W=W, b=b, A=Ab, lda=lda)
+    fls.fls_sync(ctx)
+    rows = wl.sample_rows(R, 8, 256 if R > 100_000 else 61)
+    Ag, rg = rows_from_colmajor(Ab, lda, F, rows)
+    del Ab
+    torch.cuda.empty_cache()
+    Wo, bo = oracle.features(d, F, float(p.sigma), int(p.seed))
+    Ao, ro, S = oracle.assemble(Wo, bo, p.blocks, rows=rows)
+    emax, e999 = scaled_err(Ag, Ao, S)
+    assert emax <= ENTRY_TOL, (emax, e999)
+    assert np.array_equal(rg, ro)
+
+
 def wl_round4(n):
     return ((n + 3) // 4) * 4
 
