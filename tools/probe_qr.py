@@ -1,5 +1,6 @@
 """Time fls_geqrf (libfls blocked QR) vs torch.geqrf (cuSOLVER) at the solve shapes of C3, C4 and
-the C5 262,144-row subset ([A | b], ridge rows included for C5).
+the C5 262,144-row subset ([A | b], ridge rows included for C5), plus C2 and the paper's
+Newton size (7,300 x 1,501).
 
     FLS_QR_NB=256 python tools/probe_qr.py [c3 c4 c5]
 """
@@ -13,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2602_10541_b200 import fls  # noqa: E402
 
-SHAPES = {"c3": (25000, 4001), "c4": (65000, 8001), "c5": (262144 + 8192, 8193)}
+SHAPES = {"c2": (4800, 2001), "newton": (7300, 1501), "c3": (25000, 4001), "c4": (65000, 8001), "c5": (262144 + 8192, 8193)}
 
 
 def main(names):
