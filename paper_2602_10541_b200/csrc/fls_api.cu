@@ -416,6 +416,10 @@ fls_status launch_prefactors(fls_ctx *ctx, const AsmPlan &ap, const double *W, c
   return FLS_OK;
 }
 
+// largest assembly launch that gets PDL: C3 (1e8 entries) 147.8 -> 144.9 us per graph step,
+// unfused C2 27.5 -> 24.6 us; none for C4 / C5
+constexpr int64_t kPdlMaxEntries = int64_t(1) << 28;
+
 // a3-a8: assembly launches for global rows [row_begin, row_end) into local rows of A / rhs.
 // blocks[q]'s X / fields / values pointers refer to point index pt_base[q] (0 for the caller's
 // own arrays; the slice start for staged copies).  Column-major: consecutive blocks that share
@@ -423,7 +427,7 @@ fls_status launch_prefactors(fls_ctx *ctx, const AsmPlan &ap, const double *W, c
 fls_status assemble_range(fls_ctx *ctx, const AsmPlan &ap, int32_t dim, int64_t F,
                           const fls_block *blocks, const int64_t *pt_base, int64_t row_begin,
                           int64_t row_end, double *A, int64_t lda, int32_t layout, double *rhs,
-                          cudaStream_t st) {
+                          cudaStream_t st, bool pdl) {
   // vector stores need every column segment aligned: 16 B (row pairs) or 32 B (kQuad rows);
   // the row-major kernel always stores feature pairs (16 B)
   const bool quad = kQuad && layout == FLS_COL_MAJOR;
@@ -448,7 +452,13 @@ fls_status assemble_range(fls_ctx *ctx, const AsmPlan &ap, int32_t dim, int64_t 
     }
     cudaError_t e = cudaSuccess;
     if (layout == FLS_COL_MAJOR) {
-      e = launch_assemble_cm(dim, bG, bK, batch, nb, st);
+      // PDL only between kernels (a timing event recorded in between would sit in the way),
+      // and only for launches short enough that the saved launch latency shows: on C5
+      // (1.7e10 entries) it cost 0.6% (early-dispatched CTAs skew its two long waves)
+      int64_t entries = 0;
+      for (int i = 0; i < nb; ++i) entries += (batch[i].lr1 - batch[i].lr0) * F;
+      e = launch_assemble_cm(dim, bG, bK, batch, nb, st,
+                             pdl && !ctx->timing && entries <= kPdlMaxEntries);
     } else {
       for (int i = 0; i < nb && e == cudaSuccess; ++i) e = launch_assemble_rm(dim, bG, bK, batch[i], st);
     }
@@ -489,6 +499,15 @@ fls_status assemble_range(fls_ctx *ctx, const AsmPlan &ap, int32_t dim, int64_t 
     for (int i = 0; i < FLS_MAX_FIELDS; ++i) aa.gfield[i] = pl.gfield[i];
   }
   return flush();
+}
+
+// programmatic dependent launch of the assembly after its prefactor launch (FLS_PDL=0: off)
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *v = getenv("FLS_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
 }
 
 fls_status ensure_dev(double *&p, size_t &cap, size_t bytes, cudaStream_t st) {
@@ -571,7 +590,7 @@ fls_status fls_features_assemble(fls_ctx *ctx, int32_t dim, int64_t n_features, 
   }
   if (row_end == row_begin) return FLS_OK;
   return assemble_range(ctx, ap, dim, F, blocks, nullptr, row_begin, row_end, A, lda, layout, rhs,
-                        ctx->stream);
+                        ctx->stream, pdl_enabled());
 }
 
 fls_status fls_assemble(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
@@ -589,7 +608,7 @@ fls_status fls_assemble(fls_ctx *ctx, const double *W, const double *b, int32_t 
                                        row_begin, row_end, ctx->stream))
     return s;
   return assemble_range(ctx, ap, dim, n_features, blocks, nullptr, row_begin, row_end, A, lda,
-                        layout, rhs, ctx->stream);
+                        layout, rhs, ctx->stream, pdl_enabled());
 }
 
 fls_status fls_assemble_host(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
@@ -671,7 +690,7 @@ fls_status fls_assemble_host(fls_ctx *ctx, const double *W, const double *b, int
     const int64_t r0 = row_begin + c * chunk_rows, r1 = std::min(row_end, r0 + chunk_rows);
     if (c >= 2) FLS_CUDA(cudaStreamWaitEvent(cs, ctx->hev[2 + slot], 0));  // buffer drained
     if (fls_status s = assemble_range(ctx, ap, dim, F, dblk, base, r0, r1, buf, ldc, FLS_COL_MAJOR,
-                                      rhs ? buf + F * ldc : nullptr, cs))
+                                      rhs ? buf + F * ldc : nullptr, cs, false))
       return s;
     FLS_CUDA(cudaEventRecord(ctx->hev[slot], cs));
     FLS_CUDA(cudaStreamWaitEvent(xs, ctx->hev[slot], 0));

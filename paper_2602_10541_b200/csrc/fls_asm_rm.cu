@@ -129,12 +129,13 @@ cudaError_t launch_assemble_rm(int D, int G, int kmode, const AsmArgs &a, cudaSt
 #undef FLS_RM_G
 }
 
-cudaError_t launch_assemble_cm_sin(int D, int G, AsmArgs *blks, int n, cudaStream_t st);
-cudaError_t launch_assemble_cm_sincos(int D, int G, AsmArgs *blks, int n, cudaStream_t st);
+cudaError_t launch_assemble_cm_sin(int D, int G, AsmArgs *blks, int n, cudaStream_t st, bool pdl);
+cudaError_t launch_assemble_cm_sincos(int D, int G, AsmArgs *blks, int n, cudaStream_t st, bool pdl);
 
-cudaError_t launch_assemble_cm(int D, int G, int kmode, AsmArgs *blks, int n, cudaStream_t st) {
-  return kmode == KM_SIN ? launch_assemble_cm_sin(D, G, blks, n, st)
-                         : launch_assemble_cm_sincos(D, G, blks, n, st);
+cudaError_t launch_assemble_cm(int D, int G, int kmode, AsmArgs *blks, int n, cudaStream_t st,
+                               bool pdl) {
+  return kmode == KM_SIN ? launch_assemble_cm_sin(D, G, blks, n, st, pdl)
+                         : launch_assemble_cm_sincos(D, G, blks, n, st, pdl);
 }
 
 }  // namespace fls

@@ -5,7 +5,7 @@
 namespace fls {
 
 template <int D, int G>
-static cudaError_t go_sin(AsmArgs *blks, int n, cudaStream_t st) {
+static cudaError_t go_sin(AsmArgs *blks, int n, cudaStream_t st, bool pdl) {
   constexpr int S = pf_stride(D, G, KM_SIN);
   const size_t smem = (size_t)kFC * S * sizeof(double);
   AsmBatch bt;
@@ -25,18 +25,17 @@ static cudaError_t go_sin(AsmArgs *blks, int n, cudaStream_t st) {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  assemble_cm_kernel<D, G, KM_SIN><<<(unsigned)total, kNT, smem, st>>>(bt);
-  return cudaGetLastError();
+  return asm_launch(assemble_cm_kernel<D, G, KM_SIN>, (unsigned)total, smem, st, pdl, bt);
 }
 
-cudaError_t launch_assemble_cm_sin(int D, int G, AsmArgs *blks, int n, cudaStream_t st) {
+cudaError_t launch_assemble_cm_sin(int D, int G, AsmArgs *blks, int n, cudaStream_t st, bool pdl) {
 #define FLS_G(d)                                 \
   switch (G) {                                   \
-    case 0: return go_sin<d, 0>(blks, n, st);    \
-    case 1: return go_sin<d, 1>(blks, n, st);    \
-    case 2: return go_sin<d, 2>(blks, n, st);    \
-    case 3: return go_sin<d, 3>(blks, n, st);    \
-    case 4: return go_sin<d, 4>(blks, n, st);    \
+    case 0: return go_sin<d, 0>(blks, n, st, pdl);    \
+    case 1: return go_sin<d, 1>(blks, n, st, pdl);    \
+    case 2: return go_sin<d, 2>(blks, n, st, pdl);    \
+    case 3: return go_sin<d, 3>(blks, n, st, pdl);    \
+    case 4: return go_sin<d, 4>(blks, n, st, pdl);    \
     default: return cudaErrorInvalidValue;       \
   }
   switch (D) {

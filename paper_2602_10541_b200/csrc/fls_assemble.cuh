@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
     }
   }
   if (bad) atomicOr(a.err, 1u);
+  pdl_wait();  // the prefactor records of the preceding launch are complete from here on
 
   // this CTA's feature range [f0, f1) (a.fpc features per CTA, chosen by the launcher), walked
   // in shared-memory chunks of at most kFC records
@@ -260,6 +261,25 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
       }
     }
   }
+}
+
+// launch one batch, with the programmatic-dependent-launch attribute when the caller knows the
+// preceding operation on the stream is the prefactor launch of the same call (or an earlier
+// assembly batch of it, which writes disjoint rows)
+template <class Kern>
+inline cudaError_t asm_launch(Kern kern, unsigned ctas, size_t smem, cudaStream_t st, bool pdl,
+                              const AsmBatch &bt) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(kNT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, bt);
 }
 
 }  // namespace fls

@@ -77,6 +77,13 @@ __device__ __forceinline__ double sin_halfturns(double h) {
   return sinpi_core(flipsign(f, sgn), f * f);
 }
 
+// Programmatic dependent launch (sm_90+): the prefactor kernels let the assembly grid that
+// follows them on the stream launch at once (pdl_trigger at entry); the assembly kernel loads
+// its points, then waits for the prefactor grid's completion and memory flush (pdl_wait)
+// before reading the records.  Both are no-ops when the launch has no PDL attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ bool finite(double v) {
   // exponent field all ones <=> Inf / NaN
   return (__double2hiint(v) & 0x7ff00000) != 0x7ff00000;

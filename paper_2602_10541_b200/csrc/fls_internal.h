@@ -139,7 +139,9 @@ cudaError_t launch_prefactor_batch(const PrefBatch &b, int64_t F, cudaStream_t s
 cudaError_t launch_features_prefactor(int32_t dim, int64_t F, const FeatBlocks &fb, uint64_t seed,
                                       double *W, double *b, const PrefBatch &pb, cudaStream_t st);
 // blks: n (<= kMaxBatch) blocks of one variant; fpc is set per block by the launcher
-cudaError_t launch_assemble_cm(int D, int G, int kmode, AsmArgs *blks, int n, cudaStream_t st);
+// pdl: launch with programmatic dependent launch (only right after this call's prefactor launch)
+cudaError_t launch_assemble_cm(int D, int G, int kmode, AsmArgs *blks, int n, cudaStream_t st,
+                               bool pdl);
 cudaError_t launch_assemble_rm(int D, int G, int kmode, const AsmArgs &a, cudaStream_t st);
 cudaError_t launch_eval(int D, const EvalArgs &a, cudaStream_t st);
 cudaError_t launch_ridge_fill(double *Ab, int64_t lda, int64_t row0, int64_t F, int64_t ncols,

@@ -129,6 +129,7 @@ __global__ void prefactor_kernel(const PrefArgs a) {
 
 // all blocks of one fls_assemble call in one launch (grid.y = block)
 __global__ void prefactor_batch_kernel(const PrefBatch b) {
+  pdl_trigger();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const PrefArgs &a = b.blk[blockIdx.y];
   if (j < a.F) prefactor_one(a, j);
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(kFpFeat * FLS_MAX_DIM)
 features_prefactor_kernel(int32_t D, int64_t F, const FeatBlocks fb, uint64_t seed, double *W,
                           double *b, const PrefBatch pb) {
   __shared__ double ws[kFpFeat * FLS_MAX_DIM];
+  pdl_trigger();
   const int64_t j0 = (int64_t)blockIdx.x * kFpFeat;
   const double two_pi = 6.283185307179586476925286766559;
   const int t = threadIdx.x;
