@@ -204,7 +204,7 @@ cudaError_t launch_stack_permute(const double *S, int64_t lds, int32_t P, int64_
                                  double sqrt_mu, int64_t gq, int64_t m_total, int64_t n, double *M,
                                  int64_t ldm, cudaStream_t st);
 size_t qr_blocked_ws(int64_t m, int64_t n);  // doubles of ws (incl. nothing for tau)
-int qr_panel_width();
+int qr_panel_width(int64_t n);
 int64_t qr_blocked_max_rows();  // taller blocks use cusolverDnDgeqrf
 
 }  // namespace fls

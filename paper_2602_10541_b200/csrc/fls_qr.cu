@@ -417,16 +417,20 @@ int64_t qr_blocked_max_rows() {
   return mx;
 }
 
-int qr_panel_width() {
-  static int nb = 0;
-  if (!nb) {
-    nb = 256;
+// panel width for an n-column block: 128 up to 4,096 columns, 256 above (FLS_QR_NB sweep,
+// profiles/r01_qr_nb_sweep.jsonl: C2 15.2 -> 14.2 ms and C3 57.5 -> 56.2 ms at 128; C4 best
+// at 256, C5 flat 256-512)
+int qr_panel_width(int64_t n) {
+  static int forced = -1;
+  if (forced < 0) {
+    forced = 0;
     if (const char *s = getenv("FLS_QR_NB")) {  // tuning sweeps only
       const int v = atoi(s);
-      if (v >= kQrB) nb = (v / kQrB) * kQrB;
+      if (v >= kQrB) forced = (v / kQrB) * kQrB;
     }
   }
-  return nb;
+  if (forced) return forced;
+  return n <= 4096 ? 128 : 256;
 }
 
 static int qr_grid() {
@@ -442,7 +446,7 @@ static int qr_grid() {
 
 // workspace (doubles) qr_blocked needs for an m x n block: panel V, T, W, leaf S, partials
 size_t qr_blocked_ws(int64_t m, int64_t n) {
-  const int64_t nb = qr_panel_width();
+  const int64_t nb = qr_panel_width(n);
   const int64_t ldv = (m + 3) / 4 * 4;
   return (size_t)ldv * nb + (size_t)nb * nb + (size_t)nb * (n > nb ? n : nb) + (size_t)kQrB * kQrB +
          (size_t)2 * qr_grid() * (kQrB + 1) + 2 * (kQrB + 1) + 1;  // + barrier counter
@@ -494,7 +498,7 @@ const char *qr_blocked(cublasHandle_t h, cudaStream_t st, double *A, int64_t m, 
   *berr = CUBLAS_STATUS_SUCCESS;
   const int64_t k = m < n ? m : n;
   if (k <= 0) return nullptr;
-  const int64_t nb = qr_panel_width();
+  const int64_t nb = qr_panel_width(n);
   QrCtx q;
   q.h = h;
   q.st = st;
