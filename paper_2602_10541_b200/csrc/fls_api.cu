@@ -730,9 +730,11 @@ static fls_status ensure_handles(fls_ctx *ctx) {
 }
 
 // Householder QR of an m x n column-major block in place (R in the upper trapezoid, reflectors
-// below, geqrf format).  Default: libfls's blocked QR (fls_qr.cu) for n >= 1024 columns, one
-// cusolverDnDgeqrf call below that.  tau_out (k = min(m, n) doubles) may be NULL.
-constexpr int64_t kQrBlockedMinCols = 1024;
+// below, geqrf format).  Default: libfls's blocked QR (fls_qr.cu) for n >= 1000 columns, one
+// cusolverDnDgeqrf call below that (profiles/r01_qr_small.log: cuSOLVER 2.6 / 4.8 ms vs 3.2 /
+// 5.2 ms at 1,002 x 501 / 2,000 x 801; blocked 6.8 vs 9.1 ms at 4,000 x 1,001).
+// tau_out (k = min(m, n) doubles) may be NULL.
+constexpr int64_t kQrBlockedMinCols = 1000;
 
 // per-context solver scratch (grow-only): repeated solves (Newton, AdamW, RHS sweeps) never
 // allocate -- per-call stream-ordered allocations stalled the host sporadically
