@@ -743,3 +743,40 @@ def test_features_assemble_fused_bit_identical(ctx, name):
         assert torch.equal(Arm2[:, :F], Arm[:, :F]) and torch.equal(rrm2, rrm)
     with pytest.raises(fls.FlsError):
         fls.fls_features_assemble(ctx, d, F, -1.0, seed, base)
+
+
+def test_pdl_off_gives_identical_entries(ctx, tmp_path):
+    """FLS_PDL=0 (assembly launched without programmatic dependent launch, read once per
+    process) writes the same bits as the default PDL launch, for the fused and unfused calls"""
+    import subprocess
+    import sys
+    script = tmp_path / "asm.py"
+    script.write_text(
+        "import sys, torch\n"
+        f"sys.path.insert(0, {str(wl.__file__.rsplit('/workloads/', 1)[0])!r})\n"
+        "sys.path.insert(0, sys.argv[2])\n"
+        "import workloads as wl\n"
+        "from gpu_common import dev_blocks\n"
+        "from paper_2602_10541_b200 import fls\n"
+        "p = wl.make_problem('c3_poisson5d', 'mini')\n"
+        "ctx = fls.Context()\n"
+        "bs = fls.BlockSet(dev_blocks(p), p.dim)\n"
+        "W, b, A, lda = fls.fls_features_assemble(ctx, p.dim, p.n_features, p.sigma, p.seed, bs)\n"
+        "A2, _ = fls.fls_assemble(ctx, W, b, bs)\n"
+        "fls.fls_sync(ctx)\n"
+        "torch.save({'A': A.cpu(), 'A2': A2.cpu(), 'lda': lda}, sys.argv[1])\n")
+    import os
+    here = os.path.dirname(os.path.abspath(__file__))
+    outs = []
+    for pdl in ("1", "0"):
+        out = tmp_path / f"a{pdl}.pt"
+        env = dict(os.environ, FLS_PDL=pdl)
+        r = subprocess.run([sys.executable, str(script), str(out), here], env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(torch.load(out))
+    p = wl.make_problem("c3_poisson5d", "mini")
+    F, R, lda = p.n_features, p.n_rows, outs[0]["lda"]
+    for key in ("A", "A2"):
+        a, b = (o[key][: (F + 1) * lda].view(F + 1, lda)[:, :R] for o in outs)
+        assert torch.equal(a, b), key
