@@ -419,3 +419,77 @@ def test_zero_source_gives_zero_beta_and_mu0_is_lstsq():
     b1, r1, _ = oracle.lstsq(A, bv)
     b2, r2, _ = oracle.lstsq_mu(A, bv, 0.0)
     assert np.allclose(b1, b2, rtol=1e-13, atol=1e-13) and abs(r1 - r2) <= 1e-13 * max(r1, 1.0)
+
+
+# ------------------------------------------------------------------------------------------------
+# Alg. 1 line 2 ("Sample collocation points"): orc_sample_box / orc_sample_faces.
+# Pinned to numpy's own Philox4x64-10 (library routine of the same generator) with the uniform map
+# of DESIGN.md R1, u = (raw >> 11) 2^-53, written here independently of the oracle, plus the
+# geometric facts every sample must satisfy (face counts and order, on-face coordinates, in-box,
+# per-axis uniformity).
+# ------------------------------------------------------------------------------------------------
+def _np_uniform(seed, stream, n):
+    raw = np.random.Philox(key=seed + (stream << 64)).random_raw(n)
+    return (raw >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+
+@pytest.mark.parametrize("dim,n,seed,stream", [(1, 7, 0, 3), (2, 33, 0, 3), (3, 101, 5, 6),
+                                               (5, 64, 0, 3), (8, 9, 2 ** 40 + 3, 11)])
+def test_sample_box_matches_numpy_philox(dim, n, seed, stream):
+    """pin: X[i][k] = lo_k + (hi_k - lo_k) u(i*dim + k) -- row-major word order, the stream's
+    key word, the 53-bit uniform and the affine map, each checked bit-exactly against numpy"""
+    g = np.random.default_rng(dim * 1000 + n)
+    lo = g.uniform(-2.0, 0.5, dim)
+    hi = lo + g.uniform(0.25, 3.0, dim)
+    X = oracle.sample_box(dim, n, lo, hi, seed, stream)
+    assert X.shape == (n, dim)
+    u = _np_uniform(seed, stream, n * dim).reshape(n, dim)
+    ref = lo[None, :] + (hi - lo)[None, :] * u          # numpy: no contraction, same rounding
+    assert np.array_equal(X, ref)
+    # the transposed word order (k * n + i) is a different array: the pin would catch it
+    if n > 1 and dim > 1:
+        wrong = lo[None, :] + (hi - lo)[None, :] * u.reshape(dim, n).T
+        assert not np.array_equal(X, wrong)
+    # another stream is another array (the stream is the key's high word)
+    assert not np.array_equal(X, oracle.sample_box(dim, n, lo, hi, seed, stream + 1))
+    assert np.all(X >= lo) and np.all(X < hi)
+
+
+@pytest.mark.parametrize("dim,per_face,mask", [(2, 5, 0b11), (3, 4, 0b011), (5, 3, 0b11111),
+                                               (3, 6, 0b101), (1, 2, 0b1)])
+def test_sample_faces_matches_numpy_philox_and_geometry(dim, per_face, mask):
+    """pin: for each axis k in the mask (increasing k): per_face points on x_k = lo_k, then
+    per_face on x_k = hi_k; the other coordinates are word row*dim + l of the stream mapped to
+    [lo_l, hi_l).  Checked against numpy's Philox and the face geometry"""
+    lo = np.linspace(-1.0, 0.0, dim)
+    hi = lo + np.linspace(1.0, 2.0, dim)
+    seed, stream = 0, 4
+    X = oracle.sample_faces(dim, per_face, mask, lo, hi, seed, stream)
+    axes = [k for k in range(dim) if mask & (1 << k)]
+    rows = 2 * per_face * len(axes)
+    assert X.shape == (rows, dim)
+    u = _np_uniform(seed, stream, rows * dim).reshape(rows, dim)
+    ref = lo[None, :] + (hi - lo)[None, :] * u
+    r = 0
+    for k in axes:
+        for side, val in ((0, lo[k]), (1, hi[k])):
+            blk = X[r:r + per_face]
+            assert np.all(blk[:, k] == val), f"face {k}/{side}: coordinate not pinned to the face"
+            others = [l for l in range(dim) if l != k]
+            assert np.array_equal(blk[:, others], ref[r:r + per_face, others])
+            r += per_face
+    assert r == rows
+    assert np.all(X >= lo) and np.all(X <= hi)
+
+
+def test_sample_box_uniform_ks_per_axis():
+    """statistical pin: every axis of the box sample is U[lo_k, hi_k) (KS, p > 1e-4), and the
+    axes are uncorrelated"""
+    dim, n = 5, 20_000
+    lo = np.array([0.0, -1.0, 2.0, 0.0, -3.0])
+    hi = np.array([1.0, 1.0, 2.5, 10.0, -2.0])
+    X = oracle.sample_box(dim, n, lo, hi, 0, 3)
+    for k in range(dim):
+        assert stats.kstest(X[:, k], "uniform", args=(lo[k], hi[k] - lo[k])).pvalue > 1e-4
+    Cm = np.corrcoef(X.T)
+    assert np.max(np.abs(Cm - np.eye(dim))) < 5.0 / math.sqrt(n)
