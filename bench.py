@@ -12,6 +12,11 @@ ranks (strong scaling: the config fixes the total rows).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fls|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
+Launch contract: one rank per GPU.  Under a launcher (WORLD_SIZE set) the
+world size must equal --gpus; without one, --gpus N > 1 re-launches this script under
+torch.distributed.run with N ranks (and exits 2 if the node has fewer than N GPUs).  n_gpus in
+the JSON line is the number of distinct devices behind the ranks (checked == ranks).
+
 Timing: W warm-up steps, then K steps bracketed by barrier + cuda.synchronize, CUDA events on
 the ctx stream, max over ranks.  The output (137 GB) is >1000x L2, so every step streams past
 L2 (no flush needed).  The dominant kernel's duration comes from libfls's own event pairs
@@ -360,7 +365,409 @@ def solve_measure(args, world, rank, local):
     return out
 
 
-def main():
+# ------------------------------------------------------------------------------------------------
+# per-config block: BASELINE.json configs 1-4 on the same GPU (rank 0, N = 1)
+# ------------------------------------------------------------------------------------------------
+def per_config(names=("c1_poisson1d", "c2_poisson2d", "c3_poisson5d", "c4_heat2d"), budget_s=60.0):
+    """For each config: the fused features + assembly step captured once in a CUDA graph and
+    replayed (the launch-latency-bound C1/C2 measured without host gaps) -> steady-state
+    entries/s and fraction of the copy peak; the single-shot latency (host call -> kernels
+    done); the end-to-end solve by phase.  Bounded to about budget_s seconds."""
+    import torch
+    import workloads as wl
+    from paper_2602_10541_b200 import fls
+
+    hbm_peak, _ = _peaks()
+    out = {}
+    t_start = time.perf_counter()
+    for name in names:
+        if time.perf_counter() - t_start > budget_s:
+            out[name] = {"skipped": f"time budget of {budget_s:.0f} s spent"}
+            continue
+        p = wl.make_problem(name, "full")
+        F, R, d = p.n_features, p.n_rows, p.dim
+        ctx = fls.Context()
+        s = torch.cuda.Stream()
+        ctx.set_stream(s)
+        bset = fls.BlockSet([fls.Block(torch.from_numpy(blk.X).cuda(), blk.terms, blk.weight,
+                                       torch.from_numpy(blk.values).cuda(),
+                                       torch.from_numpy(blk.fields).cuda()
+                                       if blk.fields is not None else None)
+                             for blk in p.blocks], d)
+        lda = fls.round_up(R, 4)
+        Ab = torch.empty(((F + 1) * lda,), dtype=torch.float64, device="cuda")
+        W = torch.empty((F, d), dtype=torch.float64, device="cuda")
+        b = torch.empty((F,), dtype=torch.float64, device="cuda")
+
+        def step():
+            fls.fls_features_assemble(ctx, d, F, p.sigma, p.seed, bset, W=W, b=b, A=Ab, lda=lda)
+
+        reps = max(5, min(2000, int(2e10 / (R * F))))
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                step()
+            torch.cuda.synchronize()
+            singles = []
+            for _ in range(5):
+                t0 = time.perf_counter()
+                step()
+                torch.cuda.synchronize()
+                singles.append(1e6 * (time.perf_counter() - t0))
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                step()
+            for _ in range(3):
+                g.replay()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(s)
+            for _ in range(reps):
+                g.replay()
+            e1.record(s)
+            torch.cuda.synchronize()
+        fls.fls_sync(ctx)
+        ms = e0.elapsed_time(e1) / reps
+        del g, Ab
+        ctx.close()
+        torch.cuda.empty_cache()
+
+        class A_:
+            workload = name
+        sol = solve_measure(A_, 1, 0, 0)
+        out[name] = {"rows": R, "features": F, "entries": R * F, "reps": reps,
+                     "graph_us_per_step": 1e3 * ms, "entries_per_s": R * F / (ms / 1e3),
+                     "hbm_write_gbs": 8.0 * R * (F + 1) / (ms / 1e3) / 1e9,
+                     "frac_of_copy_peak": 8.0 * R * F / (ms / 1e3) / 1e9 / hbm_peak,
+                     "single_shot_us": statistics.median(singles),
+                     "solve_ms": {k: sol[k] for k in ("ms", "features_ms", "assemble_ms",
+                                                      "lstsq_ms", "eval_ms")},
+                     "qr_tflops": sol["qr_tflops"],
+                     "rel_l2_vs_u_star": sol.get("rel_l2_vs_u_star")}
+    return out
+
+
+# ------------------------------------------------------------------------------------------------
+# the engine: everything that touches the GPU (bench orchestration below is engine-agnostic so
+# the multi-rank contract -- spawn, one device per rank, barrier + max-over-ranks timing, one
+# JSON line -- is testable on CPU with an injected engine, tests/test_bench_cpu.py)
+# ------------------------------------------------------------------------------------------------
+class FlsEngine:
+    backend = "nccl"
+
+    @staticmethod
+    def device_count() -> int:
+        import torch
+        return torch.cuda.device_count()
+
+    def __init__(self, args, world, rank, local):
+        import torch
+        import workloads as wl
+        from paper_2602_10541_b200 import fls
+        self.torch, self.fls, self.args = torch, fls, args
+        self.world, self.rank, self.local = world, rank, local
+        torch.cuda.set_device(local)
+        kw = {"n_int": args.rows} if args.rows else {}
+        if args.scaling == "weak":
+            base_rows = args.rows or wl.FULL[args.workload]["n_int"]
+            kw["n_int"] = base_rows * world
+        p = wl.make_problem(args.workload, "full", **kw)
+        self.p = p
+        F, R, d = p.n_features, p.n_rows, p.dim
+        a, e = wl.shard_range(R, rank, world)
+        self.a, self.e, self.n_local = a, e, e - a
+        offs = p.block_offsets()
+        blocks = []
+        for blk, o in zip(p.blocks, offs):
+            lo, hi = max(a, o), min(e, o + blk.n)
+            if hi <= lo:
+                continue
+            sl = slice(lo - o, hi - o)
+            blocks.append(fls.Block(torch.from_numpy(np.ascontiguousarray(blk.X[sl])).cuda(), blk.terms,
+                                    blk.weight, torch.from_numpy(np.ascontiguousarray(blk.values[sl])).cuda(),
+                                    torch.from_numpy(np.ascontiguousarray(blk.fields[sl])).cuda()
+                                    if blk.fields is not None else None))
+        self.ctx = fls.Context(local)
+        self.bset = fls.BlockSet(blocks, d)
+        self.row_major = args.layout == "row"
+        n_local = self.n_local
+        self.lda = fls.round_up(F, 2) if self.row_major else fls.round_up(n_local, 4)
+        self.Ab = torch.empty(((n_local if self.row_major else F + 1) * self.lda,),
+                              dtype=torch.float64, device="cuda")
+        self.rhs = torch.empty((n_local,), dtype=torch.float64, device="cuda") if self.row_major else None
+        self.W = torch.empty((F, d), dtype=torch.float64, device="cuda")
+        self.b = torch.empty((F,), dtype=torch.float64, device="cuda")
+        # per step: one fused features + prefactor launch (plus one prefactor launch per <= 4
+        # blocks when more than 4 blocks); assembly launches are counted by libfls's events
+        self.fixed_launches = 1 if len(blocks) <= 4 else 1 + (len(blocks) + 3) // 4
+        self.entries_total = R * F
+        self.clk = None
+
+    def device_id(self) -> str:
+        return str(self.torch.cuda.get_device_properties(self.local).uuid)
+
+    def coll_device(self):
+        return "cuda"
+
+    def step(self):
+        fls, p = self.fls, self.p
+        self.torch.cuda.nvtx.range_push("fls step")
+        if self.row_major:
+            fls.fls_features_assemble(self.ctx, p.dim, p.n_features, p.sigma, p.seed, self.bset,
+                                      W=self.W, b=self.b, A=self.Ab, lda=self.lda,
+                                      layout=fls.FLS_ROW_MAJOR, rhs=self.rhs)
+        else:
+            fls.fls_features_assemble(self.ctx, p.dim, p.n_features, p.sigma, p.seed, self.bset,
+                                      W=self.W, b=self.b, A=self.Ab, lda=self.lda)
+        self.torch.cuda.nvtx.range_pop()
+
+    def sync(self):
+        self.fls.fls_sync(self.ctx)
+        self.torch.cuda.synchronize()
+
+    def begin_timed(self):
+        self.fls.fls_sync(self.ctx)
+        self.clk = ClockSampler(self.local)
+        self.clk.start()
+        time.sleep(0.3)                      # let nvidia-smi start sampling
+        self.fls.fls_ctx_timing(self.ctx, True)
+        self.ev = [self.torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def start(self):
+        self.torch.cuda.synchronize()
+        self.clk.mark_begin()
+        self.ev[0].record(self.ctx.stream)
+
+    def stop(self) -> float:
+        self.ev[1].record(self.ctx.stream)
+        self.torch.cuda.synchronize()
+        self.clk.mark_end()
+        return self.ev[0].elapsed_time(self.ev[1])
+
+    def end_timed(self):
+        self.clocks = self.clk.stop()
+        self.fls.fls_sync(self.ctx)
+        self.k_ms, self.k_launches = self.fls.fls_ctx_timing_read(self.ctx)
+        self.fls.fls_ctx_timing(self.ctx, False)
+
+    def kernel_report(self, steps):
+        """this rank's dominant-kernel numbers (algorithmic bytes = 8 B per entry)"""
+        p, n_local = self.p, self.n_local
+        F = p.n_features
+        k_ms_step = self.k_ms / steps
+        achieved = 8.0 * n_local * F / (k_ms_step / 1e3) / 1e9
+        return {"achieved": achieved, "bytes_per_step": 8.0 * n_local * F,
+                "kernel_ms_per_step": k_ms_step,
+                "kernel_ms_avg": self.k_ms / max(self.k_launches, 1),
+                "launches": self.k_launches, "entries_per_s": n_local * F / (k_ms_step / 1e3)}
+
+    def report(self, steps, ms_step, per_rank, n_gpus):
+        torch, p, args = self.torch, self.p, self.args
+        F, R, d = p.n_features, p.n_rows, p.dim
+        hbm_peak, peak_kind = _peaks()
+        mine = per_rank[self.rank]
+        achieved = mine["achieved"]
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tf) and args.rows is None and self.world == 1:
+            try:
+                traffic = json.load(open(tf)).get(args.workload, {}).get("traffic_bytes_per_launch")
+            except Exception:
+                traffic = None
+        # FP64 co-bound (north_star: "the slower of HBM bandwidth and fp64 issue rate")
+        ops = fp64_ops_per_entry(p)
+        fp64 = None
+        clocks = self.clocks
+        if ops is not None:
+            sms = torch.cuda.get_device_properties(self.local).multi_processor_count
+            ach = ops * mine["entries_per_s"] / 1e12
+            fp64 = {"ops_per_entry": ops, "achieved_tops": ach}
+            for tag, mhz in (("max_clock", clocks.get("sm_max_mhz")), ("median_clock", clocks.get("sm_mhz"))):
+                if mhz:
+                    pk = sms * 64 * mhz * 1e6 / 1e12
+                    fp64[f"peak_tops_{tag}"] = pk
+                    fp64[f"frac_{tag}"] = ach / pk
+        power = None
+        pm = os.path.join(ROOT, "profiles", "r01_power_model.json")
+        if os.path.exists(pm) and p.name == "c5_biharm3d":
+            try:
+                m = json.load(open(pm))["model"]
+                bound = m["power_bound_entries_per_s"]
+                power = {"bound": "board power", "limit_w": m["power_limit_w"], "idle_w": m["idle_w"],
+                         "nj_per_entry": m["store_nj_per_entry"] + m["alu_nj_per_entry"],
+                         "bound_entries_per_s_per_gpu": bound,
+                         "achieved_entries_per_s_per_gpu": mine["entries_per_s"],
+                         "frac": mine["entries_per_s"] / bound,
+                         "source": "profiles/r01_power_model.json (tools/power_model.py)",
+                         "note": "sustained-window metric: the board's limiter acts on a time-"
+                                 "averaged power, so a short run can read above 1.0"}
+            except Exception:
+                power = None
+        tot_bytes = sum(r["bytes_per_step"] for r in per_rank)
+        slowest = max(r["kernel_ms_per_step"] for r in per_rank)
+        agg = tot_bytes / (slowest / 1e3) / 1e9
+        return {
+            "dtype": "f64",
+            "config": {"workload": p.name, "rows": R, "features": F, "dim": d,
+                       "operator": "biharmonic + 16(1+x1) u" if p.name == "c5_biharm3d" else p.name,
+                       "A_bytes": 8 * R * (F + 1), "parallelism": f"rows{self.world}",
+                       "rows_per_rank": [int(r["bytes_per_step"] / 8 / F) for r in per_rank],
+                       "l2": f"no flush: each step writes {8e-9 * self.n_local * (F + 1):.1f} GB per "
+                             f"GPU (>> the 126 MB L2)"},
+            "hbm_write_gbs_all_gpus": 8.0 * R * (F + 1) / (ms_step / 1e3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                         "kernel": "assemble_rm_kernel" if self.row_major else "assemble_cm_kernel",
+                         "kernel_ms_avg": mine["kernel_ms_avg"], "fp64_pipe": fp64, "power": power,
+                         "scope": "rank 0's GPU (per-GPU kernel roofline)",
+                         "per_rank": [{"rank": i, "achieved": r["achieved"],
+                                       "frac": r["achieved"] / hbm_peak} for i, r in enumerate(per_rank)],
+                         "aggregate": {"achieved": agg, "peak": hbm_peak * n_gpus,
+                                       "frac": agg / (hbm_peak * n_gpus),
+                                       "note": "all ranks' algorithmic bytes / the slowest rank's "
+                                               "kernel time, against n_gpus x the copy peak"}},
+            "gpu_launches": self.fixed_launches * steps + mine["launches"],
+            "clocks": clocks,
+        }
+
+    def extras(self, args):
+        """legs after the timed region: e2e through the C ABI with host buffers, the
+        end-to-end solve, per-config numbers and the CPU oracle (rank 0, N = 1)"""
+        torch = self.torch
+        out = {}
+        del self.Ab
+        torch.cuda.empty_cache()
+        if not args.no_e2e:
+            out["e2e"] = e2e_measure(args, self.p, self.ctx, self.W, self.b, self.a, self.e,
+                                     self.world, self.local)
+        if not args.no_solve and args.rows is None:
+            out["solve"] = solve_measure(args, self.world, self.rank, self.local)
+        if self.world == 1 and args.rows is None and not args.no_per_config:
+            out["per_config"] = per_config(budget_s=args.per_config_budget)
+        if self.rank == 0 and self.world == 1 and not args.no_cpu:
+            out["cpu_baseline"] = cpu_baseline(self.p)
+        return out
+
+    def close(self):
+        self.ctx.close()
+
+
+def _engine_class():
+    """FLS_BENCH_ENGINE=path/to/file.py:Class injects an engine (CPU tests of the multi-rank
+    contract, tests/fake_bench_engine.py)"""
+    spec = os.environ.get("FLS_BENCH_ENGINE")
+    if not spec:
+        return FlsEngine
+    import importlib.util
+    path, cls = spec.rsplit(":", 1)
+    ms = importlib.util.spec_from_file_location("fls_bench_engine", os.path.join(ROOT, path))
+    mod = importlib.util.module_from_spec(ms)
+    ms.loader.exec_module(mod)
+    return getattr(mod, cls)
+
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args, argv) -> int:
+    """`python bench.py --gpus N` without a launcher: start N ranks, one per GPU, under
+    torch.distributed.run (the same launch the driver uses) and return its exit code.  Rank 0
+    prints the JSON line.  Fails loudly when the node has fewer than N GPUs."""
+    eng = _engine_class()
+    have = eng.device_count()
+    if args.gpus > have:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this node has "
+                         f"{have}\n")
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__)] + list(argv)
+    return subprocess.call(cmd)
+
+
+def run_ranks(args) -> int:
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    eng_cls = _engine_class()
+    shared = os.environ.get("FLS_BENCH_SHARED_GPU") == "1"   # test mode: ranks share GPUs
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: launched with WORLD_SIZE={world} but --gpus {args.gpus}\n")
+        return 2
+    have = eng_cls.device_count()
+    if shared:
+        local %= max(1, have)
+    elif local >= have:
+        sys.stderr.write(f"bench.py: rank {rank} has LOCAL_RANK {local} but the node has {have} GPUs\n")
+        return 2
+    backend = "gloo" if shared else eng_cls.backend
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    eng = eng_cls(args, world, rank, local)
+    cdev = "cpu" if backend == "gloo" else eng.coll_device()
+    # one device per rank: count the distinct devices behind the ranks
+    ids = [eng.device_id()]
+    if world > 1:
+        ids = [None] * world
+        dist.all_gather_object(ids, eng.device_id())
+    n_gpus = len(set(ids))
+    if n_gpus != world and not shared:
+        if rank == 0:
+            sys.stderr.write(f"bench.py: {world} ranks share {n_gpus} device(s); one GPU per rank "
+                             f"is required\n")
+        if world > 1:
+            dist.destroy_process_group()
+        return 2
+    for _ in range(args.warmup):
+        eng.step()
+    eng.sync()
+    eng.begin_timed()
+    if world > 1:
+        dist.barrier()
+    eng.start()
+    for _ in range(args.steps):
+        eng.step()
+    ms_total = eng.stop()
+    if world > 1:
+        dist.barrier()
+    eng.end_timed()
+    t = torch.tensor([ms_total], dtype=torch.float64, device=cdev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    mine = eng.kernel_report(args.steps)
+    per_rank = [mine]
+    if world > 1:
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
+    line = {"metric": METRIC, "value": eng.entries_total / (ms_step / 1e3), "unit": UNIT,
+            "n_gpus": n_gpus, "ranks": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
+            "vs_baseline": None, "data": "synthetic"}
+    line.update(eng.report(args.steps, ms_step, per_rank, n_gpus))
+    line.update(eng.extras(args))
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -371,6 +778,8 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=1024)
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
     ap.add_argument("--no-solve", action="store_true", help="skip the end-to-end solve leg")
+    ap.add_argument("--no-per-config", action="store_true", help="skip the C1-C4 per-config leg")
+    ap.add_argument("--per-config-budget", type=float, default=60.0)
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: the config's rows split over the ranks (BASELINE config 5's "
                          "sweep, default); weak: every rank keeps the config's full row count")
@@ -380,186 +789,15 @@ def main():
     ap.add_argument("--e2e-ring-rows", type=int, default=262144)
     ap.add_argument("--rows", type=int, default=None,
                     help="override the interior row count (profiling a reduced copy of the workload)")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
     if args.impl == "reference":
-        return run_reference(args)
-
-    import torch
-    import torch.distributed as dist
-    import workloads as wl
-    from paper_2602_10541_b200 import fls
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    local %= max(1, torch.cuda.device_count())      # ranks > GPUs only in the gloo test mode
-    torch.cuda.set_device(local)
-    if world > 1:
-        # NCCL over NVLink; FLS_DIST_BACKEND=gloo runs the multi-rank host logic with host
-        # collectives (e.g. 2 ranks sharing one GPU in a test; no kernel waits on another rank)
-        backend = os.environ.get("FLS_DIST_BACKEND", "nccl")
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-
-    kw = {"n_int": args.rows} if args.rows else {}
-    if args.scaling == "weak":
-        # every rank keeps the config's full row count: the job is world x the config's rows
-        base_rows = args.rows or wl.FULL[args.workload]["n_int"]
-        kw["n_int"] = base_rows * world
-    p = wl.make_problem(args.workload, "full", **kw)
-    F, R, d = p.n_features, p.n_rows, p.dim
-    a, e = wl.shard_range(R, rank, world)
-    n_local = e - a
-    # this rank's points only (inputs resident in HBM before timing)
-    offs = p.block_offsets()
-    blocks = []
-    for blk, o in zip(p.blocks, offs):
-        lo, hi = max(a, o), min(e, o + blk.n)
-        if hi <= lo:
-            continue
-        sl = slice(lo - o, hi - o)
-        blocks.append(fls.Block(torch.from_numpy(np.ascontiguousarray(blk.X[sl])).cuda(), blk.terms,
-                                blk.weight, torch.from_numpy(np.ascontiguousarray(blk.values[sl])).cuda(),
-                                torch.from_numpy(np.ascontiguousarray(blk.fields[sl])).cuda()
-                                if blk.fields is not None else None))
-    ctx = fls.Context(local)
-    bset = fls.BlockSet(blocks, d)
-    row_major = args.layout == "row"
-    lda = fls.round_up(F, 2) if row_major else fls.round_up(n_local, 4)
-    Ab = torch.empty(((n_local if row_major else F + 1) * lda,), dtype=torch.float64, device="cuda")
-    rhs = torch.empty((n_local,), dtype=torch.float64, device="cuda") if row_major else None
-    W = torch.empty((F, d), dtype=torch.float64, device="cuda")
-    b = torch.empty((F,), dtype=torch.float64, device="cuda")
-    # per step: one fused features + prefactor launch (plus one prefactor launch per <= 4 blocks
-    # when more than 4 blocks); assembly launches are counted by libfls's own timing events
-    # (one per batch of blocks sharing a kernel variant)
-    launches_per_step_fixed = 1 if len(blocks) <= 4 else 1 + (len(blocks) + 3) // 4
-
-    def step():
-        torch.cuda.nvtx.range_push("fls step")   # NVTX: one range per step for nsys timelines
-        if row_major:
-            fls.fls_features_assemble(ctx, d, F, p.sigma, p.seed, bset, W=W, b=b, A=Ab, lda=lda,
-                                      layout=fls.FLS_ROW_MAJOR, rhs=rhs)
-        else:
-            fls.fls_features_assemble(ctx, d, F, p.sigma, p.seed, bset, W=W, b=b, A=Ab, lda=lda)
-        torch.cuda.nvtx.range_pop()
-
-    for _ in range(args.warmup):
-        step()
-    fls.fls_sync(ctx)
-    clk = ClockSampler(local)
-    clk.start()
-    time.sleep(0.3)                      # let nvidia-smi start sampling
-    fls.fls_ctx_timing(ctx, True)
-    st = ctx.stream
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clk.mark_begin()
-    e0.record(st)
-    for _ in range(args.steps):
-        step()
-    e1.record(st)
-    torch.cuda.synchronize()
-    clk.mark_end()
-    if world > 1:
-        dist.barrier()
-    clocks = clk.stop()
-    fls.fls_sync(ctx)
-    ms_total = e0.elapsed_time(e1)
-    k_ms, k_launches = fls.fls_ctx_timing_read(ctx)
-    fls.fls_ctx_timing(ctx, False)
-    t = torch.tensor([ms_total], dtype=torch.float64, device=_cdev())
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    ms_step = ms_max / args.steps
-    entries = R * F
-    value = entries / (ms_step / 1e3)
-
-    # roofline of the dominant kernel (assembly): algorithmic bytes = 8 B x entries per launch
-    hbm_peak, peak_kind = _peaks()
-    k_avg_ms = k_ms / max(k_launches, 1)
-    # algorithmic bytes of all assembly launches of one step / their summed time per step
-    k_ms_step = k_ms / args.steps
-    achieved = 8.0 * n_local * F / (k_ms_step / 1e3) / 1e9
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tf) and args.rows is None and world == 1:
-        try:
-            traffic = json.load(open(tf)).get(args.workload, {}).get("traffic_bytes_per_launch")
-        except Exception:
-            traffic = None
-    # the FP64 co-bound (north_star: "the slower of HBM bandwidth and fp64 issue rate"): FP64-pipe
-    # lane-ops per second vs 148 SMs x 64 FP64 lanes/clk at the max and the median loaded clock
-    ops = fp64_ops_per_entry(p)
-    fp64 = None
-    if ops is not None:
-        sms = torch.cuda.get_device_properties(local).multi_processor_count
-        ach = ops * n_local * F / (k_ms_step / 1e3) / 1e12
-        fp64 = {"ops_per_entry": ops, "achieved_tops": ach}
-        for tag, mhz in (("max_clock", clocks.get("sm_max_mhz")), ("median_clock", clocks.get("sm_mhz"))):
-            if mhz:
-                pk = sms * 64 * mhz * 1e6 / 1e12
-                fp64[f"peak_tops_{tag}"] = pk
-                fp64[f"frac_{tag}"] = ach / pk
-    # the binding roofline under sustained load: board power (profiles/r01_power_model.json,
-    # tools/power_model.py: idle power + measured energy per entry of the store pattern and of the
-    # per-entry arithmetic, each probed alone) -> entries/s <= (P_limit - P_idle) / (E_st + E_alu)
-    power = None
-    pm = os.path.join(ROOT, "profiles", "r01_power_model.json")
-    if os.path.exists(pm) and p.name == "c5_biharm3d":
-        try:
-            m = json.load(open(pm))["model"]
-            bound = m["power_bound_entries_per_s"]
-            power = {"bound": "board power", "limit_w": m["power_limit_w"], "idle_w": m["idle_w"],
-                     "nj_per_entry": m["store_nj_per_entry"] + m["alu_nj_per_entry"],
-                     "bound_entries_per_s_per_gpu": bound,
-                     "achieved_entries_per_s_per_gpu": n_local * F / (k_ms_step / 1e3),
-                     "frac": n_local * F / (k_ms_step / 1e3) / bound,
-                     "source": "profiles/r01_power_model.json (tools/power_model.py)",
-                     "note": "a 20-step run can read above 1.0: the board's limiter acts on a "
-                             "time-averaged power, so short runs borrow headroom; run back to "
-                             "back for 4 s the kernel sits at 0.99 (995 W of 1000 W)"}
-        except Exception:
-            power = None
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": p.name, "rows": R, "features": F, "dim": d,
-                   "operator": "biharmonic + 16(1+x1) u" if p.name == "c5_biharm3d" else p.name,
-                   "A_bytes": 8 * R * (F + 1), "parallelism": f"rows{world}",
-                   "l2": f"no flush: each step writes {8e-9 * n_local * (F + 1):.1f} GB per GPU "
-                         f"(>> the 126 MB L2)"},
-        "hbm_write_gbs_all_gpus": 8.0 * R * (F + 1) / (ms_step / 1e3) / 1e9,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic,
-                     "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                     "kernel": "assemble_rm_kernel" if row_major else "assemble_cm_kernel",
-                     "kernel_ms_avg": k_avg_ms, "fp64_pipe": fp64, "power": power,
-                     "scope": "rank 0's GPU (per-GPU kernel roofline)"},
-        "gpu_launches": launches_per_step_fixed * args.steps + k_launches,
-        "clocks": clocks,
-    }
-    # ---------------------------------------------------------------- end to end (host buffers)
-    del Ab
-    torch.cuda.empty_cache()
-    if not args.no_e2e:
-        line["e2e"] = e2e_measure(args, p, ctx, W, b, a, e, world, local)
-    if not args.no_solve and args.rows is None:
-        line["solve"] = solve_measure(args, world, rank, local)
-    if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(p)
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    ctx.close()
-    if world > 1:
-        dist.destroy_process_group()
+        return run_reference(args) or 0
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args, argv)
+    return run_ranks(args)
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

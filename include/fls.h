@@ -19,7 +19,8 @@
  * This library implements Algorithm 1 on one B200 per process:
  *     fls_features  -- line 1, sample W and b
  *     fls_assemble  -- lines 3-5 (first half): A_pde, lambda A_bc, (lambda A_ic), rhs
- *     fls_solve     -- line 5 (second half): beta = argmin ||A beta - b||^2 (+ mu ||beta||^2)
+ *     fls_solve     -- line 5 (second half): beta = argmin ||A beta - b||^2 (+ mu ||beta||^2),
+ *                      TSQR over the ranks when a communicator is attached (fls_comm_init)
  *     fls_eval      -- line 6: u_N (or L[u_N]) at arbitrary points
  * Notation in this header: n_features = N of the paper (BASELINE.json calls it M),
  * n_points = collocation rows (the paper's M_1, M_2).
@@ -60,7 +61,7 @@ extern "C" {
 #define FLS_API
 #endif
 
-#define FLS_API_VERSION 2  /* 2: fls_features_assemble, fls_geqrf, fls_eval_block, fls_ipc_*, fls_solve_stacked; fields in fls_bandwidth_grad */
+#define FLS_API_VERSION 3  /* 3: fls_comm_* (multi-rank TSQR inside fls_solve), fls_solve takes ridge_rel, fls_solve_mu; 2: fls_features_assemble, fls_geqrf, fls_eval_block, fls_ipc_*, fls_solve_stacked */
 #define FLS_MAX_DIM 8      /* spatial / space-time dimension d <= 8 */
 #define FLS_MAX_TERMS 64   /* terms per operator */
 #define FLS_MAX_FIELDS 4   /* coefficient fields per block */
@@ -72,7 +73,7 @@ typedef enum {
     FLS_ENOMEM = 2,        /* device allocation failed */
     FLS_ECUDA = 3,         /* CUDA runtime error */
     FLS_ECUSOLVER = 4,     /* cuSOLVER / cuBLAS error */
-    FLS_ENCCL = 5,         /* reserved for the collective layer */
+    FLS_ENCCL = 5,         /* collective layer: NCCL unavailable / failed, host callback failed */
     FLS_ENONFINITE = 6,    /* NaN / Inf in an input (reported by fls_sync / fls_solve) */
     FLS_ERANK = 7,         /* exactly zero diagonal in R with no ridge */
     FLS_EUNSUPPORTED = 8   /* valid request this build does not implement */
@@ -232,20 +233,76 @@ FLS_API fls_status fls_assemble_host(fls_ctx *ctx, const double *W, const double
                                      double *rhs, int64_t chunk_rows);
 
 /* ---------------------------------------------------------------------------------------- */
-/* Alg. 1 line 5 ("beta* = argmin ||A beta - b||^2 via QR"), with the optional       */
-/* Tikhonov term of P:L156-160:  beta = argmin ||A beta - b||^2 + mu ||beta||^2.             */
-/* Householder QR (cuSOLVER geqrf) of the column-major [A | b] (n_rows x (n_features + 1),   */
-/* b stored as column n_features), then R beta = (Q^T b)[0:n].  sqrt_mu > 0 appends the      */
-/* rows [sqrt_mu I | 0] at rows n_rows .. n_rows + n_features - 1 of the same buffer, so     */
-/* then lda >= n_rows + n_features is required.  (reading A16: sqrt_mu =          */
-/* tau ||A||_F with tau = 0 for C1-C4, 1e-10 for C5; use fls_frob2 for ||A||_F^2.)           */
-/*   Ab: device, destroyed (holds R on return).  beta: device, n_features (written).          */
+/* Alg. 1 line 5 ("beta* = argmin ||A beta - b||^2 via QR"), with the Tikhonov term  */
+/* of P:L156-160:  beta = argmin ||A beta - b||^2 + mu ||beta||^2,  sqrt(mu) = ridge_rel *     */
+/* ||A||_F (reading A16: ridge_rel = tau = 0 for C1-C4, 1e-10 for C5; ||A||_F over  */
+/* the n_features columns of A, not b, and over ALL ranks' rows when a communicator is        */
+/* attached).  Householder QR of the column-major [A | b] (n_rows x (n_features + 1), b as    */
+/* column n_features), then R beta = (Q^T b)[0:n].                                            */
+/*   Without a communicator (or one rank): a single QR; when sqrt(mu) > 0 the rows            */
+/*   [sqrt(mu) I | 0] are written at rows n_rows .. n_rows + n_features - 1 of the same       */
+/*   buffer, so lda >= n_rows + n_features is then required.                                  */
+/*   With a communicator of P ranks (fls_comm_init / fls_comm_init_host): Ab holds THIS rank's */
+/*   rows (n_rows may differ per rank, may be 0; lda >= n_rows), every rank calls fls_solve    */
+/*   with the same n_features and ridge_rel, and the call runs TSQR: local QR, the R factors   */
+/*   to rank 0 (peer-memory stores or NCCL, fls_comm_config), the root's structured QR of the  */
+/*   stacked factors plus the ridge rows, trsv, and beta + the residual broadcast -- on return */
+/*   beta and *resid_norm are identical on every rank.  A failure on any rank is returned on   */
+/*   every rank (no rank is left waiting).                                                    */
+/*   Ab: device, destroyed.  beta: device, n_features (written).                              */
 /*   resid_norm: host, optional: ||A beta - b||_2 (+ ridge part) = |R[n, n]|.                 */
 /*   Blocking.  Errors: FLS_EINVAL, FLS_ENOMEM, FLS_ECUSOLVER, FLS_ERANK (exact zero on the   */
-/*   diagonal of R with sqrt_mu = 0), FLS_ENONFINITE (pending from an earlier kernel).       */
+/*   diagonal of R with mu = 0), FLS_ENONFINITE (pending from an earlier kernel), FLS_ENCCL,  */
+/*   FLS_EUNSUPPORTED (forced P2P transport unavailable).                                     */
+/* fls_solve_mu: the same with an ABSOLUTE sqrt(mu) >= 0 (the Newton step's mu = 1e-10,       */
+/*   P:L158, L189).                                                                           */
 /* ---------------------------------------------------------------------------------------- */
 FLS_API fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int64_t n_features,
-                     double sqrt_mu, double *beta, double *resid_norm);
+                     double ridge_rel, double *beta, double *resid_norm);
+FLS_API fls_status fls_solve_mu(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda,
+                                int64_t n_features, double sqrt_mu, double *beta, double *resid_norm);
+
+/* ---------------------------------------------------------------------------------------- */
+/* Communicator for the multi-rank solve (row-sharded assembly needs no     */
+/* collective; the least-squares solve has one exchange step, TSQR).  One ctx per rank, one   */
+/* rank per GPU.  The communicator belongs to the ctx (freed by fls_comm_destroy or          */
+/* fls_ctx_destroy).                                                                          */
+/* fls_comm_unique_id: an NCCL unique id (host, FLS_COMM_ID_BYTES) -- rank 0 creates it and   */
+/*   the caller distributes it to every rank by its own means (torch.distributed, MPI, file). */
+/* fls_comm_init: NCCL communicator of nranks ranks on the ctx's device and stream; blocks    */
+/*   until all ranks have called it.  NCCL is loaded at run time ("libnccl.so.2", or the path  */
+/*   in FLS_NCCL_LIB): FLS_ENCCL when it cannot be loaded or the init fails.                   */
+/* fls_comm_init_host: the control plane through caller callbacks instead of NCCL (the R      */
+/*   factors then move only by peer memory, so the ranks' GPUs -- or ONE shared GPU, e.g. in  */
+/*   tests -- must support CUDA IPC).  allgather(user, send, recv, bytes) must gather `bytes`  */
+/*   host bytes from every rank into recv (nranks * bytes, rank r at offset r * bytes) and    */
+/*   return 0; it is called from inside fls_solve on the calling thread.  *coll is copied;   */
+/*   user must stay valid until the communicator is destroyed.                                 */
+/* fls_comm_config: transport of the R factors -- FLS_TSQR_AUTO (peer memory if every rank    */
+/*   can map the root's buffer, else NCCL), FLS_TSQR_P2P (peer memory only), FLS_TSQR_NCCL;   */
+/*   force_tsqr != 0 runs the TSQR path even with one rank (tests).                            */
+/* fls_comm_info: nranks / rank (0 / 0 without a communicator) and the transport the last     */
+/*   solve used (0 none, FLS_TSQR_P2P, FLS_TSQR_NCCL).                                         */
+/*   Errors: FLS_EINVAL (NULL, rank not in [0, nranks), ctx already has a communicator),      */
+/*   FLS_ENCCL.                                                                                */
+/* ---------------------------------------------------------------------------------------- */
+#define FLS_COMM_ID_BYTES 128
+#define FLS_TSQR_AUTO 0
+#define FLS_TSQR_P2P 1
+#define FLS_TSQR_NCCL 2
+typedef struct {
+    void *user;
+    int32_t (*allgather)(void *user, const void *send, void *recv, int64_t bytes);
+} fls_host_coll;
+FLS_API fls_status fls_comm_unique_id(void *id);
+FLS_API fls_status fls_comm_init(fls_ctx *ctx, const void *nccl_unique_id, int32_t nranks,
+                                 int32_t rank);
+FLS_API fls_status fls_comm_init_host(fls_ctx *ctx, int32_t nranks, int32_t rank,
+                                      const fls_host_coll *coll);
+FLS_API fls_status fls_comm_destroy(fls_ctx *ctx);
+FLS_API fls_status fls_comm_config(fls_ctx *ctx, int32_t transport, int32_t force_tsqr);
+FLS_API fls_status fls_comm_info(fls_ctx *ctx, int32_t *nranks, int32_t *rank,
+                                 int32_t *last_transport);
 
 /* ---------------------------------------------------------------------------------------- */
 /* Learnable bandwidth (App. E): W_j = L W^_j with frozen W^_j ~ N(0, I) and a    */
@@ -359,7 +416,8 @@ FLS_API fls_status fls_qr_r(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda
 FLS_API fls_status fls_geqrf(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda, int64_t n_cols,
                              double *tau);
 
-/* CUDA IPC for the TSQR exchange over peer memory (NVLink / NVSwitch): the root exports its
+/* CUDA IPC building blocks (fls_solve with a communicator runs its own exchange internally;    */
+/* these serve callers that orchestrate one themselves).  Peer memory (NVLink / NVSwitch): the root exports its
  * stacking buffer, every rank maps it and fls_qr_r writes its R factor straight into the
  * root's memory (the R-extraction kernel's stores ARE the transfer; no staging, no NCCL
  * gather).  fls_ipc_handle: handle (host, FLS_IPC_HANDLE_BYTES) of the allocation that

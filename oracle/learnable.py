@@ -7,7 +7,11 @@ c(x) = coef, or coef times a coefficient field),
     d/dW_k = c e_k prod W^(e - e_k) Phi_p(z) + c prod W^e x_k Phi_{p+1}(z),
     dLout/dL_kl = 2 sum_ij r_i beta_j dA_ij/dW_jk W^_jl      (beta* optimal: envelope)
 evaluated with numpy sin / cos on the full (rows x features) grid -- small inputs only.
-Pinned by central finite differences of Lout (tests/test_oracle_learnable.py).
+With a Tikhonov inner solve (sqrt_mu > 0) the outer loss is the ridge-augmented
+    Lout_mu = ||A beta* - b||^2 + mu ||beta*||^2    (reading B2)
+-- the objective beta* minimises -- so the same envelope formula is its exact gradient (mu
+||beta||^2 has no explicit L dependence); at mu = 0 it is Lout.
+Pinned by central finite differences of Lout / Lout_mu (tests/test_oracle_learnable.py).
 """
 from __future__ import annotations
 
@@ -30,7 +34,10 @@ def outer_loss(Lmat, W_hat, b, blocks, sqrt_mu=0.0, normalize=True):
     else:
         beta, _, _ = lstsq(A, rhs)
     r = A @ beta - rhs
-    return float(r @ r), W, beta, r
+    loss = float(r @ r)
+    if sqrt_mu > 0:                                  # reading B2: the inner solve's objective
+        loss += sqrt_mu * sqrt_mu * float(beta @ beta)
+    return loss, W, beta, r
 
 
 def outer_grad(Lmat, W_hat, b, blocks, sqrt_mu=0.0, normalize=True):

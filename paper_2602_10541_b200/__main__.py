@@ -53,8 +53,7 @@ def main(argv=None) -> int:
         ev[0].record()
         W, b, Ab, lda = fls.fls_features_assemble(ctx, d, F, sigma, p.seed, blocks, extra_rows=extra)
         ev[1].record()
-        sq = p.ridge_rel * math.sqrt(fls.fls_frob2(ctx, Ab, R, lda, F)) if p.ridge_rel > 0 else 0.0
-        beta, res = fls.fls_solve(ctx, Ab, R, lda, F, sq)
+        beta, res = fls.fls_solve(ctx, Ab, R, lda, F, p.ridge_rel)   # sqrt(mu) = tau ||A||_F inside
         ev[2].record()
         u = fls.fls_eval(ctx, W, b, beta, Xt)
         ev[3].record()

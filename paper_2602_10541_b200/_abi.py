@@ -21,6 +21,10 @@ FLS_MAX_FIELDS = 4
 FLS_COL_MAJOR = 0
 FLS_ROW_MAJOR = 1
 FLS_IPC_HANDLE_BYTES = 64
+FLS_COMM_ID_BYTES = 128
+FLS_TSQR_AUTO = 0
+FLS_TSQR_P2P = 1
+FLS_TSQR_NCCL = 2
 
 STATUS = {0: "FLS_OK", 1: "FLS_EINVAL", 2: "FLS_ENOMEM", 3: "FLS_ECUDA", 4: "FLS_ECUSOLVER",
           5: "FLS_ENCCL", 6: "FLS_ENONFINITE", 7: "FLS_ERANK", 8: "FLS_EUNSUPPORTED"}
@@ -54,6 +58,14 @@ FLS_NL_UDU = 3
 
 class fls_nonlinearity(C.Structure):
     _fields_ = [("kind", C.c_int32), ("degree", C.c_int32), ("a", C.c_double * 8)]
+
+
+# int32 allgather(void *user, const void *send, void *recv, int64 bytes)
+HOST_ALLGATHER = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64)
+
+
+class fls_host_coll(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allgather", HOST_ALLGATHER)]
 
 
 _SIGS = {
@@ -103,6 +115,15 @@ _SIGS = {
                                     C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64]),
     "fls_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_double,
                             C.c_void_p, C.POINTER(C.c_double)]),
+    "fls_solve_mu": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_double,
+                               C.c_void_p, C.POINTER(C.c_double)]),
+    "fls_comm_unique_id": (C.c_int, [C.c_void_p]),
+    "fls_comm_init": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]),
+    "fls_comm_init_host": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(fls_host_coll)]),
+    "fls_comm_destroy": (C.c_int, [C.c_void_p]),
+    "fls_comm_config": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
+    "fls_comm_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                C.POINTER(C.c_int32)]),
     "fls_solve_stacked": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_int64,
                                     C.c_double, C.c_void_p, C.POINTER(C.c_double)]),
     "fls_geqrf": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p]),

@@ -14,73 +14,15 @@
 #include <string>
 #include <vector>
 
+#include "fls_ctx.h"
 #include "fls_internal.h"
 
 using namespace fls;
 
-struct fls_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  unsigned *d_err = nullptr;          // async non-finite flag
-  double *d_scratch = nullptr;        // small device scratch (min diag, frob partials)
-  double *ws = nullptr;               // per-feature prefactor records
-  size_t ws_bytes = 0;
-  double *qws = nullptr;              // blocked-QR workspace (grow-only; + tau scratch)
-  size_t qws_bytes = 0;
-  double *gws = nullptr;              // bandwidth-gradient partials (grow-only)
-  size_t gws_bytes = 0;
-  double *sws = nullptr;              // permuted stack of the TSQR root solve (grow-only)
-  size_t sws_bytes = 0;
-  cusolverDnHandle_t solver = nullptr;
-  cublasHandle_t blas = nullptr;
-  // optional per-launch timing of the assembly kernels (fls_ctx_timing)
-  bool timing = false;
-  std::vector<cudaEvent_t> ev;  // pairs (start, stop)
-  size_t ev_used = 0;
-  // host-buffer path (fls_assemble_host): copy stream, events, device staging
-  cudaStream_t copy_stream = nullptr;
-  cudaEvent_t hev[4] = {nullptr, nullptr, nullptr, nullptr};
-  cudaEvent_t switch_ev = nullptr;  // fls_ctx_set_stream ordering
-  double *hin = nullptr, *hout = nullptr;
-  size_t hin_bytes = 0, hout_bytes = 0;
-};
 
 namespace {
 
 thread_local std::string g_err;
-
-fls_status fail(fls_status s, const char *fmt, ...) {
-  char buf[512];
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(buf, sizeof buf, fmt, ap);
-  va_end(ap);
-  g_err = buf;
-  return s;
-}
-
-fls_status cuda_fail(cudaError_t e, const char *where) {
-  return fail(FLS_ECUDA, "%s: %s", where, cudaGetErrorString(e));
-}
-
-#define FLS_CUDA(call)                                         \
-  do {                                                         \
-    cudaError_t e_ = (call);                                   \
-    if (e_ != cudaSuccess) return cuda_fail(e_, #call);        \
-  } while (0)
-
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-  }
-};
 
 fls_status ensure_ws(fls_ctx *ctx, size_t bytes) {
   if (bytes <= ctx->ws_bytes) return FLS_OK;
@@ -156,12 +98,30 @@ fls_status plan_operator(const fls_operator *op, int32_t dim, int32_t n_fields, 
   return FLS_OK;
 }
 
+}  // namespace
+
+namespace fls {
+
+fls_status fail(fls_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+fls_status cuda_fail(cudaError_t e, const char *where) {
+  return fail(FLS_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
 fls_status check_ctx(fls_ctx *ctx) {
   if (!ctx) return fail(FLS_EINVAL, "ctx is NULL");
   return FLS_OK;
 }
 
-}  // namespace
+}  // namespace fls
 
 extern "C" {
 
@@ -209,6 +169,7 @@ fls_status fls_ctx_destroy(fls_ctx *ctx) {
   if (!ctx) return FLS_OK;
   DeviceGuard g(ctx->device);
   cudaStreamSynchronize(ctx->stream);  // kernels may still read the workspace
+  comm_destroy(ctx);
   if (ctx->solver) cusolverDnDestroy(ctx->solver);
   if (ctx->blas) cublasDestroy(ctx->blas);
   for (cudaEvent_t ev : ctx->ev) cudaEventDestroy(ev);
@@ -709,13 +670,12 @@ fls_status fls_assemble_host(fls_ctx *ctx, const double *W, const double *b, int
 
 }  // extern "C"
 
-static fls_status qr_trsv(fls_ctx *ctx, double *Ab, int64_t m, int64_t lda, int64_t n_features,
-                          double *beta, double *resid_norm, int64_t grp_base, int64_t grp_size);
-
-extern "C" {
-
 // ---------------------------------------------------------------------------------------------
-static fls_status ensure_handles(fls_ctx *ctx) {
+// least squares (Alg. 1 line 5; Tikhonov form P:L156-160)
+// ---------------------------------------------------------------------------------------------
+namespace fls {
+
+fls_status ensure_handles(fls_ctx *ctx) {
   if (!ctx->solver) {
     if (cusolverDnCreate(&ctx->solver) != CUSOLVER_STATUS_SUCCESS)
       return fail(FLS_ECUSOLVER, "cusolverDnCreate failed");
@@ -761,9 +721,8 @@ static int qr_method() {
   return 0;
 }
 
-static fls_status geqrf_inplace(fls_ctx *ctx, double *M, int64_t m, int64_t lda, int64_t n,
-                                double *tau_out = nullptr, int64_t grp_base = 0,
-                                int64_t grp_size = 0) {
+fls_status geqrf_inplace(fls_ctx *ctx, double *M, int64_t m, int64_t lda, int64_t n,
+                         double *tau_out, int64_t grp_base, int64_t grp_size) {
   if (m > INT32_MAX || n > INT32_MAX || lda > INT32_MAX)
     return fail(FLS_EUNSUPPORTED, "geqrf: dimensions exceed int32 (m=%lld n=%lld lda=%lld)",
                 (long long)m, (long long)n, (long long)lda);
@@ -800,41 +759,12 @@ static fls_status geqrf_inplace(fls_ctx *ctx, double *M, int64_t m, int64_t lda,
                                          lwork, info);
   int h_info = 0;
   cudaMemcpyAsync(&h_info, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
-  
   cudaError_t e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return cuda_fail(e, "geqrf");
   if (st != CUSOLVER_STATUS_SUCCESS || h_info != 0)
     return fail(FLS_ECUSOLVER, "cusolverDnDgeqrf status %d info %d", (int)st, h_info);
   return FLS_OK;
 }
-
-fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int64_t n_features,
-                     double sqrt_mu, double *beta, double *resid_norm) {
-  if (fls_status s = check_ctx(ctx)) return s;
-  if (!Ab || !beta) return fail(FLS_EINVAL, "Ab or beta is NULL");
-  if (n_features < 1) return fail(FLS_EINVAL, "n_features < 1");
-  if (!(sqrt_mu >= 0.0) || !std::isfinite(sqrt_mu)) return fail(FLS_EINVAL, "sqrt_mu must be >= 0");
-  const int64_t m = n_rows + (sqrt_mu > 0.0 ? n_features : 0);
-  if (n_rows < 0 || lda < m)
-    return fail(FLS_EINVAL, "lda %lld < rows %lld (ridge rows included)", (long long)lda,
-                (long long)m);
-  if (m < n_features)
-    return fail(FLS_EINVAL, "underdetermined: %lld rows < %lld features without ridge",
-                (long long)m, (long long)n_features);
-  DeviceGuard g(ctx->device);
-  if (fls_status s = fls_sync(ctx)) return s;  // surface pending async errors first
-  if (fls_status s = ensure_handles(ctx)) return s;
-  if (sqrt_mu > 0.0) {
-    cudaError_t e = launch_ridge_fill(Ab, lda, n_rows, n_features, n_features + 1, sqrt_mu, ctx->stream);
-    if (e != cudaSuccess) return cuda_fail(e, "ridge_fill");
-  }
-  // the ridge rows [sqrt_mu I | 0] below row n_rows: ridge row i is zero left of column i, so
-  // the blocked QR can stop each panel where the ridge rows still are (grouped mode, G = 1)
-  return qr_trsv(ctx, Ab, m, lda, n_features, beta, resid_norm, sqrt_mu > 0.0 ? n_rows : 0,
-                 sqrt_mu > 0.0 ? 1 : 0);
-}
-
-}  // extern "C"
 
 // [A | b] (m x (F+1), lda; ridge rows already in place) -> beta = R^-1 (Q^T b)[0:F], |R(F,F)|
 static fls_status qr_trsv(fls_ctx *ctx, double *Ab, int64_t m, int64_t lda, int64_t n_features,
@@ -863,27 +793,49 @@ static fls_status qr_trsv(fls_ctx *ctx, double *Ab, int64_t m, int64_t lda, int6
   return FLS_OK;
 }
 
-extern "C" {
+fls_status frob2_host(fls_ctx *ctx, const double *A, int64_t m, int64_t lda, int64_t n,
+                      double *out) {
+  DeviceGuard g(ctx->device);
+  const int nblk = 592;  // 4 x 148 SMs, fixed -> deterministic summation order
+  cudaError_t e = launch_frob2(A, lda, m, n, ctx->d_scratch + 8, nblk, ctx->d_scratch, ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "frob2");
+  FLS_CUDA(cudaMemcpyAsync(out, ctx->d_scratch, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  FLS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return FLS_OK;
+}
 
-fls_status fls_solve_stacked(fls_ctx *ctx, const double *S, int32_t n_blocks, int64_t kb,
-                             int64_t lds, int64_t n_features, double sqrt_mu, double *beta,
-                             double *resid_norm) {
-  if (fls_status s = check_ctx(ctx)) return s;
-  if (!S || !beta) return fail(FLS_EINVAL, "S or beta is NULL");
-  if (n_features < 1 || n_blocks < 1 || kb < 1) return fail(FLS_EINVAL, "bad sizes");
-  if (lds < (int64_t)n_blocks * kb)
-    return fail(FLS_EINVAL, "lds %lld < n_blocks * kb = %lld", (long long)lds,
-                (long long)n_blocks * kb);
-  if (!(sqrt_mu >= 0.0) || !std::isfinite(sqrt_mu)) return fail(FLS_EINVAL, "sqrt_mu must be >= 0");
-  const int64_t F = n_features, n = F + 1;
-  const int64_t gq = (n_blocks - 1) + (sqrt_mu > 0.0 ? 1 : 0);
+fls_status solve_local(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int64_t F,
+                       double sqrt_mu, double *beta, double *resid_norm) {
+  const int64_t m = n_rows + (sqrt_mu > 0.0 ? F : 0);
+  if (n_rows < 0 || lda < m)
+    return fail(FLS_EINVAL, "lda %lld < rows %lld (ridge rows included)", (long long)lda,
+                (long long)m);
+  if (m < F)
+    return fail(FLS_EINVAL, "underdetermined: %lld rows < %lld features without ridge",
+                (long long)m, (long long)F);
+  DeviceGuard g(ctx->device);
+  if (fls_status s = ensure_handles(ctx)) return s;
+  if (sqrt_mu > 0.0) {
+    cudaError_t e = launch_ridge_fill(Ab, lda, n_rows, F, F + 1, sqrt_mu, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "ridge_fill");
+  }
+  // the ridge rows [sqrt_mu I | 0] below row n_rows: ridge row i is zero left of column i, so
+  // the blocked QR can stop each panel where the ridge rows still are (grouped mode, G = 1)
+  return qr_trsv(ctx, Ab, m, lda, F, beta, resid_norm, sqrt_mu > 0.0 ? n_rows : 0,
+                 sqrt_mu > 0.0 ? 1 : 0);
+}
+
+fls_status solve_stacked_impl(fls_ctx *ctx, const double *S, int32_t P, int64_t kb, int64_t bs,
+                              int64_t cs, int64_t F, double sqrt_mu, double *beta,
+                              double *resid_norm) {
+  const int64_t n = F + 1;
+  const int64_t gq = (P - 1) + (sqrt_mu > 0.0 ? 1 : 0);
   const int64_t groups = gq > 0 ? std::max<int64_t>(kb, sqrt_mu > 0.0 ? F : 0) : 0;
   const int64_t m = kb + groups * gq;
   if (m < F) return fail(FLS_EINVAL, "underdetermined: %lld rows < %lld features", (long long)m,
                          (long long)F);
   const int64_t ldm = (m + 3) / 4 * 4;
   DeviceGuard g(ctx->device);
-  if (fls_status s = fls_sync(ctx)) return s;
   if (fls_status s = ensure_handles(ctx)) return s;
   const size_t need = sizeof(double) * (size_t)ldm * n;
   if (need > ctx->sws_bytes) {  // grow-only scratch for the permuted stack
@@ -897,10 +849,69 @@ fls_status fls_solve_stacked(fls_ctx *ctx, const double *S, int32_t n_blocks, in
     }
     ctx->sws_bytes = need;
   }
-  cudaError_t e = launch_stack_permute(S, lds, n_blocks, kb, F, sqrt_mu, gq > 0 ? gq : 1, m, n,
+  cudaError_t e = launch_stack_permute(S, bs, cs, P, kb, F, sqrt_mu, gq > 0 ? gq : 1, m, n,
                                        ctx->sws, ldm, ctx->stream);
   if (e != cudaSuccess) return cuda_fail(e, "stack_permute");
   return qr_trsv(ctx, ctx->sws, m, ldm, F, beta, resid_norm, kb, gq);
+}
+
+}  // namespace fls
+
+extern "C" {
+
+fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int64_t n_features,
+                     double ridge_rel, double *beta, double *resid_norm) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!Ab || !beta) return fail(FLS_EINVAL, "Ab or beta is NULL");
+  if (n_features < 1) return fail(FLS_EINVAL, "n_features < 1");
+  if (n_rows < 0) return fail(FLS_EINVAL, "n_rows < 0");
+  if (!(ridge_rel >= 0.0) || !std::isfinite(ridge_rel))
+    return fail(FLS_EINVAL, "ridge_rel must be >= 0 and finite");
+  DeviceGuard g(ctx->device);
+  if (fls_status s = fls_sync(ctx)) return s;  // surface pending async errors first
+  bool handled = false;
+  fls_status cs = comm_solve(ctx, Ab, n_rows, lda, n_features, ridge_rel, -1.0, beta, resid_norm,
+                             &handled);
+  if (handled) return cs;
+  double sqrt_mu = 0.0;
+  if (ridge_rel > 0.0) {  // reading A16: sqrt(mu) = tau ||A||_F (A without the rhs column)
+    if (lda < n_rows) return fail(FLS_EINVAL, "lda < n_rows");
+    double fro2 = 0.0;
+    if (fls_status s = frob2_host(ctx, Ab, n_rows, lda, n_features, &fro2)) return s;
+    sqrt_mu = ridge_rel * std::sqrt(fro2);
+  }
+  return solve_local(ctx, Ab, n_rows, lda, n_features, sqrt_mu, beta, resid_norm);
+}
+
+fls_status fls_solve_mu(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int64_t n_features,
+                        double sqrt_mu, double *beta, double *resid_norm) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!Ab || !beta) return fail(FLS_EINVAL, "Ab or beta is NULL");
+  if (n_features < 1) return fail(FLS_EINVAL, "n_features < 1");
+  if (n_rows < 0) return fail(FLS_EINVAL, "n_rows < 0");
+  if (!(sqrt_mu >= 0.0) || !std::isfinite(sqrt_mu)) return fail(FLS_EINVAL, "sqrt_mu must be >= 0");
+  DeviceGuard g(ctx->device);
+  if (fls_status s = fls_sync(ctx)) return s;
+  bool handled = false;
+  fls_status cs = comm_solve(ctx, Ab, n_rows, lda, n_features, 0.0, sqrt_mu, beta, resid_norm,
+                             &handled);
+  if (handled) return cs;
+  return solve_local(ctx, Ab, n_rows, lda, n_features, sqrt_mu, beta, resid_norm);
+}
+
+fls_status fls_solve_stacked(fls_ctx *ctx, const double *S, int32_t n_blocks, int64_t kb,
+                             int64_t lds, int64_t n_features, double sqrt_mu, double *beta,
+                             double *resid_norm) {
+  if (fls_status s = check_ctx(ctx)) return s;
+  if (!S || !beta) return fail(FLS_EINVAL, "S or beta is NULL");
+  if (n_features < 1 || n_blocks < 1 || kb < 1) return fail(FLS_EINVAL, "bad sizes");
+  if (lds < (int64_t)n_blocks * kb)
+    return fail(FLS_EINVAL, "lds %lld < n_blocks * kb = %lld", (long long)lds,
+                (long long)n_blocks * kb);
+  if (!(sqrt_mu >= 0.0) || !std::isfinite(sqrt_mu)) return fail(FLS_EINVAL, "sqrt_mu must be >= 0");
+  DeviceGuard g(ctx->device);
+  if (fls_status s = fls_sync(ctx)) return s;
+  return solve_stacked_impl(ctx, S, n_blocks, kb, kb, lds, n_features, sqrt_mu, beta, resid_norm);
 }
 
 }  // extern "C"
@@ -1331,14 +1342,7 @@ fls_status fls_frob2(fls_ctx *ctx, const double *A, int64_t n_rows, int64_t lda,
   if (fls_status s = check_ctx(ctx)) return s;
   if (!A || !out) return fail(FLS_EINVAL, "A or out is NULL");
   if (n_rows < 0 || n_cols < 0 || lda < n_rows) return fail(FLS_EINVAL, "bad sizes");
-  DeviceGuard g(ctx->device);
-  const int nblk = 592;  // 4 x 148 SMs, fixed -> deterministic summation order
-  cudaError_t e = launch_frob2(A, lda, n_rows, n_cols, ctx->d_scratch + 8, nblk, ctx->d_scratch,
-                               ctx->stream);
-  if (e != cudaSuccess) return cuda_fail(e, "frob2");
-  FLS_CUDA(cudaMemcpyAsync(out, ctx->d_scratch, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-  FLS_CUDA(cudaStreamSynchronize(ctx->stream));
-  return FLS_OK;
+  return frob2_host(ctx, A, n_rows, lda, n_cols, out);
 }
 
 // ---------------------------------------------------------------------------------------------

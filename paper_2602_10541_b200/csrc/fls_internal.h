@@ -147,8 +147,11 @@ cudaError_t launch_eval(int D, const EvalArgs &a, cudaStream_t st);
 cudaError_t launch_ridge_fill(double *Ab, int64_t lda, int64_t row0, int64_t F, int64_t ncols,
                               double sqrt_mu,
                               cudaStream_t st);
+// R (rows_out x n, ldr) = upper trapezoid of M's first k rows, zeros below (rows_out >= k);
+// upper_only: store only the trapezoid (R pre-zeroed, e.g. a peer's buffer: half the traffic)
 cudaError_t launch_copy_upper(const double *M, int64_t lda, int64_t k, int64_t n, double *R,
-                              int64_t ldr, cudaStream_t st);
+                              int64_t ldr, cudaStream_t st, int64_t rows_out = -1,
+                              bool upper_only = false);
 cudaError_t launch_min_abs_diag(const double *M, int64_t lda, int64_t n, double *out,
                                 cudaStream_t st);
 struct NlArgs {
@@ -200,9 +203,9 @@ cudaError_t launch_frob2(const double *A, int64_t lda, int64_t m, int64_t n, dou
 const char *qr_blocked(cublasHandle_t h, cudaStream_t st, double *A, int64_t m, int64_t n,
                        int64_t lda, double *tau, double *ws, cudaError_t *cerr,
                        cublasStatus_t *berr, int64_t grp_base = 0, int64_t grp_size = 0);
-cudaError_t launch_stack_permute(const double *S, int64_t lds, int32_t P, int64_t kb, int64_t F,
-                                 double sqrt_mu, int64_t gq, int64_t m_total, int64_t n, double *M,
-                                 int64_t ldm, cudaStream_t st);
+cudaError_t launch_stack_permute(const double *S, int64_t bs, int64_t cs, int32_t P, int64_t kb,
+                                 int64_t F, double sqrt_mu, int64_t gq, int64_t m_total, int64_t n,
+                                 double *M, int64_t ldm, cudaStream_t st);
 size_t qr_blocked_ws(int64_t m, int64_t n);  // doubles of ws (incl. nothing for tau)
 int qr_panel_width(int64_t n);
 int64_t qr_blocked_max_rows();  // taller blocks use cusolverDnDgeqrf

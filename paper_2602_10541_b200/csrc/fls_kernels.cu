@@ -376,20 +376,28 @@ cudaError_t launch_ridge_fill(double *Ab, int64_t lda, int64_t row0, int64_t F, 
   return cudaGetLastError();
 }
 
-// R (k x n, column-major, ldr) = upper trapezoid of M's first k rows
+// R (rows_out x n, column-major, ldr) = upper trapezoid of M's first k rows, zeros below.  The
+// destination may be a peer GPU's memory (CUDA IPC mapping, the TSQR exchange): the stores are
+// the transfer; with upper_only the zero part is skipped (the destination is pre-zeroed).
 __global__ void copy_upper_kernel(const double *M, int64_t lda, int64_t k, int64_t n, double *R,
-                                  int64_t ldr) {
+                                  int64_t ldr, int64_t rows_out, bool upper_only) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= k * n) return;
-  const int64_t col = idx / k, i = idx % k;
-  R[col * ldr + i] = (i <= col) ? M[col * lda + i] : 0.0;
+  if (idx >= rows_out * n) return;
+  const int64_t col = idx / rows_out, i = idx % rows_out;
+  const bool in = i <= col && i < k;
+  if (in)
+    R[col * ldr + i] = M[col * lda + i];
+  else if (!upper_only)
+    R[col * ldr + i] = 0.0;
 }
 
 cudaError_t launch_copy_upper(const double *M, int64_t lda, int64_t k, int64_t n, double *R,
-                              int64_t ldr, cudaStream_t st) {
-  const int64_t tot = k * n;
+                              int64_t ldr, cudaStream_t st, int64_t rows_out, bool upper_only) {
+  if (rows_out < 0) rows_out = k;
+  const int64_t tot = rows_out * n;
   if (tot == 0) return cudaSuccess;
-  copy_upper_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(M, lda, k, n, R, ldr);
+  copy_upper_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(M, lda, k, n, R, ldr, rows_out,
+                                                                   upper_only);
   return cudaGetLastError();
 }
 

@@ -452,22 +452,24 @@ size_t qr_blocked_ws(int64_t m, int64_t n) {
          (size_t)2 * qr_grid() * (kQrB + 1) + 2 * (kQrB + 1) + 1;  // + barrier counter
 }
 
-// Row permutation of a block-order stack of P factors (block r = rows [r kb, (r+1) kb) of S)
-// into the order qr_blocked's grouped mode expects: block 0 first, then row group i = row i of
-// blocks 1..P-1 followed by ridge row i (sqrt_mu at column i), zeros where a source is absent.
-__global__ void stack_permute_kernel(const double *S, int64_t lds, int32_t P, int64_t kb, int64_t F,
-                                     double sqrt_mu, int64_t gq, int64_t m_total, int64_t n,
-                                     double *M, int64_t ldm) {
+// Row permutation of a stack of P factors into the order qr_blocked's grouped mode expects:
+// block 0 first, then row group i = row i of blocks 1..P-1 followed by ridge row i (sqrt_mu at
+// column i), zeros where a source is absent.  Factor r's row i, column c is S[r*bs + c*cs + i]:
+// bs = kb, cs = lds for the block-row layout of fls_solve_stacked; bs = kb * n, cs = kb for the
+// block-contiguous layout the multi-rank TSQR gathers into (one contiguous factor per rank).
+__global__ void stack_permute_kernel(const double *S, int64_t bs, int64_t cs, int32_t P, int64_t kb,
+                                     int64_t F, double sqrt_mu, int64_t gq, int64_t m_total,
+                                     int64_t n, double *M, int64_t ldm) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= m_total * n) return;
   const int64_t c = idx / m_total, t = idx % m_total;
   double v = 0.0;
   if (t < kb) {
-    v = S[c * lds + t];
+    v = S[c * cs + t];
   } else {
     const int64_t u = t - kb, i = u / gq, g = u % gq;
     if (g < P - 1) {
-      if (i < kb) v = S[c * lds + (g + 1) * kb + i];
+      if (i < kb) v = S[(g + 1) * bs + c * cs + i];
     } else if (c == i && i < F) {
       v = sqrt_mu;
     }
@@ -475,13 +477,13 @@ __global__ void stack_permute_kernel(const double *S, int64_t lds, int32_t P, in
   M[c * ldm + t] = v;
 }
 
-cudaError_t launch_stack_permute(const double *S, int64_t lds, int32_t P, int64_t kb, int64_t F,
-                                 double sqrt_mu, int64_t gq, int64_t m_total, int64_t n, double *M,
-                                 int64_t ldm, cudaStream_t st) {
+cudaError_t launch_stack_permute(const double *S, int64_t bs, int64_t cs, int32_t P, int64_t kb,
+                                 int64_t F, double sqrt_mu, int64_t gq, int64_t m_total, int64_t n,
+                                 double *M, int64_t ldm, cudaStream_t st) {
   const int64_t tot = m_total * n;
   if (tot == 0) return cudaSuccess;
-  stack_permute_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(S, lds, P, kb, F, sqrt_mu, gq,
-                                                                       m_total, n, M, ldm);
+  stack_permute_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(S, bs, cs, P, kb, F, sqrt_mu,
+                                                                       gq, m_total, n, M, ldm);
   return cudaGetLastError();
 }
 

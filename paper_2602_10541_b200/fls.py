@@ -8,7 +8,8 @@ raises.
     ctx = Context()                                   # borrows torch's current stream
     W, b = fls_features(ctx, dim, F, sigma, seed)
     A, rhs = fls_assemble(ctx, W, b, blocks)         # [A | rhs] column-major, lda padded
-    beta, res = fls_solve(ctx, Ab, n_rows, lda, F)   # destroys Ab
+    beta, res = fls_solve(ctx, Ab, n_rows, lda, F, ridge_rel)   # destroys Ab; TSQR over the
+                                                               # ranks when a comm is attached
     u = fls_eval(ctx, W, b, beta, X)
 """
 from __future__ import annotations
@@ -24,7 +25,9 @@ from ._abi import FLS_COL_MAJOR, FLS_ROW_MAJOR, FlsError, check
 
 Term = Tuple[Sequence[int], float, int]   # (alpha, coef, field)
 
-__all__ = ["Context", "Block", "fls_features", "fls_assemble", "fls_features_assemble", "fls_solve", "fls_qr_r",
+__all__ = ["Context", "Block", "fls_features", "fls_assemble", "fls_features_assemble", "fls_solve",
+           "fls_solve_mu", "fls_comm_unique_id", "fls_comm_init", "fls_comm_init_host",
+           "fls_comm_destroy", "fls_comm_config", "fls_comm_info", "fls_qr_r",
            "fls_frob2", "fls_geqrf", "fls_solve_stacked", "fls_eval", "fls_eval_block", "fls_ipc_handle", "fls_ipc_open",
            "fls_ipc_close", "fls_sync", "fls_ctx_timing", "fls_ctx_timing_read",
            "fls_assemble_host", "HostBlockSet", "BlockSet", "fls_features_blocks", "QRFactor",
@@ -49,6 +52,30 @@ def _dev_f64(t: torch.Tensor, name: str) -> torch.Tensor:
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
     return t
+
+
+def _on(ctx: "Context", t: torch.Tensor, name: str) -> torch.Tensor:
+    """t must live on the ctx's device (a kernel would otherwise read another GPU's address)"""
+    if t.device.type != "cuda" or t.device.index != ctx.device:
+        raise ValueError(f"{name} is on {t.device}, the ctx on cuda:{ctx.device}")
+    return t
+
+
+def _need(t: torch.Tensor, n: int, name: str):
+    """t must hold at least n doubles (the kernels write / read that far)"""
+    if t.numel() < n:
+        raise ValueError(f"{name} holds {t.numel()} doubles; this call needs >= {n}")
+
+
+def _basis(ctx: "Context", W: torch.Tensor, b: torch.Tensor):
+    _on(ctx, _dev_f64(W, "W"), "W")
+    _on(ctx, _dev_f64(b, "b"), "b")
+    if W.dim() != 2:
+        raise ValueError("W must be (n_features, dim)")
+    F, dim = int(W.shape[0]), int(W.shape[1])
+    if b.numel() != F:
+        raise ValueError(f"b has {b.numel()} entries, W has {F} features")
+    return F, dim
 
 
 class Context:
@@ -127,6 +154,10 @@ def fls_features(ctx: Context, dim: int, n_features: int, sigma: float, seed: in
     dev = torch.device("cuda", ctx.device)
     W = torch.empty((n_features, dim), dtype=torch.float64, device=dev) if W is None else W
     b = torch.empty((n_features,), dtype=torch.float64, device=dev) if b is None else b
+    _on(ctx, _dev_f64(W, "W"), "W")
+    _on(ctx, _dev_f64(b, "b"), "b")
+    _need(W, int(n_features) * int(dim), "W")
+    _need(b, int(n_features), "b")
     check(_abi.load().fls_features(ctx.handle, int(dim), int(n_features), float(sigma),
                                    C.c_uint64(int(seed) & (2**64 - 1)), _ptr(W), _ptr(b)))
     return W, b
@@ -295,8 +326,23 @@ class BlockSet:
         self.blocks = list(blocks)
         self.ops = []
         self.arr = (_abi.fls_block * len(self.blocks))()
+        self.device = None
         for q, blk in enumerate(self.blocks):
             _dev_f64(blk.X, "X")
+            if blk.X.dim() != 2 or int(blk.X.shape[1]) != dim:
+                raise ValueError(f"block {q}: X must be (n, {dim}), got {tuple(blk.X.shape)}")
+            n = int(blk.X.shape[0])
+            for t, nm in ((blk.values, "values"), (blk.fields, "fields")):
+                if t is not None and t.device != blk.X.device:
+                    raise ValueError(f"block {q}: {nm} on {t.device}, X on {blk.X.device}")
+            if blk.values is not None and blk.values.numel() != n:
+                raise ValueError(f"block {q}: values has {blk.values.numel()} entries for {n} points")
+            if blk.fields is not None and (blk.fields.dim() != 2 or int(blk.fields.shape[0]) != n):
+                raise ValueError(f"block {q}: fields must be (n={n}, n_fields), got {tuple(blk.fields.shape)}")
+            if self.device is None:
+                self.device = blk.X.device
+            elif blk.X.device != self.device:
+                raise ValueError(f"block {q}: X on {blk.X.device}, block 0 on {self.device}")
             op = _Op(dim, blk.terms)
             self.ops.append(op)
             B = self.arr[q]
@@ -328,9 +374,7 @@ def fls_assemble(ctx: Context, W: torch.Tensor, b: torch.Tensor, blocks, *,
     (F + 1) * lda doubles; column j at Ab[j*lda : j*lda + n_local]; rhs in column F.
     extra_rows reserves rows after the local block (e.g. ridge rows for fls_solve).
     Row-major: returns (A (n_local, lda) with lda >= F, rhs (n_local,))."""
-    _dev_f64(W, "W")
-    _dev_f64(b, "b")
-    F, dim = int(W.shape[0]), int(W.shape[1])
+    F, dim = _basis(ctx, W, b)
     bs = blocks if isinstance(blocks, BlockSet) else BlockSet(blocks, dim)
     row_end = bs.total if row_end is None else int(row_end)
     n_local = row_end - int(row_begin)
@@ -349,12 +393,27 @@ def fls_assemble(ctx: Context, W: torch.Tensor, b: torch.Tensor, blocks, *,
             A = torch.empty((max(n_local, 0), lda), dtype=torch.float64, device=dev)
         if with_rhs and rhs is None:
             rhs = torch.empty((max(n_local, 0),), dtype=torch.float64, device=dev)
+    _check_outputs(ctx, bs, A, lda, rhs if with_rhs else None, F, n_local, layout)
     check(_abi.load().fls_assemble(ctx.handle, _ptr(W), _ptr(b), dim, F, int(bool(normalize)),
                                    bs.arr, len(bs.blocks), int(row_begin), row_end, _ptr(A),
                                    int(lda), int(layout), _ptr(rhs) if with_rhs else None))
     if layout == FLS_COL_MAJOR:
         return A, lda
     return A, rhs
+
+
+def _check_outputs(ctx, bs, A, lda, rhs, F, n_local, layout):
+    if bs.device is not None and (bs.device.type != "cuda" or bs.device.index != ctx.device):
+        raise ValueError(f"the blocks' tensors are on {bs.device}, the ctx on cuda:{ctx.device}")
+    _on(ctx, _dev_f64(A, "A"), "A")
+    if n_local > 0:
+        if layout == FLS_COL_MAJOR:
+            _need(A, (F - 1) * int(lda) + n_local, "A")
+        else:
+            _need(A, (n_local - 1) * int(lda) + F, "A")
+        if rhs is not None:
+            _on(ctx, _dev_f64(rhs, "rhs"), "rhs")
+            _need(rhs, n_local, "rhs")
 
 
 def fls_features_assemble(ctx: Context, dim: int, n_features: int, sigma: float, seed: int,
@@ -373,8 +432,10 @@ def fls_features_assemble(ctx: Context, dim: int, n_features: int, sigma: float,
         W = torch.empty((F, dim), dtype=torch.float64, device=dev)
     if b is None:
         b = torch.empty((F,), dtype=torch.float64, device=dev)
-    _dev_f64(W, "W")
-    _dev_f64(b, "b")
+    _on(ctx, _dev_f64(W, "W"), "W")
+    _on(ctx, _dev_f64(b, "b"), "b")
+    _need(W, F * int(dim), "W")
+    _need(b, F, "b")
     bs = blocks if isinstance(blocks, BlockSet) else BlockSet(blocks, dim)
     row_end = bs.total if row_end is None else int(row_end)
     n_local = row_end - int(row_begin)
@@ -392,6 +453,7 @@ def fls_features_assemble(ctx: Context, dim: int, n_features: int, sigma: float,
             A = torch.empty((max(n_local, 0), lda), dtype=torch.float64, device=dev)
         if rhs is None:
             rhs = torch.empty((max(n_local, 0),), dtype=torch.float64, device=dev)
+    _check_outputs(ctx, bs, A, lda, rhs, F, n_local, layout)
     check(_abi.load().fls_features_assemble(
         ctx.handle, int(dim), F, float(sigma), int(seed) & (2**64 - 1), _ptr(W), _ptr(b),
         int(bool(normalize)), bs.arr, len(bs.blocks), int(row_begin), row_end, _ptr(A), int(lda),
@@ -449,15 +511,93 @@ def fls_assemble_host(ctx: Context, W, b, blocks, A, lda: int, rhs=None, *, norm
 
 
 def fls_solve(ctx: Context, Ab: torch.Tensor, n_rows: int, lda: int, n_features: int,
-              sqrt_mu: float = 0.0, beta: Optional[torch.Tensor] = None):
-    """beta = argmin ||A beta - b||^2 + mu ||beta||^2 on the column-major [A | b] (destroyed)."""
-    _dev_f64(Ab, "Ab")
+              ridge_rel: float = 0.0, beta: Optional[torch.Tensor] = None):
+    """beta = argmin ||A beta - b||^2 + mu ||beta||^2, sqrt(mu) = ridge_rel ||A||_F (reading A16),
+    on the column-major [A | b] (destroyed).  With a communicator attached (fls_comm_init*),
+    Ab is this rank's rows and the call runs TSQR over the ranks; beta is replicated.
+    Returns (beta, residual norm)."""
+    _on(ctx, _dev_f64(Ab, "Ab"), "Ab")
+    _need(Ab, int(n_features) * int(lda) + int(n_rows), "Ab")
     if beta is None:
         beta = torch.empty((n_features,), dtype=torch.float64, device=Ab.device)
+    _need(_on(ctx, _dev_f64(beta, "beta"), "beta"), int(n_features), "beta")
     res = C.c_double(0.0)
     check(_abi.load().fls_solve(ctx.handle, _ptr(Ab), int(n_rows), int(lda), int(n_features),
-                                float(sqrt_mu), _ptr(beta), C.byref(res)))
+                                float(ridge_rel), _ptr(beta), C.byref(res)))
     return beta, res.value
+
+
+def fls_solve_mu(ctx: Context, Ab: torch.Tensor, n_rows: int, lda: int, n_features: int,
+                 sqrt_mu: float = 0.0, beta: Optional[torch.Tensor] = None):
+    """fls_solve with an ABSOLUTE sqrt(mu) (the Newton step's Tikhonov term)"""
+    _on(ctx, _dev_f64(Ab, "Ab"), "Ab")
+    _need(Ab, int(n_features) * int(lda) + int(n_rows), "Ab")
+    if beta is None:
+        beta = torch.empty((n_features,), dtype=torch.float64, device=Ab.device)
+    _need(_on(ctx, _dev_f64(beta, "beta"), "beta"), int(n_features), "beta")
+    res = C.c_double(0.0)
+    check(_abi.load().fls_solve_mu(ctx.handle, _ptr(Ab), int(n_rows), int(lda), int(n_features),
+                                   float(sqrt_mu), _ptr(beta), C.byref(res)))
+    return beta, res.value
+
+
+_TRANSPORTS = {"auto": _abi.FLS_TSQR_AUTO, "p2p": _abi.FLS_TSQR_P2P, "nccl": _abi.FLS_TSQR_NCCL}
+_TRANSPORT_NAMES = {0: None, _abi.FLS_TSQR_P2P: "p2p", _abi.FLS_TSQR_NCCL: "nccl"}
+
+
+def fls_comm_unique_id() -> bytes:
+    """an NCCL unique id (rank 0 creates it; the caller distributes it to the other ranks)"""
+    buf = (C.c_char * _abi.FLS_COMM_ID_BYTES)()
+    check(_abi.load().fls_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def fls_comm_init(ctx: Context, uid: bytes, nranks: int, rank: int):
+    """attach an NCCL communicator (blocks until every rank has called it)"""
+    if len(uid) != _abi.FLS_COMM_ID_BYTES:
+        raise ValueError(f"uid must be {_abi.FLS_COMM_ID_BYTES} bytes")
+    buf = (C.c_char * _abi.FLS_COMM_ID_BYTES).from_buffer_copy(uid)
+    check(_abi.load().fls_comm_init(ctx.handle, buf, int(nranks), int(rank)))
+
+
+def fls_comm_init_host(ctx: Context, nranks: int, rank: int, allgather):
+    """attach a communicator whose control plane is the Python callable
+    allgather(data: bytes) -> bytes (nranks * len(data) bytes, rank order); the R factors move
+    by peer memory (CUDA IPC)"""
+    n = int(nranks)
+
+    def _cb(user, send, recv, nbytes):
+        try:
+            out = allgather(C.string_at(send, nbytes))
+            if len(out) != n * nbytes:
+                return 1
+            C.memmove(recv, out, len(out))
+            return 0
+        except Exception:           # a Python error must not unwind through C
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    fn = _abi.HOST_ALLGATHER(_cb)
+    coll = _abi.fls_host_coll(None, fn)
+    check(_abi.load().fls_comm_init_host(ctx.handle, n, int(rank), C.byref(coll)))
+    ctx._comm_keep = (fn, coll, allgather)       # the C side keeps calling fn
+
+
+def fls_comm_destroy(ctx: Context):
+    check(_abi.load().fls_comm_destroy(ctx.handle))
+    ctx._comm_keep = None
+
+
+def fls_comm_config(ctx: Context, transport: str = "auto", force_tsqr: bool = False):
+    check(_abi.load().fls_comm_config(ctx.handle, _TRANSPORTS[transport], int(bool(force_tsqr))))
+
+
+def fls_comm_info(ctx: Context):
+    """(nranks, rank, transport of the last solve: None / "p2p" / "nccl")"""
+    a, b, c = C.c_int32(), C.c_int32(), C.c_int32()
+    check(_abi.load().fls_comm_info(ctx.handle, C.byref(a), C.byref(b), C.byref(c)))
+    return a.value, b.value, _TRANSPORT_NAMES.get(c.value, c.value)
 
 
 def fls_solve_stacked(ctx: Context, S: torch.Tensor, n_blocks: int, kb: int, lds: int,
@@ -520,6 +660,9 @@ def fls_ipc_close(ctx: Context, ptr: int):
 
 
 def fls_frob2(ctx: Context, A: torch.Tensor, n_rows: int, lda: int, n_cols: int) -> float:
+    _on(ctx, _dev_f64(A, "A"), "A")
+    if n_rows > 0 and n_cols > 0:
+        _need(A, (int(n_cols) - 1) * int(lda) + int(n_rows), "A")
     out = C.c_double(0.0)
     check(_abi.load().fls_frob2(ctx.handle, _ptr(A), int(n_rows), int(lda), int(n_cols),
                                 C.byref(out)))
@@ -530,12 +673,13 @@ def fls_eval_block(ctx: Context, W: torch.Tensor, b: torch.Tensor, beta: torch.T
                    normalize: bool = True, out: Optional[torch.Tensor] = None) -> torch.Tensor:
     """A_block @ beta for one row block (its operator, coefficient fields and weight), without
     materialising A"""
-    for t, nm in ((W, "W"), (b, "b"), (beta, "beta")):
-        _dev_f64(t, nm)
-    F, dim = int(W.shape[0]), int(W.shape[1])
+    F, dim = _basis(ctx, W, b)
+    _need(_on(ctx, _dev_f64(beta, "beta"), "beta"), F, "beta")
     bs = BlockSet([block], dim)
+    _on(ctx, block.X, "block.X")
     if out is None:
         out = torch.empty((block.n,), dtype=torch.float64, device=W.device)
+    _need(_on(ctx, _dev_f64(out, "out"), "out"), block.n, "out")
     check(_abi.load().fls_eval_block(ctx.handle, _ptr(W), _ptr(b), dim, F, int(bool(normalize)),
                                      _ptr(beta), bs.arr, _ptr(out)))
     return out
@@ -544,12 +688,16 @@ def fls_eval_block(ctx: Context, W: torch.Tensor, b: torch.Tensor, beta: torch.T
 def fls_eval(ctx: Context, W: torch.Tensor, b: torch.Tensor, beta: torch.Tensor, X: torch.Tensor,
              terms: Optional[Sequence[Term]] = None, normalize: bool = True,
              out: Optional[torch.Tensor] = None) -> torch.Tensor:
-    for t, nm in ((W, "W"), (b, "b"), (beta, "beta"), (X, "X")):
-        _dev_f64(t, nm)
-    F, dim = int(W.shape[0]), int(W.shape[1])
+    F, dim = _basis(ctx, W, b)
+    for t, nm in ((beta, "beta"), (X, "X")):
+        _on(ctx, _dev_f64(t, nm), nm)
+    _need(beta, F, "beta")
+    if X.dim() != 2 or int(X.shape[1]) != dim:
+        raise ValueError(f"X must be (n, {dim}), got {tuple(X.shape)}")
     n = int(X.shape[0])
     if out is None:
         out = torch.empty((n,), dtype=torch.float64, device=X.device)
+    _need(_on(ctx, _dev_f64(out, "out"), "out"), n, "out")
     op = _Op(dim, terms) if terms is not None else None
     check(_abi.load().fls_eval(ctx.handle, _ptr(W), _ptr(b), dim, F, int(bool(normalize)),
                                _ptr(beta), C.pointer(op.op) if op else None, _ptr(X), n, _ptr(out)))

@@ -3,7 +3,8 @@
     W_j = L W^_j  (scalar: L = sigma I;  anisotropic: lower-triangular Cholesky factor)
     beta* = argmin ||A(L) beta - b||^2            (inner exact solve, fls_solve)
     Lout  = ||A(L) beta* - b||^2                  (outer loss)
-    dLout/dL via fls_bandwidth_grad (no differentiation through the solve: beta* is optimal)
+    dLout/dL via fls_bandwidth_grad (no differentiation through the solve: beta* is optimal;
+    with a ridge the loss gains mu ||beta*||^2 so that this stays exact, reading B2)
     AdamW on the d(d+1)/2 (or 1) bandwidth parameters
 
 Every arithmetic step on F- or R-sized data is a libfls call; the optimiser updates the
@@ -22,13 +23,15 @@ from . import fls
 
 def outer_loss_and_grad(ctx, L, W_hat, b, blocks: Sequence[fls.Block], sqrt_mu: float = 0.0,
                         normalize: bool = True):
-    """(Lout, dLout/dL (d x d), beta) at the factor L"""
+    """(Lout, dLout/dL (d x d), beta) at the factor L.  With sqrt_mu > 0 the loss is the
+    ridge-augmented Lout + mu ||beta*||^2 -- the objective the inner solve minimises -- whose
+    gradient the envelope formula gives exactly (reading B2); at mu = 0 it is Lout."""
     F, d = int(W_hat.shape[0]), int(W_hat.shape[1])
     W = fls.fls_features_transform(ctx, L, W_hat)
     R = sum(blk.n for blk in blocks)
     extra = F if sqrt_mu > 0 else 0
     Ab, lda = fls.fls_assemble(ctx, W, b, blocks, normalize=normalize, extra_rows=extra)
-    beta, _ = fls.fls_solve(ctx, Ab, R, lda, F, sqrt_mu)
+    beta, _ = fls.fls_solve_mu(ctx, Ab, R, lda, F, sqrt_mu)
     loss = 0.0
     rblocks = []
     for blk in blocks:
@@ -37,6 +40,8 @@ def outer_loss_and_grad(ctx, L, W_hat, b, blocks: Sequence[fls.Block], sqrt_mu: 
         r = fls.fls_axpy(ctx, -blk.weight, vals, Abeta)                        # w (L[u] - v)
         loss += fls.fls_frob2(ctx, r, r.numel(), max(r.numel(), 1), 1) if r.numel() else 0.0
         rblocks.append(fls.Block(blk.X, blk.terms, blk.weight, r, blk.fields))
+    if sqrt_mu > 0:
+        loss += sqrt_mu * sqrt_mu * fls.fls_frob2(ctx, beta, F, F, 1)
     G = fls.fls_bandwidth_grad(ctx, W, W_hat, b, rblocks, beta, normalize=normalize)
     return loss, G, beta
 

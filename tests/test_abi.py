@@ -9,6 +9,8 @@ import pytest
 from paper_2602_10541_b200 import _abi
 from paper_2602_10541_b200.build import LIB, build
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
 
 @pytest.fixture(scope="module")
 def lib():
@@ -30,7 +32,7 @@ def test_library_exports_every_header_symbol(lib):
 
 
 def test_api_version_and_status_strings(lib):
-    assert lib.fls_api_version() == 2
+    assert lib.fls_api_version() == 3
     for k, v in _abi.STATUS.items():
         assert lib.fls_status_string(k).decode() == v
 
@@ -90,3 +92,26 @@ def test_missing_library_fails_loudly(tmp_path):
     env = dict(os.environ, FLS_LIB=str(tmp_path / "libfls_missing.so"))
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=120)
     assert "RAISED FlsError" in r.stdout, r.stdout + r.stderr
+
+
+def test_nccl_missing_gives_fls_enccl():
+    """FLS_ENCCL is reachable: libfls loads NCCL at run time; a missing library is reported, not
+    a load failure of libfls itself (subprocess: the loader runs once per process)"""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2602_10541_b200 import fls\n"
+            "try:\n    fls.fls_comm_unique_id()\n    print('no error')\n"
+            "except fls.FlsError as e:\n    print(e.name, str(e))\n") % ROOT
+    env = dict(os.environ, FLS_NCCL_LIB="/nonexistent/libnccl.so.2")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.startswith("FLS_ENCCL") and "cannot load NCCL" in r.stdout
+
+
+def test_nccl_unique_id_on_host():
+    """with NCCL present, the unique id needs no GPU: 128 bytes, fresh per call"""
+    from paper_2602_10541_b200 import fls
+    a, b = fls.fls_comm_unique_id(), fls.fls_comm_unique_id()
+    assert len(a) == len(b) == 128 and a != b

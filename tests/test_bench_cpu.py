@@ -66,3 +66,43 @@ def test_clock_sampler_keeps_timed_window_and_flags_reasons():
     out = c.stop()                       # nothing inside the window: every sample counts
     assert out["window"] == "sampler lifetime" and out["samples"] == 5
     assert out["reasons"] == ["sw_power_cap", "sw_thermal_slowdown"]
+
+
+def _bench(args, env_extra, timeout=600):
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env.update(env_extra)
+    return subprocess.run([sys.executable, "bench.py"] + args, cwd=ROOT, capture_output=True,
+                          text=True, timeout=timeout, env=env)
+
+
+FAKE = {"FLS_BENCH_ENGINE": "tests/fake_bench_engine.py:FakeEngine"}
+
+
+def test_gpus_flag_spawns_one_rank_per_device():
+    """`bench.py --gpus 2` without a launcher starts 2 ranks itself (torch.distributed.run);
+    exactly one JSON line, n_gpus = distinct devices = 2, time = max over ranks"""
+    r = _bench(["--gpus", "2", "--steps", "5", "--warmup", "3"], dict(FAKE, FAKE_GPUS="2"))
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = _json_lines(r.stdout)
+    assert len(lines) == 1, r.stdout
+    j = lines[0]
+    assert j["n_gpus"] == 2 and j["ranks"] == 2 and j["steps"] == 5 and j["warmup"] == 3
+    assert j["ms_per_step"] >= 2.0                    # rank 1 sleeps 2 ms per step: the max
+    assert j["value"] == 2_000_000 / (j["ms_per_step"] / 1e3)
+    assert j["config"]["ranks_reported"] == 2 and j["warmup_and_steps_done_rank0"] == 8
+
+
+def test_gpus_flag_fails_loudly_without_enough_devices():
+    r = _bench(["--gpus", "4", "--steps", "1"], dict(FAKE, FAKE_GPUS="2"))
+    assert r.returncode == 2 and "needs 4 GPUs" in r.stderr and not _json_lines(r.stdout)
+    # the real engine on this GPU-less box
+    r = _bench(["--gpus", "2", "--steps", "1"], {})
+    assert r.returncode == 2 and "needs 2 GPUs" in r.stderr
+
+
+def test_world_size_must_match_gpus_and_devices_must_be_distinct():
+    r = _bench(["--gpus", "1", "--steps", "1"], dict(FAKE, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0"))
+    assert r.returncode == 2 and "WORLD_SIZE=2" in r.stderr
+    r = _bench(["--gpus", "2", "--steps", "2", "--warmup", "3"],
+               dict(FAKE, FAKE_GPUS="2", FAKE_SAME_DEVICE="1"))
+    assert r.returncode != 0 and "share 1 device" in r.stderr and not _json_lines(r.stdout)

@@ -447,10 +447,13 @@ def test_solve_and_eval_parity(ctx, name, size):
     F, R = p.n_features, p.n_rows
     ridge = p.ridge_rel > 0
     Ab, lda = fls.fls_assemble(ctx, Wd, bd, dev_blocks(p), extra_rows=F if ridge else 0)
-    sq = 0.0
+    if ridge:   # the relative ridge computed inside libfls == the absolute one from fls_frob2
+        Ab2 = Ab.clone()
+        sq = p.ridge_rel * math.sqrt(fls.fls_frob2(ctx, Ab2, R, lda, F))
+        beta2, res2 = fls.fls_solve_mu(ctx, Ab2, R, lda, F, sq)
+    beta, res = fls.fls_solve(ctx, Ab, R, lda, F, p.ridge_rel)   # sqrt(mu) = tau ||A||_F inside
     if ridge:
-        sq = p.ridge_rel * math.sqrt(fls.fls_frob2(ctx, Ab, R, lda, F))
-    beta, res = fls.fls_solve(ctx, Ab, R, lda, F, sq)
+        assert torch.equal(beta, beta2) and res == res2
     Xt = p.test_points(10_000)
     u_gpu = fls.fls_eval(ctx, Wd, bd, beta, torch.from_numpy(Xt).cuda()).cpu().numpy()
     # oracle chain
@@ -589,8 +592,7 @@ def test_full_size_solve_parity_with_oracle_artifact(ctx, name):
     F, R = p.n_features, p.n_rows
     ridge = p.ridge_rel > 0
     Ab, lda = fls.fls_assemble(ctx, Wd, bd, dev_blocks(p), extra_rows=F if ridge else 0)
-    sq = p.ridge_rel * math.sqrt(fls.fls_frob2(ctx, Ab, R, lda, F)) if ridge else 0.0
-    beta, _ = fls.fls_solve(ctx, Ab, R, lda, F, sq)
+    beta, _ = fls.fls_solve(ctx, Ab, R, lda, F, p.ridge_rel)
     del Ab
     torch.cuda.empty_cache()
     Xt = p.test_points(10_000)

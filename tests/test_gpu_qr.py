@@ -118,8 +118,7 @@ def test_solve_parity_with_oracle_on_both_qr_paths(ctx, name, size):
     F, R = p.n_features, p.n_rows
     ridge = p.ridge_rel > 0
     Ab, lda = fls.fls_assemble(ctx, Wd, bd, dev_blocks(p), extra_rows=F if ridge else 0)
-    sq = p.ridge_rel * math.sqrt(fls.fls_frob2(ctx, Ab, R, lda, F)) if ridge else 0.0
-    beta, _ = fls.fls_solve(ctx, Ab, R, lda, F, sq)
+    beta, _ = fls.fls_solve(ctx, Ab, R, lda, F, p.ridge_rel)
     Xt = p.test_points(10_000)
     u_gpu = fls.fls_eval(ctx, Wd, bd, beta, torch.from_numpy(Xt).cuda()).cpu().numpy()
     Ao, ro, _ = oracle.assemble(W, b, p.blocks, want_scale=False)
@@ -150,7 +149,7 @@ def test_solve_stacked_matches_dense_solve(ctx, P, kb, n, ridge):
     ld = ((lds + F + 3) // 4) * 4
     M = torch.zeros(((F + 1) * ld,), dtype=torch.float64, device="cuda")
     M.view(F + 1, ld)[:, :lds] = Sv
-    beta_d, res_d = fls.fls_solve(ctx, M, lds, ld, F, sq)
+    beta_d, res_d = fls.fls_solve_mu(ctx, M, lds, ld, F, sq)
     assert float(torch.linalg.norm(beta_s - beta_d) / torch.linalg.norm(beta_d)) <= 1e-10
     assert abs(res_s - res_d) <= 1e-10 * max(res_d, 1e-300)
     assert torch.equal(Sv[:, :1], S.view(F + 1, lds)[:, :1])   # S not modified (spot check)
@@ -187,5 +186,5 @@ def test_solve_zero_column_is_erank(ctx):
     M2 = M.clone()
     with pytest.raises(fls.FlsError, match="ERANK"):
         fls.fls_solve(ctx, M, m, ld, n, 0.0)
-    beta, _ = fls.fls_solve(ctx, M2, m, ld, n, 1e-6)
+    beta, _ = fls.fls_solve_mu(ctx, M2, m, ld, n, 1e-6)
     assert bool(torch.isfinite(beta).all()) and abs(float(beta[17])) <= 1e-6 * float(beta.abs().max())

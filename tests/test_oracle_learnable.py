@@ -60,3 +60,31 @@ def test_gradient_with_coefficient_field_matches_fd():
                                  fields=None), p.blocks[1]]
     _, G0, _ = ol.outer_grad(L, W_hat, b, const)
     assert np.abs(G0 - G).max() > 1e-3 * np.abs(G).max()
+
+
+def test_ridge_augmented_gradient_matches_fd():
+    """reading B2: with a Tikhonov inner solve the outer loss is ||A beta* - b||^2 + mu ||beta*||^2
+    and the envelope gradient is its exact derivative -- brute force by central FD; the plain
+    residual loss (without mu ||beta||^2) would NOT match at this mu"""
+    p, W_hat, b = _setup()
+    sq = 3e-2
+    L = np.array([[3.0, 0.0], [0.7, 4.0]])
+    loss, G, beta = ol.outer_grad(L, W_hat, b, p.blocks, sqrt_mu=sq)
+    for (k, l) in [(0, 0), (1, 0), (1, 1)]:
+        h = 1e-5
+        Lp, Lm = L.copy(), L.copy()
+        Lp[k, l] += h
+        Lm[k, l] -= h
+        fd = (ol.outer_loss(Lp, W_hat, b, p.blocks, sqrt_mu=sq)[0]
+              - ol.outer_loss(Lm, W_hat, b, p.blocks, sqrt_mu=sq)[0]) / (2 * h)
+        assert abs(G[k, l] - fd) <= 1e-5 * max(abs(fd), abs(G).max()), (k, l, G[k, l], fd)
+    # the residual part alone differs from its FD by the dropped -2 mu beta^T dbeta/dL term
+    def res_only(Lm_):
+        lo, _, bt, _ = ol.outer_loss(Lm_, W_hat, b, p.blocks, sqrt_mu=sq)
+        return lo - sq * sq * float(bt @ bt)
+    h = 1e-5
+    Lp, Lm = L.copy(), L.copy()
+    Lp[1, 1] += h
+    Lm[1, 1] -= h
+    fd_res = (res_only(Lp) - res_only(Lm)) / (2 * h)
+    assert abs(G[1, 1] - fd_res) > 1e-3 * abs(G).max()

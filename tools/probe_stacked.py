@@ -43,7 +43,7 @@ def main(Ps):
         ld = ((lds + F + 3) // 4) * 4
         M = torch.zeros((n * ld,), dtype=torch.float64, device="cuda")
         M.view(n, ld)[:, :lds] = Sv
-        ms_d, (b_d, r_d) = timed(lambda: fls.fls_solve(ctx, M, lds, ld, F, sq))
+        ms_d, (b_d, r_d) = timed(lambda: fls.fls_solve_mu(ctx, M, lds, ld, F, sq))
         out[f"P={P}"] = {"stacked_ms": ms_s, "dense_ms": ms_d,
                          "beta_rel_diff": float(torch.linalg.norm(b_s - b_d) / torch.linalg.norm(b_d)),
                          "resid_stacked": r_s, "resid_dense": r_d}
