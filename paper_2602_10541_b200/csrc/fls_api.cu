@@ -113,6 +113,9 @@ fls_status fail(fls_status s, const char *fmt, ...) {
 }
 
 fls_status cuda_fail(cudaError_t e, const char *where) {
+  // reset the runtime's (non-sticky) last error, so that a failed call here is not reported
+  // again by the next launch's cudaGetLastError() in this thread
+  cudaGetLastError();
   return fail(FLS_ECUDA, "%s: %s", where, cudaGetErrorString(e));
 }
 

@@ -406,13 +406,16 @@ def _check_outputs(ctx, bs, A, lda, rhs, F, n_local, layout):
     if bs.device is not None and (bs.device.type != "cuda" or bs.device.index != ctx.device):
         raise ValueError(f"the blocks' tensors are on {bs.device}, the ctx on cuda:{ctx.device}")
     _on(ctx, _dev_f64(A, "A"), "A")
-    if n_local > 0:
+    if rhs is not None:
+        _on(ctx, _dev_f64(rhs, "rhs"), "rhs")
+    # (an lda too small for the layout is the C ABI's FLS_EINVAL, reported by the call)
+    lda_ok = int(lda) >= (n_local if layout == FLS_COL_MAJOR else F)
+    if n_local > 0 and lda_ok:
         if layout == FLS_COL_MAJOR:
             _need(A, (F - 1) * int(lda) + n_local, "A")
         else:
             _need(A, (n_local - 1) * int(lda) + F, "A")
         if rhs is not None:
-            _on(ctx, _dev_f64(rhs, "rhs"), "rhs")
             _need(rhs, n_local, "rhs")
 
 

@@ -79,7 +79,7 @@ def test_nccl_comm_world1_forced_tsqr(name, transport):
     u_o = _oracle_u(p)
     assert np.linalg.norm(u - u_o) / np.linalg.norm(u_o) <= 1e-6
     assert np.linalg.norm(u - u_d) / np.linalg.norm(u_d) <= 1e-9
-    assert abs(res - res_d) <= 1e-9 * max(abs(res_d), 1e-300)
+    assert abs(res - res_d) <= 1e-9 * max(abs(res_d), 1e-2)
     ctx.close()
 
 
@@ -224,7 +224,8 @@ def test_p2p_tsqr_across_processes_matches_dense_and_oracle(name, world):
         assert np.linalg.norm(u - u_o) / np.linalg.norm(u_o) <= 1e-6
         assert np.linalg.norm(u - u_d) / np.linalg.norm(u_d) <= 1e-9
         assert np.array_equal(u, out[0][0]) and res == out[0][1]   # replicated
-    assert abs(out[0][1] - res_d) <= 1e-9 * max(abs(res_d), 1e-300)
+    # the residual norm is a rounding-level number on C1 (~1e-12): compare on the rhs's scale
+    assert abs(out[0][1] - res_d) <= 1e-9 * max(abs(res_d), 1e-2)
     ctx.close()
 
 
@@ -245,3 +246,17 @@ def test_ipc_errors():
     assert len(h) == 64 and off >= 80 and off % 8 == 0      # offset of t[10:] in its allocation
     with pytest.raises(fls.FlsError, match="ECUDA"):
         fls.fls_ipc_open(ctx, h)
+
+
+def test_failed_runtime_call_does_not_poison_the_next_launch():
+    """a CUDA failure inside libfls (here: opening this process's own IPC handle) resets the
+    runtime's last-error state, so the next kernel launch succeeds"""
+    from paper_2602_10541_b200 import fls
+    ctx = fls.Context(0)
+    t = torch.zeros(64, dtype=torch.float64, device="cuda")
+    h, _ = fls.fls_ipc_handle(ctx, t)
+    with pytest.raises(fls.FlsError, match="ECUDA"):
+        fls.fls_ipc_open(ctx, h)
+    W, b = fls.fls_features(ctx, 2, 16, 1.0, 0)     # launches a kernel, checks cudaGetLastError
+    fls.fls_sync(ctx)
+    ctx.close()

@@ -782,3 +782,31 @@ def test_pdl_off_gives_identical_entries(ctx, tmp_path):
     for key in ("A", "A2"):
         a, b = (o[key][: (F + 1) * lda].view(F + 1, lda)[:, :R] for o in outs)
         assert torch.equal(a, b), key
+
+
+def test_binding_rejects_wrong_shapes_and_small_buffers(ctx):
+    """the thin binding validates what the C ABI cannot see (tensor sizes, shapes, devices)
+    before the call: a wrong shape or a short buffer would otherwise be written out of bounds"""
+    p = wl.make_problem("c1_poisson1d", "mini")
+    _, _, Wd, bd = _parity_feats(p)
+    blocks = dev_blocks(p)
+    F, R = p.n_features, p.n_rows
+    with pytest.raises(ValueError, match="X must be"):
+        fls.fls_assemble(ctx, Wd, bd, [fls.Block(blocks[0].X.view(-1, 1).repeat(1, 2), blocks[0].terms)])
+    with pytest.raises(ValueError, match="values has"):
+        fls.fls_assemble(ctx, Wd, bd, [fls.Block(blocks[0].X, blocks[0].terms, 1.0, blocks[0].values[:-1])])
+    with pytest.raises(ValueError, match="fields must be"):
+        fls.fls_assemble(ctx, Wd, bd, [fls.Block(blocks[0].X, blocks[0].terms, 1.0, None,
+                                                 torch.ones((3, 1), dtype=torch.float64, device="cuda"))])
+    with pytest.raises(ValueError, match="b has"):
+        fls.fls_assemble(ctx, Wd, bd[:-1], blocks)
+    lda = fls.round_up(R, 4)
+    short = torch.empty((F * lda,), dtype=torch.float64, device="cuda")      # no room for column F
+    with pytest.raises(ValueError, match="rhs holds"):
+        fls.fls_assemble(ctx, Wd, bd, blocks, A=short, lda=lda)
+    with pytest.raises(ValueError, match="A holds"):
+        fls.fls_assemble(ctx, Wd, bd, blocks, A=short[: (F - 1) * lda], lda=lda, with_rhs=False)
+    with pytest.raises(ValueError, match="beta holds"):
+        fls.fls_eval(ctx, Wd, bd, torch.zeros(F - 1, dtype=torch.float64, device="cuda"), blocks[0].X)
+    with pytest.raises(ValueError, match="Ab holds"):
+        fls.fls_solve(ctx, short[:100], R, lda, F)
