@@ -66,6 +66,16 @@ extern "C" {
 #define FLS_MAX_TERMS 64   /* terms per operator */
 #define FLS_MAX_FIELDS 4   /* coefficient fields per block */
 #define FLS_MAX_FEAT_BLOCKS 16 /* bandwidth blocks of a multi-block basis */
+/* Phase range: every phase z_ij = W_j . x_i + b_j the assembly / eval kernels evaluate (b_j
+ * including the amplitude/phase fold's shift, |psi| <= pi) must satisfy |z_ij| <= FLS_MAX_PHASE.
+ * The kernels reduce z in half turns (z / pi - rint(z / pi)) exactly, but z itself carries the
+ * rounding of W_j . x_i + b_j, so an entry's error grows like pi ulp(|z| / pi): <= ~4e-14 of its
+ * term-magnitude scale at |z| <= 60 (the BASELINE configs), ~1e-12 at |z| ~ 2e3, ~5e-12 at the
+ * limit.  Beyond it the call still completes but the next fls_sync (or fls_solve) returns
+ * FLS_EUNSUPPORTED and the affected entries are unspecified.  The check is exact (|z| itself,
+ * not a bound) and costs nothing on the entry path: a per-CTA bound ||W_j||_1 ||x_i||_inf +
+ * |b_j| selects the rows that are re-checked. */
+#define FLS_MAX_PHASE 1.0e4
 
 typedef enum {
     FLS_OK = 0,
@@ -100,7 +110,8 @@ FLS_API fls_status fls_ctx_destroy(fls_ctx *ctx);
  * ctx's workspace is never used by both streams at once.  Errors: FLS_EINVAL, FLS_ECUDA. */
 FLS_API fls_status fls_ctx_set_stream(fls_ctx *ctx, void *cuda_stream);
 /* block until the ctx stream is idle; returns FLS_ENONFINITE (and clears the flag) if a
- * kernel saw a non-finite input since the last check, FLS_ECUDA on an asynchronous fault. */
+ * kernel saw a non-finite input since the last check, FLS_EUNSUPPORTED if a phase exceeded
+ * FLS_MAX_PHASE, FLS_ECUDA on an asynchronous fault. */
 FLS_API fls_status fls_sync(fls_ctx *ctx);
 /* measurement hook: with enable != 0 every assembly-kernel launch of fls_assemble is bracketed
  * by CUDA events on the ctx stream (the prefactor kernel is not included).  timing_read

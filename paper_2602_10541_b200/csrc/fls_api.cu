@@ -244,7 +244,11 @@ fls_status fls_sync(fls_ctx *ctx) {
   if (h) {
     FLS_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(unsigned), ctx->stream));
     FLS_CUDA(cudaStreamSynchronize(ctx->stream));
-    return fail(FLS_ENONFINITE, "non-finite value in an input (W, b, X, values or fields)");
+    if (h & 1u)
+      return fail(FLS_ENONFINITE, "non-finite value in an input (W, b, X, values or fields)");
+    return fail(FLS_EUNSUPPORTED, "a phase |W_j . x_i + b_j| exceeds FLS_MAX_PHASE = %g (the "
+                "half-turn range reduction loses accuracy as ulp(|z|); entries unspecified)",
+                (double)FLS_MAX_PHASE);
   }
   return FLS_OK;
 }

@@ -31,6 +31,21 @@ __global__ void __launch_bounds__(kRmNT, asm_min_blocks<D, G, KM>()) assemble_rm
     rec1[s] = jin1 ? __ldg(a.pf + (j + 1) * S + s) : 0.0;
   }
   const bool pair_ok = a.vec && jin1;
+  // phase-range guard (FLS_MAX_PHASE): feature side from the thread's two records, row side
+  // max-reduced over the staged rows (s_xinf); exact re-check only past the bound
+  __shared__ unsigned long long s_xinf;
+  double w1 = 0.0, bb = 0.0;
+  {
+    double w0 = 0.0, w1b = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      w0 += fabs(rec0[k]);
+      w1b += fabs(rec1[k]);
+    }
+    w1 = fmax(w0, w1b);
+    bb = fmax(fabs(rec0[D]), fabs(rec1[D]));
+  }
+  if (threadIdx.x == 0) s_xinf = 0ull;
   const int64_t r0 = a.lr0 + (int64_t)blockIdx.y * a.fpc;
   const int64_t r1 = r0 + a.fpc < a.lr1 ? r0 + a.fpc : a.lr1;
   bool bad = false;
@@ -45,6 +60,7 @@ __global__ void __launch_bounds__(kRmNT, asm_min_blocks<D, G, KM>()) assemble_rm
       else v = G > 0 ? __ldg(a.fields + i * a.nf + a.gfield[k - D]) : 0.0;
       bad |= !finite(v);
       xs[t] = v;
+      if (k < D) atomicMax(&s_xinf, (unsigned long long)__double_as_longlong(fabs(v)));
     }
     if (blockIdx.x == 0 && a.rhs != nullptr) {
       for (int rr = threadIdx.x; rr < nrow; rr += kRmNT) {
@@ -72,7 +88,24 @@ __global__ void __launch_bounds__(kRmNT, asm_min_blocks<D, G, KM>()) assemble_rm
       }
     }
   }
-  if (bad) atomicOr(a.err, 1u);
+  if (bad) atomicOr(a.err, kErrNonFinite);
+  __syncthreads();
+  if (fma(w1, __longlong_as_double((long long)s_xinf), bb) > kMaxHalfTurns) {
+    for (int64_t r = r0; r < r1; ++r) {   // exact re-check of this thread's two features
+      const int64_t i = a.pt0 + (r - a.lr0);
+      double h0 = rec0[D], h1 = rec1[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const double xv = __ldg(a.X + i * D + k);
+        h0 = fma(rec0[k], xv, h0);
+        h1 = fma(rec1[k], xv, h1);
+      }
+      if ((jin0 && !(fabs(h0) <= kMaxHalfTurns)) || (jin1 && !(fabs(h1) <= kMaxHalfTurns))) {
+        atomicOr(a.err, kErrPhaseRange);
+        break;
+      }
+    }
+  }
 }
 
 template <int D, int G, int KM>

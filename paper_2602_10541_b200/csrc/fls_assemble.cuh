@@ -147,6 +147,27 @@ __device__ __forceinline__ void store_full(double *colp, const double (&o)[NQ]) 
   }
 }
 
+// exact phase-range check of one thread's rows against features [f0, f1) (only threads whose
+// bound exceeded the limit run it): h as EntryMath::entry computes it
+template <int D, int S, int NQ>
+__device__ __forceinline__ void phase_check(const double *pf, int64_t f0, int64_t f1,
+                                         const double (&x)[NQ][D], const bool (&in)[NQ],
+                                         unsigned *err) {
+  for (int64_t j = f0; j < f1; ++j) {
+    const double *r = pf + j * S;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      double h = __ldg(r + D);
+#pragma unroll
+      for (int k = 0; k < D; ++k) h = fma(__ldg(r + k), x[q][k], h);
+      if (in[q] && !(fabs(h) <= kMaxHalfTurns)) {
+        atomicOr(err, kErrPhaseRange);
+        return;
+      }
+    }
+  }
+}
+
 // One launch covers up to kMaxBatch row blocks that share the kernel variant (e.g. a PDE block
 // and its identity BC / IC blocks): the 1-D grid is the concatenation of each block's
 // (row tile, feature group) CTAs, row tile fastest.
@@ -195,7 +216,17 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
       a.rhs[r] = a.weight * v;
     }
   }
-  if (bad) atomicOr(a.err, 1u);
+  if (bad) atomicOr(a.err, kErrNonFinite);
+  // phase-range guard (FLS_MAX_PHASE): |h_ij| <= ||W_j/pi||_1 ||x_i||_inf + |b'_j/pi|.  The
+  // feature side is max-reduced over the CTA's records chunk by chunk (s_guard, off the entry
+  // path); at the end a thread whose bound exceeds the limit re-checks its rows exactly.
+  __shared__ unsigned long long s_guard[2];
+  double xinf = 0.0;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+#pragma unroll
+    for (int k = 0; k < D; ++k) xinf = fmax(xinf, fabs(x[q][k]));
+  if (threadIdx.x == 0) s_guard[0] = s_guard[1] = 0ull;  // visible after the first chunk sync
   pdl_wait();  // the prefactor records of the preceding launch are complete from here on
 
   // this CTA's feature range [f0, f1) (a.fpc features per CTA, chosen by the launcher), walked
@@ -212,6 +243,14 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
       for (int t = threadIdx.x; t < n2; t += kNT) dst[t] = __ldg(src + t);
     }
     __syncthreads();
+    if (threadIdx.x < nfe) {
+      const double *r = sp + threadIdx.x * S;
+      double w1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < D; ++k) w1 += fabs(r[k]);
+      atomicMax(&s_guard[0], (unsigned long long)__double_as_longlong(w1));
+      atomicMax(&s_guard[1], (unsigned long long)__double_as_longlong(fabs(r[D])));
+    }
     double *colp = a.A + j0 * a.lda + rbase;
     if (full) {
       int jj = 0;
@@ -261,6 +300,10 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
       }
     }
   }
+  __syncthreads();
+  const double bound = fma(__longlong_as_double((long long)s_guard[0]), xinf,
+                           __longlong_as_double((long long)s_guard[1]));
+  if (bound > kMaxHalfTurns) phase_check<D, S, NQ>(a.pf, f0, f1, x, in, a.err);
 }
 
 // launch one batch, with the programmatic-dependent-launch attribute when the caller knows the

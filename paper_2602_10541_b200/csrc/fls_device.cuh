@@ -15,11 +15,17 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/fls.h"
+
 namespace fls {
 
 constexpr double kPi = 3.141592653589793238462643383279502884;
 constexpr double kInvPi = 0.318309886183790671537767526745028724;
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: x + kMagic rounds x to an integer
+// phase-range guard (fls.h FLS_MAX_PHASE, in radians) in half turns: |h| beyond it sets bit 1 of
+// the ctx error word (FLS_EUNSUPPORTED at the next fls_sync)
+constexpr double kMaxHalfTurns = FLS_MAX_PHASE * kInvPi;
+constexpr unsigned kErrNonFinite = 1u, kErrPhaseRange = 2u;
 
 // Coefficients live in constant memory so DFMA reads them as c[bank][offset] operands
 // (no per-iteration materialisation of 64-bit immediates).

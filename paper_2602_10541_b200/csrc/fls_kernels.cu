@@ -295,6 +295,7 @@ __global__ void __launch_bounds__(256) eval_kernel(const EvalArgs a) {
     }
   }
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  double hmax = 0.0;  // phase-range guard (FLS_MAX_PHASE)
   for (int64_t j = lane; j < a.F; j += 32) {
     const double *p = a.pf + j * a.S;
     double w[D];
@@ -313,6 +314,7 @@ __global__ void __launch_bounds__(256) eval_kernel(const EvalArgs a) {
       double h = bp;
 #pragma unroll
       for (int k = 0; k < D; ++k) h = fma(w[k], x[q][k], h);
+      hmax = fmax(hmax, r0 + q < a.n ? fabs(h) : 0.0);
       int sgn;
       const double f = halfturn(h, sgn);
       const double u = f * f;
@@ -338,7 +340,8 @@ __global__ void __launch_bounds__(256) eval_kernel(const EvalArgs a) {
     for (int q = 0; q < 4; ++q)
       if (r0 + q < a.n) a.out[r0 + q] = acc[q];
   }
-  if (bad) atomicOr(a.err, 1u);
+  if (bad) atomicOr(a.err, kErrNonFinite);
+  if (!(hmax <= kMaxHalfTurns)) atomicOr(a.err, kErrPhaseRange);
 }
 
 cudaError_t launch_eval(int D, const EvalArgs &a, cudaStream_t st) {

@@ -810,3 +810,76 @@ def test_binding_rejects_wrong_shapes_and_small_buffers(ctx):
         fls.fls_eval(ctx, Wd, bd, torch.zeros(F - 1, dtype=torch.float64, device="cuda"), blocks[0].X)
     with pytest.raises(ValueError, match="Ab holds"):
         fls.fls_solve(ctx, short[:100], R, lda, F)
+
+
+# ------------------------------------------------------------------------- phase-range guard
+def _guard_case(zmax_target, d=1, n=3000, F=300, seed=0):
+    """features with |W_j| ~ zmax_target on x in [0.5, 1]^d: max |z| ~ zmax_target"""
+    g = np.random.default_rng(seed)
+    W = g.uniform(0.5, 1.0, (F, d)) * (zmax_target / d) * np.where(g.random((F, d)) < 0.5, -1, 1)
+    b = g.uniform(0, 2 * np.pi, F)
+    X = g.uniform(0.5, 1.0, (n, d))
+    z = X @ W.T + b
+    return W, b, X, float(np.abs(z).max())
+
+
+@pytest.mark.parametrize("layout", ["col", "row"])
+def test_phase_beyond_limit_reports_unsupported(ctx, layout):
+    """|z| > FLS_MAX_PHASE = 1e4 -> FLS_EUNSUPPORTED at the next fls_sync (no silent garbage);
+    just below the limit -> no error, entries within the documented error at that |z|"""
+    from paper_2602_10541_b200._abi import FlsError
+    lay = fls.FLS_COL_MAJOR if layout == "col" else fls.FLS_ROW_MAJOR
+    W, b, X, zmax = _guard_case(3.0e4)
+    assert zmax > 1e4
+    blk = [fls.Block(torch.from_numpy(X).cuda(), [((2,), -1.0, -1)], 1.0)]
+    fls.fls_assemble(ctx, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(), blk, layout=lay)
+    with pytest.raises(FlsError, match="EUNSUPPORTED"):
+        fls.fls_sync(ctx)
+    fls.fls_sync(ctx)                                        # flag cleared
+    W, b, X, zmax = _guard_case(9.0e3)
+    assert 5e3 < zmax < 1e4
+    blk = [fls.Block(torch.from_numpy(X).cuda(), [((2,), -1.0, -1)], 1.0)]
+    A, _ = fls.fls_assemble(ctx, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(), blk, layout=lay)
+    fls.fls_sync(ctx)
+    F, n = W.shape[0], X.shape[0]
+    M = (A[: F * fls.round_up(n, 4)].view(F, -1)[:, :n].T if layout == "col"
+         else A.view(n, -1)[:, :F]).cpu().numpy()
+    class _OBlk:
+        pass
+    h = _OBlk()
+    h.X, h.terms, h.weight, h.values, h.fields = X, [((2,), -1.0, -1)], 1.0, np.zeros(n), None
+    Ao, _, S = oracle.assemble(W, b, [h])
+    err = (np.abs(M - Ao) / S).max()
+    # rounding of z itself: ~ a few ulp(|z|) ~ 1e-12 x |z| / 1e4 relative to S
+    assert err <= 8 * np.spacing(zmax), err
+
+
+def test_phase_bound_exceeded_but_phase_in_range_is_not_an_error(ctx):
+    """the per-CTA bound ||W_j||_1 ||x_i||_inf + |b_j| can exceed the limit while every actual
+    |z| is small: the exact re-check keeps such inputs valid (no false positive)"""
+    g = np.random.default_rng(1)
+    F, n = 256, 2048
+    W = np.zeros((F, 2))
+    W[:, 0] = g.uniform(5e5, 1e6, F)                         # ||W_j||_1 ~ 1e6
+    b = g.uniform(0, 2 * np.pi, F)
+    X = np.stack([g.uniform(0, 1e-3, n), g.uniform(10, 50, n)], 1)   # ||x||_inf ~ 50, z = W0 x0 + b <= 1e3
+    z = X @ W.T + b
+    assert np.abs(z).max() < 1.01e3
+    blk = [fls.Block(torch.from_numpy(X).cuda(), [((0, 0), 1.0, -1)], 1.0)]
+    Wd, bd = torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda()
+    for lay in (fls.FLS_COL_MAJOR, fls.FLS_ROW_MAJOR):
+        fls.fls_assemble(ctx, Wd, bd, blk, layout=lay)
+        fls.fls_sync(ctx)                                    # no FLS_EUNSUPPORTED
+    u = fls.fls_eval(ctx, Wd, bd, torch.ones(F, dtype=torch.float64, device="cuda"),
+                     torch.from_numpy(X).cuda())
+    fls.fls_sync(ctx)
+    assert np.allclose(u.cpu().numpy(), np.sin(z).sum(1) / np.sqrt(F), rtol=0, atol=1e-10)
+
+
+def test_eval_phase_beyond_limit_reports_unsupported(ctx):
+    from paper_2602_10541_b200._abi import FlsError
+    W, b, X, zmax = _guard_case(2.0e4, d=2)
+    u = fls.fls_eval(ctx, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(),
+                     torch.ones(W.shape[0], dtype=torch.float64, device="cuda"), torch.from_numpy(X).cuda())
+    with pytest.raises(FlsError, match="EUNSUPPORTED"):
+        fls.fls_sync(ctx)
