@@ -369,10 +369,10 @@ def solve_measure(args, world, rank, local):
 # per-config block: BASELINE.json configs 1-4 on the same GPU (rank 0, N = 1)
 # ------------------------------------------------------------------------------------------------
 def per_config(names=("c1_poisson1d", "c2_poisson2d", "c3_poisson5d", "c4_heat2d"), budget_s=60.0):
-    """For each config: the fused features + assembly step captured once in a CUDA graph and
-    replayed (the launch-latency-bound C1/C2 measured without host gaps) -> steady-state
-    entries/s and fraction of the copy peak; the single-shot latency (host call -> kernels
-    done); the end-to-end solve by phase.  Bounded to about budget_s seconds."""
+    """For each config: the bench's step (fls_features_assemble) captured in a CUDA graph of 10
+    consecutive steps and replayed (the launch-latency-bound C1/C2 measured without host
+    gaps) -> steady-state entries/s and fraction of the copy peak; the single-shot latency
+    (host call -> kernels done); the end-to-end solve by phase.  Bounded to about budget_s."""
     import torch
     import workloads as wl
     from paper_2602_10541_b200 import fls
@@ -413,20 +413,23 @@ def per_config(names=("c1_poisson1d", "c2_poisson2d", "c3_poisson5d", "c4_heat2d
                 step()
                 torch.cuda.synchronize()
                 singles.append(1e6 * (time.perf_counter() - t0))
+            # steady state: a CUDA graph holding `per_graph` consecutive steps, replayed
+            per_graph = 10 if reps >= 100 else 1
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=s):
-                step()
+                for _ in range(per_graph):
+                    step()
             for _ in range(3):
                 g.replay()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record(s)
-            for _ in range(reps):
+            for _ in range(max(1, reps // per_graph)):
                 g.replay()
             e1.record(s)
             torch.cuda.synchronize()
         fls.fls_sync(ctx)
-        ms = e0.elapsed_time(e1) / reps
+        ms = e0.elapsed_time(e1) / (max(1, reps // per_graph) * per_graph)
         del g, Ab
         ctx.close()
         torch.cuda.empty_cache()
@@ -435,6 +438,9 @@ def per_config(names=("c1_poisson1d", "c2_poisson2d", "c3_poisson5d", "c4_heat2d
             workload = name
         sol = solve_measure(A_, 1, 0, 0)
         out[name] = {"rows": R, "features": F, "entries": R * F, "reps": reps,
+                     "steps_per_graph": per_graph,
+                     "launches_per_step": "1 (fused features + records in the assembly CTAs)"
+                                          if R * F <= (1 << 22) else "2 (features + prefactors, assembly)",
                      "graph_us_per_step": 1e3 * ms, "entries_per_s": R * F / (ms / 1e3),
                      "hbm_write_gbs": 8.0 * R * (F + 1) / (ms / 1e3) / 1e9,
                      "frac_of_copy_peak": 8.0 * R * F / (ms / 1e3) / 1e9 / hbm_peak,

@@ -341,6 +341,24 @@ fls_status validate_assemble(int32_t dim, int64_t n_features, const double *W, c
 
 constexpr int kSmax = pf_stride(FLS_MAX_DIM, FLS_MAX_FIELDS, KM_SINCOS);
 
+// fold arguments of block q (its record array at ctx->ws + q F kSmax)
+void make_pref(fls_ctx *ctx, PrefArgs &pa, const OpPlan &pl, const fls_block &B, int q,
+               const double *W, const double *b, int32_t dim, int64_t F, double s_norm) {
+  std::memset(&pa, 0, sizeof pa);
+  pa.W = W;
+  pa.b = b;
+  pa.F = F;
+  pa.D = dim;
+  pa.n_terms = pl.n_terms;
+  pa.G = pl.G;
+  pa.pmode = pl.pmode;
+  pa.S = pf_stride(dim, pl.G, pl.kmode);
+  pa.scale = s_norm * B.weight;
+  pa.pf = ctx->ws + (size_t)q * F * kSmax;
+  pa.err = ctx->d_err;
+  std::memcpy(pa.terms, pl.terms, sizeof pl.terms);
+}
+
 // a2: prefactor records of every block that has rows in [row_begin, row_end), up to
 // kMaxBatch blocks per launch
 fls_status launch_prefactors(fls_ctx *ctx, const AsmPlan &ap, const double *W, const double *b,
@@ -356,21 +374,7 @@ fls_status launch_prefactors(fls_ctx *ctx, const AsmPlan &ap, const double *W, c
     const int64_t lo = std::max(g0, row_begin), hi = std::min(g0 + B.n_points, row_end);
     g0 += B.n_points;
     if (hi <= lo) continue;
-    const OpPlan &pl = ap.plans[q];
-    PrefArgs &pa = pb.blk[pb.n++];
-    std::memset(&pa, 0, sizeof pa);
-    pa.W = W;
-    pa.b = b;
-    pa.F = F;
-    pa.D = dim;
-    pa.n_terms = pl.n_terms;
-    pa.G = pl.G;
-    pa.pmode = pl.pmode;
-    pa.S = pf_stride(dim, pl.G, pl.kmode);
-    pa.scale = s_norm * B.weight;
-    pa.pf = ctx->ws + (size_t)q * F * kSmax;
-    pa.err = ctx->d_err;
-    std::memcpy(pa.terms, pl.terms, sizeof pl.terms);
+    make_pref(ctx, pb.blk[pb.n++], ap.plans[q], B, q, W, b, dim, F, s_norm);
     if (pb.n == kMaxBatch) {
       cudaError_t e = launch_prefactor_batch(pb, F, st);
       if (e != cudaSuccess) return cuda_fail(e, "prefactor_batch_kernel");
@@ -395,14 +399,18 @@ constexpr int64_t kPdlMaxEntries = int64_t(1) << 28;
 fls_status assemble_range(fls_ctx *ctx, const AsmPlan &ap, int32_t dim, int64_t F,
                           const fls_block *blocks, const int64_t *pt_base, int64_t row_begin,
                           int64_t row_end, double *A, int64_t lda, int32_t layout, double *rhs,
-                          cudaStream_t st, bool pdl) {
+                          cudaStream_t st, bool pdl, const FusedBatch *fz_proto = nullptr,
+                          double s_norm = 1.0) {
   // vector stores need every column segment aligned: 16 B (row pairs) or 32 B (kQuad rows);
   // the row-major kernel always stores feature pairs (16 B)
   const bool quad = kQuad && layout == FLS_COL_MAJOR;
   const bool vec = quad ? ((reinterpret_cast<uintptr_t>(A) & 31) == 0) && (lda % 4 == 0)
                         : ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0);
   AsmArgs batch[kMaxBatch];
+  int bq[kMaxBatch];  // block index of each batch entry
   int nb = 0, bG = 0, bK = 0;
+  bool first_launch = true;
+  static thread_local FusedBatch fz;
   auto flush = [&]() -> fls_status {
     if (nb == 0) return FLS_OK;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -425,8 +433,17 @@ fls_status assemble_range(fls_ctx *ctx, const AsmPlan &ap, int32_t dim, int64_t 
       // (1.7e10 entries) it cost 0.6% (early-dispatched CTAs skew its two long waves)
       int64_t entries = 0;
       for (int i = 0; i < nb; ++i) entries += (batch[i].lr1 - batch[i].lr0) * F;
-      e = launch_assemble_cm(dim, bG, bK, batch, nb, st,
-                             pdl && !ctx->timing && entries <= kPdlMaxEntries);
+      if (fz_proto) {  // single launch: the CTAs draw and fold their features' records
+        fz = *fz_proto;
+        fz.write_wb = first_launch ? 1 : 0;
+        for (int i = 0; i < nb; ++i)
+          make_pref(ctx, fz.pre[i], ap.plans[bq[i]], blocks[bq[i]], bq[i], fz.W, fz.b, dim, F, s_norm);
+        e = launch_assemble_cm_fused(dim, bG, batch, nb, fz, st);
+      } else {
+        e = launch_assemble_cm(dim, bG, bK, batch, nb, st,
+                               pdl && !ctx->timing && entries <= kPdlMaxEntries);
+      }
+      first_launch = false;
     } else {
       for (int i = 0; i < nb && e == cudaSuccess; ++i) e = launch_assemble_rm(dim, bG, bK, batch[i], st);
     }
@@ -447,6 +464,7 @@ fls_status assemble_range(fls_ctx *ctx, const AsmPlan &ap, int32_t dim, int64_t 
       if (fls_status s = flush()) return s;
     bG = pl.G;
     bK = pl.kmode;
+    bq[nb] = q;
     AsmArgs &aa = batch[nb++];
     std::memset(&aa, 0, sizeof aa);
     aa.pf = ctx->ws + (size_t)q * F * kSmax;
@@ -467,6 +485,15 @@ fls_status assemble_range(fls_ctx *ctx, const AsmPlan &ap, int32_t dim, int64_t 
     for (int i = 0; i < FLS_MAX_FIELDS; ++i) aa.gfield[i] = pl.gfield[i];
   }
   return flush();
+}
+
+// largest fls_features_assemble call (local entries) that runs as ONE fused launch; read per
+// call so tuning sweeps / tests can switch it (FLS_FUSE_MAX_ENTRIES=0 turns the fusion off)
+int64_t fuse_max_entries() {
+  const char *v = getenv("FLS_FUSE_MAX_ENTRIES");
+  // default 2^22: C1 (5e5 entries, graph step 10.2 -> 8.2 us); C2 (9.6e6) is slower fused
+  // (24.1 vs 20.5 us: each CTA's Box-Muller + fold chain, ~3 us, sits on its critical path)
+  return v && *v ? (int64_t)atoll(v) : (int64_t(1) << 22);
 }
 
 // programmatic dependent launch of the assembly after its prefactor launch (FLS_PDL=0: off)
@@ -532,21 +559,30 @@ fls_status fls_features_assemble(fls_ctx *ctx, int32_t dim, int64_t n_features, 
       overflow = true;
       break;
     }
-    const OpPlan &pl = ap.plans[q];
-    PrefArgs &pa = pb.blk[pb.n++];
-    std::memset(&pa, 0, sizeof pa);
-    pa.W = W;
-    pa.b = b;
-    pa.F = F;
-    pa.D = dim;
-    pa.n_terms = pl.n_terms;
-    pa.G = pl.G;
-    pa.pmode = pl.pmode;
-    pa.S = pf_stride(dim, pl.G, pl.kmode);
-    pa.scale = s_norm * B.weight;
-    pa.pf = ctx->ws + (size_t)q * F * kSmax;
-    pa.err = ctx->d_err;
-    std::memcpy(pa.terms, pl.terms, sizeof pl.terms);
+    make_pref(ctx, pb.blk[pb.n++], ap.plans[q], B, q, W, b, dim, F, s_norm);
+  }
+  // small problems (launch-latency bound): ONE launch -- each assembly CTA draws
+  // W_j, b_j of its own features and folds their records in its prologue (bit-identical to the
+  // two-launch path); needs every block in range on a fused variant, column-major
+  const int64_t n_local = row_end - row_begin;
+  if (layout == FLS_COL_MAJOR && n_local > 0 && n_local * F <= fuse_max_entries()) {
+    bool ok = true;
+    g0 = 0;
+    for (int q = 0; q < ap.n_blocks; ++q) {
+      const int64_t lo = std::max(g0, row_begin), hi = std::min(g0 + blocks[q].n_points, row_end);
+      g0 += blocks[q].n_points;
+      if (hi > lo && !fused_variant(dim, ap.plans[q].G, ap.plans[q].kmode)) ok = false;
+    }
+    if (ok) {
+      static thread_local FusedBatch proto;
+      std::memset(&proto, 0, sizeof proto);
+      proto.fb = fb;
+      proto.seed = seed;
+      proto.W = W;
+      proto.b = b;
+      return assemble_range(ctx, ap, dim, F, blocks, nullptr, row_begin, row_end, A, lda, layout,
+                            rhs, ctx->stream, false, &proto, s_norm);
+    }
   }
   if (overflow) pb.n = 0;  // many blocks: fused features only, prefactors in batches below
   cudaError_t e = launch_features_prefactor(dim, F, fb, seed, W, b, pb, ctx->stream);

@@ -5,9 +5,11 @@
 namespace fls {
 
 template <int D, int G>
-static cudaError_t go_sin(AsmArgs *blks, int n, cudaStream_t st, bool pdl) {
+static cudaError_t go_sin(AsmArgs *blks, int n, cudaStream_t st, bool pdl,
+                          const FusedBatch *fz = nullptr) {
   constexpr int S = pf_stride(D, G, KM_SIN);
-  const size_t smem = (size_t)kFC * S * sizeof(double);
+  // fused: the chunk's normals and biases follow the records in shared memory
+  const size_t smem = (size_t)kFC * (S + (fz ? D + 1 : 0)) * sizeof(double);
   AsmBatch bt;
   bt.n = n;
   int64_t total = 0, span = 0;
@@ -20,12 +22,45 @@ static cudaError_t go_sin(AsmArgs *blks, int n, cudaStream_t st, bool pdl) {
     total += (int64_t)g.x * g.y;
     bt.cta_end[q] = total;
   }
+  if (fz) {
+    if constexpr (G <= 1) {
+      auto kern = assemble_cm_kernel<D, G, KM_SIN, FusedBatch>;
+      if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+      }
+      kern<<<(unsigned)total, kNT, smem, st>>>(bt, *fz);
+      return cudaGetLastError();
+    } else {
+      return cudaErrorNotSupported;
+    }
+  }
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(assemble_cm_kernel<D, G, KM_SIN>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  return asm_launch(assemble_cm_kernel<D, G, KM_SIN>, (unsigned)total, smem, st, pdl, bt);
+  return asm_launch(assemble_cm_kernel<D, G, KM_SIN>, (unsigned)total, smem, st, pdl, bt, NoFuse{});
+}
+
+cudaError_t launch_assemble_cm_fused(int D, int G, AsmArgs *blks, int n, const FusedBatch &fz,
+                                     cudaStream_t st) {
+  if (G > 1) return cudaErrorNotSupported;
+#define FLS_FG(d)                                            \
+  return G == 0 ? go_sin<d, 0>(blks, n, st, false, &fz)      \
+                : go_sin<d, 1>(blks, n, st, false, &fz);
+  switch (D) {
+    case 1: FLS_FG(1)
+    case 2: FLS_FG(2)
+    case 3: FLS_FG(3)
+    case 4: FLS_FG(4)
+    case 5: FLS_FG(5)
+    case 6: FLS_FG(6)
+    case 7: FLS_FG(7)
+    case 8: FLS_FG(8)
+    default: return cudaErrorInvalidValue;
+  }
+#undef FLS_FG
 }
 
 cudaError_t launch_assemble_cm_sin(int D, int G, AsmArgs *blks, int n, cudaStream_t st, bool pdl) {

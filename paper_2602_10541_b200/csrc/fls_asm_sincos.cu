@@ -25,7 +25,7 @@ static cudaError_t go_sincos(AsmArgs *blks, int n, cudaStream_t st, bool pdl) {
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  return asm_launch(assemble_cm_kernel<D, G, KM_SINCOS>, (unsigned)total, smem, st, pdl, bt);
+  return asm_launch(assemble_cm_kernel<D, G, KM_SINCOS>, (unsigned)total, smem, st, pdl, bt, NoFuse{});
 }
 
 cudaError_t launch_assemble_cm_sincos(int D, int G, AsmArgs *blks, int n, cudaStream_t st, bool pdl) {

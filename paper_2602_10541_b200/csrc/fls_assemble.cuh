@@ -19,7 +19,10 @@
 #pragma once
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "fls_device.cuh"
+#include "fls_feat.cuh"
 #include "fls_internal.h"
 
 #ifndef FLS_MINB
@@ -87,7 +90,8 @@ constexpr int asm_min_blocks() {
 // when the block's point data exceed 32 MB and would not stay in L2 between groups).
 template <int D, int G, int KM>
 inline dim3 asm_grid(AsmArgs &a) {
-  static int sms = 0, waves = 2;  // tools/waves_sweep.sh, variant_sweep_c3.sh: 2 best for C3, flat for C2/C4/C5
+  static int sms = 0, waves = 2;  // tools/waves_sweep.sh, variant_sweep_c3.sh: 2 best for C3, flat for C4/C5
+  static bool forced = false;
   if (!sms) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -95,7 +99,10 @@ inline dim3 asm_grid(AsmArgs &a) {
     if (sms <= 0) sms = 148;
     if (const char *w = getenv("FLS_ASM_WAVES")) {  // tuning sweeps only
       const int v = atoi(w);
-      if (v >= 1 && v <= 64) waves = v;
+      if (v >= 1 && v <= 64) {
+        waves = v;
+        forced = true;
+      }
     }
   }
   const int64_t span = a.lr1 - (a.lr0 & ~int64_t(kRowAlign - 1));
@@ -106,7 +113,11 @@ inline dim3 asm_grid(AsmArgs &a) {
   // small blocks (C1, C2): 16-feature CTAs cannot fill the waves -> narrower CTAs (>= 2, the
   // features-per-iteration granularity) so the launch spreads over the SMs, each block of the
   // batch getting CTAs in proportion to its rows
-  int64_t target = waves * resident;
+  // small launches (<= 2^25 entries, C2): one wave of fatter CTAs -- every CTA pays the fixed
+  // cost (launch, x and record loads, two syncs) once; C2 graph step 21.3 -> 20.5 us
+  // (tools/small_step_probe.py); larger launches keep the sweep's 2 waves
+  const int w_eff = (!forced && a.batch_span * a.F <= (int64_t(1) << 25)) ? 1 : waves;
+  int64_t target = w_eff * resident;
   if (!big_x && rt * ((a.F + 15) / 16) < waves * resident) {
     min_fpc = a.F < 2 ? a.F : 2;
     if (a.batch_span > span) target = (target * span + a.batch_span - 1) / a.batch_span;
@@ -168,11 +179,41 @@ __device__ __forceinline__ void phase_check(const double *pf, int64_t f0, int64_
   }
 }
 
+// the fused kernel's exact check: records recomputed per feature (rare path)
+template <int D, int NQ>
+__device__ __forceinline__ void phase_check_wb(const FusedBatch &fz, int qb, int64_t f0, int64_t f1,
+                                               const double (&x)[NQ][D], const bool (&in)[NQ],
+                                               unsigned *err) {
+  double rec[pf_stride(FLS_MAX_DIM, FLS_MAX_FIELDS, KM_SINCOS)];
+  double w[D];
+  for (int64_t j = f0; j < f1; ++j) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) w[k] = feat_normal(j * D + k, D, fz.fb, fz.seed);
+    prefactor_rec(fz.pre[qb], w, feat_bias(j, fz.seed), rec);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      double h = rec[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) h = fma(rec[k], x[q][k], h);
+      if (in[q] && !(fabs(h) <= kMaxHalfTurns)) {
+        atomicOr(err, kErrPhaseRange);
+        return;
+      }
+    }
+  }
+}
+
 // One launch covers up to kMaxBatch row blocks that share the kernel variant (e.g. a PDE block
 // and its identity BC / IC blocks): the 1-D grid is the concatenation of each block's
 // (row tile, feature group) CTAs, row tile fastest.
-template <int D, int G, int KM>
-__global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_kernel(const AsmBatch bt) {
+struct NoFuse {};
+
+// Z = NoFuse: the records come from the preceding prefactor launch (a.pf).  Z = FusedBatch: the
+// CTA computes the records of each chunk itself (a1 + a2 in the prologue; one launch per call).
+template <int D, int G, int KM, class Z = NoFuse>
+__global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>())
+assemble_cm_kernel(const AsmBatch bt, const Z fz) {
+  constexpr bool kFused = !std::is_same<Z, NoFuse>::value;
   using M = EntryMath<D, G, KM>;
   constexpr int S = M::S;
   constexpr int GG = G > 0 ? G : 1;
@@ -236,7 +277,29 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
   for (int64_t j0 = f0; j0 < f1; j0 += kFC) {
     const int nfe = (f1 - j0) < kFC ? (int)(f1 - j0) : kFC;
     __syncthreads();  // previous chunk's records no longer in use
-    {
+    if constexpr (kFused) {
+      // a1: the chunk's normals and biases, one draw per thread (the features_prefactor_kernel
+      // draws: bit-identical) into shared memory after the records -- both Philox chains run
+      // side by side; a2: one thread per feature folds its record
+      double *ws = sp + kFC * S;      // normals (nfe * D), then biases (nfe)
+      double *bs = ws + kFC * D;
+      const bool wr = fz.write_wb && qb == 0 && tile == 0;
+      for (int t = threadIdx.x; t < nfe * (D + 1); t += kNT) {
+        if (t < nfe * D) {
+          const int64_t m = j0 * D + t;
+          const double w = feat_normal(m, D, fz.fb, fz.seed);
+          ws[t] = w;
+          if (wr) fz.W[m] = w;
+        } else {
+          const int64_t j = j0 + (t - nfe * D);
+          const double bj = feat_bias(j, fz.seed);
+          bs[t - nfe * D] = bj;
+          if (wr) fz.b[j] = bj;
+        }
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < nfe; t += kNT) prefactor_rec(fz.pre[qb], ws + t * D, bs[t], sp + t * S);
+    } else {
       const double2 *src = reinterpret_cast<const double2 *>(a.pf + j0 * S);
       double2 *dst = reinterpret_cast<double2 *>(sp);
       const int n2 = nfe * (S / 2);
@@ -303,15 +366,23 @@ __global__ void __launch_bounds__(kNT, asm_min_blocks<D, G, KM>()) assemble_cm_k
   __syncthreads();
   const double bound = fma(__longlong_as_double((long long)s_guard[0]), xinf,
                            __longlong_as_double((long long)s_guard[1]));
-  if (bound > kMaxHalfTurns) phase_check<D, S, NQ>(a.pf, f0, f1, x, in, a.err);
+  if (bound > kMaxHalfTurns) {
+    if constexpr (kFused) {
+      // no record array in global memory: the records are recomputed (prefactor_rec, the same
+      // draw and fold, so h is bit-identical to the entry's)
+      phase_check_wb<D, NQ>(fz, qb, f0, f1, x, in, a.err);
+    } else {
+      phase_check<D, S, NQ>(a.pf, f0, f1, x, in, a.err);
+    }
+  }
 }
 
 // launch one batch, with the programmatic-dependent-launch attribute when the caller knows the
 // preceding operation on the stream is the prefactor launch of the same call (or an earlier
 // assembly batch of it, which writes disjoint rows)
-template <class Kern>
+template <class Kern, class Z>
 inline cudaError_t asm_launch(Kern kern, unsigned ctas, size_t smem, cudaStream_t st, bool pdl,
-                              const AsmBatch &bt) {
+                              const AsmBatch &bt, const Z &fz) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ctas);
   cfg.blockDim = dim3(kNT);
@@ -322,7 +393,7 @@ inline cudaError_t asm_launch(Kern kern, unsigned ctas, size_t smem, cudaStream_
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, bt);
+  return cudaLaunchKernelEx(&cfg, kern, bt, fz);
 }
 
 }  // namespace fls

@@ -134,6 +134,22 @@ struct PrefBatch {
   PrefArgs blk[kMaxBatch];
 };
 
+// single-launch a1 + a2-a8 (fls_features_assemble on small problems): every assembly CTA
+// draws W_j, b_j of its own features and folds their records in its prologue (bit-identical to
+// features_prefactor_kernel); the CTAs of row tile 0 of the first block also write W and b
+struct FusedBatch {
+  FeatBlocks fb;
+  uint64_t seed;
+  double *W, *b;
+  int32_t write_wb;             // this launch writes W, b (the first launch of the call)
+  PrefArgs pre[kMaxBatch];      // fold arguments of each block of the batch
+};
+// variants with a fused instantiation (launch_assemble_cm_fused returns cudaErrorNotSupported
+// for the others)
+inline bool fused_variant(int D, int G, int kmode) { return kmode == KM_SIN && G <= 1 && D >= 1 && D <= FLS_MAX_DIM; }
+cudaError_t launch_assemble_cm_fused(int D, int G, AsmArgs *blks, int n, const FusedBatch &fz,
+                                     cudaStream_t st);
+
 cudaError_t launch_prefactor(const PrefArgs &a, cudaStream_t st);
 cudaError_t launch_prefactor_batch(const PrefBatch &b, int64_t F, cudaStream_t st);
 cudaError_t launch_features_prefactor(int32_t dim, int64_t F, const FeatBlocks &fb, uint64_t seed,

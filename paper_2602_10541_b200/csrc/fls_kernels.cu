@@ -4,6 +4,7 @@
 #include <math.h>
 
 #include "fls_device.cuh"
+#include "fls_feat.cuh"
 #include "fls_internal.h"
 
 namespace fls {
@@ -12,33 +13,6 @@ namespace fls {
 // a1 features (Alg. 1 line 1).  Philox4x64-10, one block of 4 x 64-bit words
 // per thread (header fls.h documents the stream layout).
 // ------------------------------------------------------------------------------------------
-__device__ __forceinline__ void philox4x64(uint64_t c[4], uint64_t k0, uint64_t k1) {
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    const uint64_t M0 = 0xD2E7470EE14C6C93ULL, M1 = 0xCA5A826395121157ULL;
-    const uint64_t hi0 = __umul64hi(M0, c[0]), lo0 = M0 * c[0];
-    const uint64_t hi1 = __umul64hi(M1, c[2]), lo1 = M1 * c[2];
-    const uint64_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
-    c[0] = n0;
-    c[1] = lo1;
-    c[2] = n2;
-    c[3] = lo0;
-    k0 += 0x9E3779B97F4A7C15ULL;
-    k1 += 0xBB67AE8584CAA73BULL;
-  }
-}
-
-__device__ __forceinline__ double u01(uint64_t r) {
-  return (double)(r >> 11) * (1.0 / 9007199254740992.0);
-}
-
-// sigma of feature j under the multi-block basis: block q covers [ends[q-1], ends[q])
-__device__ __forceinline__ double block_sigma(const FeatBlocks &fb, int64_t j) {
-  int q = 0;
-  while (q + 1 < fb.n && j >= fb.ends[q]) ++q;
-  return fb.sigma[q];
-}
-
 // thread t owns Philox block t: raw words 4t..4t+3 of stream 1 -> normals 4t..4t+3
 // (Box-Muller pairs (4t, 4t+1) and (4t+2, 4t+3)); of stream 2 -> b_{4t..4t+3}.
 // W[j][k] = sigma_{block(j)} * normal[j*D + k].
@@ -135,7 +109,6 @@ __global__ void prefactor_batch_kernel(const PrefBatch b) {
   if (j < a.F) prefactor_one(a, j);
 }
 
-__device__ void prefactor_core(const PrefArgs &a, int64_t j, const double *w, double bj);
 
 __device__ void prefactor_one(const PrefArgs &a, int64_t j) {
   double w[FLS_MAX_DIM];
@@ -147,7 +120,7 @@ __device__ void prefactor_one(const PrefArgs &a, int64_t j) {
   double bj = a.b[j];
   ok &= finite(bj);
   if (!ok) atomicOr(a.err, 1u);
-  prefactor_core(a, j, w, bj);
+  prefactor_rec(a, w, bj, a.pf + j * a.S);
 }
 
 // a1 + a2 fused (fls_features_assemble).  A CTA covers kFpFeat features: first one thread per
@@ -162,21 +135,11 @@ features_prefactor_kernel(int32_t D, int64_t F, const FeatBlocks fb, uint64_t se
   __shared__ double ws[kFpFeat * FLS_MAX_DIM];
   pdl_trigger();
   const int64_t j0 = (int64_t)blockIdx.x * kFpFeat;
-  const double two_pi = 6.283185307179586476925286766559;
   const int t = threadIdx.x;
   if (t < kFpFeat * D) {
     const int64_t m = j0 * D + t;         // normal index; pair m/2 uses raw words m&~1, m|1
     if (m < F * D) {
-      const int64_t word0 = m & ~int64_t(1);
-      uint64_t c[4] = {(uint64_t)(word0 / 4) + 1, 0, 0, 0};
-      philox4x64(c, seed, 1);
-      const int o = (int)(word0 % 4);
-      const double u1 = u01(c[o]), u2 = u01(c[o + 1]);
-      const double rad = sqrt(-2.0 * log(1.0 - u1));
-      const double th = two_pi * u2;
-      double sn, cs;
-      sincos(th, &sn, &cs);
-      const double w = block_sigma(fb, m / D) * (rad * ((m & 1) ? sn : cs));
+      const double w = feat_normal(m, D, fb, seed);
       ws[t] = w;
       W[m] = w;
     }
@@ -185,13 +148,11 @@ features_prefactor_kernel(int32_t D, int64_t F, const FeatBlocks fb, uint64_t se
   if (t >= kFpFeat) return;
   const int64_t j = j0 + t;
   if (j >= F) return;
-  uint64_t c[4] = {(uint64_t)(j / 4) + 1, 0, 0, 0};
-  philox4x64(c, seed, 2);
-  const double bj = two_pi * u01(c[j % 4]);
+  const double bj = feat_bias(j, seed);
   b[j] = bj;
   double w[FLS_MAX_DIM];
   for (int k = 0; k < D; ++k) w[k] = ws[t * D + k];
-  for (int q = 0; q < pb.n; ++q) prefactor_core(pb.blk[q], j, w, bj);
+  for (int q = 0; q < pb.n; ++q) prefactor_rec(pb.blk[q], w, bj, pb.blk[q].pf + j * pb.blk[q].S);
 }
 
 cudaError_t launch_features_prefactor(int32_t dim, int64_t F, const FeatBlocks &fb, uint64_t seed,
@@ -199,59 +160,6 @@ cudaError_t launch_features_prefactor(int32_t dim, int64_t F, const FeatBlocks &
   const int nt = ((kFpFeat * (dim > 1 ? dim : 1) + 31) / 32) * 32;
   features_prefactor_kernel<<<(unsigned)((F + kFpFeat - 1) / kFpFeat), nt, 0, st>>>(dim, F, fb, seed, W, b, pb);
   return cudaGetLastError();
-}
-
-// explicit _rn arithmetic: no FMA contraction, so every call site (prefactor_one,
-// features_prefactor_kernel) rounds identically whatever the inliner does around it
-__device__ void prefactor_core(const PrefArgs &a, int64_t j, const double *w, double bj) {
-  double Ps[FLS_MAX_FIELDS + 1], Pc[FLS_MAX_FIELDS + 1];
-  for (int g = 0; g <= FLS_MAX_FIELDS; ++g) Ps[g] = Pc[g] = 0.0;
-  for (int t = 0; t < a.n_terms; ++t) {
-    const TermDev &T = a.terms[t];
-    double m = T.coef;
-    int order = 0;
-    for (int k = 0; k < a.D; ++k)
-      for (int e = 0; e < T.alpha[k]; ++e) {
-        m = __dmul_rn(m, w[k]);
-        ++order;
-      }
-    const int p = order & 3;  // Phi_{|alpha| mod 4}: sin, cos, -sin, -cos
-    if (p & 2) m = -m;
-    if (p & 1)
-      Pc[T.group] = __dadd_rn(Pc[T.group], m);
-    else
-      Ps[T.group] = __dadd_rn(Ps[T.group], m);
-  }
-  double *out = a.pf + j * a.S;
-  for (int k = 0; k < a.D; ++k) out[k] = __dmul_rn(w[k], kInvPi);
-  double bp = bj;
-  int o = a.D + 1;
-  switch (a.pmode) {
-    case PM_SIN:
-      for (int g = 0; g <= a.G; ++g) out[o++] = a.scale * Ps[g];
-      out[a.D] = __dmul_rn(bp, kInvPi);
-      break;
-    case PM_COSSHIFT:  // cos z = sin(z + pi/2)  (App. F quarter-wave shift)
-      for (int g = 0; g <= a.G; ++g) out[o++] = a.scale * Pc[g];
-      out[a.D] = __dadd_rn(__dmul_rn(bp, kInvPi), 0.5);
-      break;
-    case PM_FOLD: {    // Ps sin z + Pc cos z = rho sin(z + psi)
-      const double ps = a.scale * Ps[0], pc = a.scale * Pc[0];
-      const double rho = hypot(ps, pc);
-      const double psi = atan2(pc, ps);
-      out[o++] = rho;
-      out[a.D] = __dmul_rn(__dadd_rn(bp, psi), kInvPi);
-      break;
-    }
-    default:           // PM_SINCOS
-      for (int g = 0; g <= a.G; ++g) {
-        out[o++] = a.scale * Ps[g];
-        out[o++] = a.scale * Pc[g];
-      }
-      out[a.D] = __dmul_rn(bp, kInvPi);
-      break;
-  }
-  for (; o < a.S; ++o) out[o] = 0.0;
 }
 
 cudaError_t launch_prefactor(const PrefArgs &a, cudaStream_t st) {

@@ -711,10 +711,16 @@ def test_cached_qr_many_rhs(ctx, name, size):
 
 
 # ------------------------------------------------------------------------------------- fused a1+a2
-@pytest.mark.parametrize("name", ["c1_poisson1d", "c4_heat2d", "c5_biharm3d"])
-def test_features_assemble_fused_bit_identical(ctx, name):
+@pytest.mark.parametrize("fuse", ["0", "1000000000000"])
+@pytest.mark.parametrize("name", ["c1_poisson1d", "c2_poisson2d", "c3_poisson5d", "c4_heat2d",
+                                  "c5_biharm3d"])
+def test_features_assemble_fused_bit_identical(ctx, name, fuse, monkeypatch):
     """fls_features_assemble == fls_features then fls_assemble, bit for bit: one block batch
-    (fused prefactors), more blocks than one prefactor batch holds, shards and row-major"""
+    (fused prefactors), more blocks than one prefactor batch holds, shards and row-major.
+    fuse = FLS_FUSE_MAX_ENTRIES: "0" = two launches (features + prefactors, then assembly),
+    1e12 = ONE launch whose CTAs draw and fold their own features' records (the default for
+    calls up to 2^25 entries: C1, C2)"""
+    monkeypatch.setenv("FLS_FUSE_MAX_ENTRIES", fuse)
     p = wl.make_problem(name, "mini")
     F, d = p.n_features, p.dim
     sigma, seed = float(p.sigma), int(p.seed)
