@@ -598,14 +598,22 @@ class FlsEngine:
             try:
                 m = json.load(open(pm))["model"]
                 bound = m["power_bound_entries_per_s"]
-                power = {"bound": "board power", "limit_w": m["power_limit_w"], "idle_w": m["idle_w"],
+                window_s = ms_step * steps / 1e3
+                sustained = window_s >= 4.0
+                power = {"bound": "board power (sustained windows >= 4 s)",
+                         "limit_w": m["power_limit_w"], "idle_w": m["idle_w"],
                          "nj_per_entry": m["store_nj_per_entry"] + m["alu_nj_per_entry"],
                          "bound_entries_per_s_per_gpu": bound,
                          "achieved_entries_per_s_per_gpu": mine["entries_per_s"],
-                         "frac": mine["entries_per_s"] / bound,
-                         "source": "profiles/r01_power_model.json (tools/power_model.py)",
-                         "note": "sustained-window metric: the board's limiter acts on a time-"
-                                 "averaged power, so a short run can read above 1.0"}
+                         "timed_window_s": window_s,
+                         # the limiter acts on a time-averaged power: over a window shorter
+                         # than ~4 s the board borrows headroom, so no fraction is claimed
+                         "frac": mine["entries_per_s"] / bound if sustained else None,
+                         "frac_short_window": None if sustained else mine["entries_per_s"] / bound,
+                         "sustained_reference": {
+                             "frac": m.get("c5_assembly_frac_of_power_bound"),
+                             "what": "the same kernel back to back for 4 s at 995 W of 1000 W"},
+                         "source": "profiles/r01_power_model.json (tools/power_model.py)"}
             except Exception:
                 power = None
         tot_bytes = sum(r["bytes_per_step"] for r in per_rank)
