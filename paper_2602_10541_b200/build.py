@@ -82,7 +82,7 @@ MB_LIB = os.path.join(HERE, "libfls_microbench.so")
 
 def build_microbench(force: bool = False) -> str:
     """roofline probes (not part of the product ABI)"""
-    deps = [MB_SRC, os.path.join(CSRC, "fls_device.cuh")]
+    deps = [MB_SRC, os.path.join(CSRC, "fls_device.cuh"), os.path.join(CSRC, "fls_feat.cuh")]
     if not force and os.path.exists(MB_LIB) and all(os.path.getmtime(d) <= os.path.getmtime(MB_LIB) for d in deps):
         return MB_LIB
     cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", MB_LIB, MB_SRC]

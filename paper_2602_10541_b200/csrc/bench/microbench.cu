@@ -9,6 +9,7 @@
 //                   = the FP64-pipe ceiling of the C5 kernel with no memory traffic at all
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 #include "../fls_device.cuh"
 
@@ -328,5 +329,85 @@ extern "C" __attribute__((visibility("default"))) int mb_op_rate(int op, double 
   *ops_per_s = (double)grid * 256 * iters * per / (time_ms(e0, e1) / 1e3);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  return (int)cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------------
+// latency (clock64 cycles, one thread) of the pieces of the fused assembly prologue (a1 + a2):
+// out[0] Philox4x64-10 block, out[1] feat_normal (Philox + Box-Muller), out[2] feat_bias,
+// out[3] prefactor_rec of a 2-term operator (C2's -Laplacian), out[4] log + sqrt alone,
+// out[5] sincos alone
+// ------------------------------------------------------------------------------------------
+#include "../fls_feat.cuh"
+
+// pass 0 runs cold (instruction cache misses on the SM), pass 1 warm: out[0..5] cold, out[6..11] warm
+__global__ void prologue_latency_kernel(long long *out_all, double *sink, uint64_t seed, PrefArgs pa) {
+  double acc = 0.0;
+  long long t0, t1;
+  __shared__ double w[2], rec[8];
+  for (int pass = 0; pass < 2; ++pass) {
+  long long *out = out_all + 6 * pass;
+  uint64_t c[4] = {(uint64_t)threadIdx.x + 7, 0, 0, 0};
+  t0 = clock64();
+  philox4x64(c, seed, 1);
+  acc += (double)(c[0] & 0xff);
+  t1 = clock64();
+  out[0] = t1 - t0;
+  const FeatBlocks fb = {1, {1 << 20}, {5.0}};
+  t0 = clock64();
+  acc += feat_normal((int64_t)(acc) + 3, 2, fb, seed);
+  t1 = clock64();
+  out[1] = t1 - t0;
+  t0 = clock64();
+  acc += feat_bias((int64_t)(acc * 0) + 5, seed);
+  t1 = clock64();
+  out[2] = t1 - t0;
+  w[0] = acc * 1e-3;
+  w[1] = 1.5;
+  t0 = clock64();
+  prefactor_rec(pa, w, acc, rec);
+  acc += rec[3];
+  t1 = clock64();
+  out[3] = t1 - t0;
+  const double u = 0.3 + acc * 1e-12;
+  t0 = clock64();
+  acc += sqrt(-2.0 * log(1.0 - u));
+  t1 = clock64();
+  out[4] = t1 - t0;
+  double sn, cs;
+  t0 = clock64();
+  sincos(6.283185307179586 * (u + acc * 1e-15), &sn, &cs);
+  acc += sn + cs;
+  t1 = clock64();
+  out[5] = t1 - t0;
+  }
+  sink[0] = acc;
+}
+
+extern "C" __attribute__((visibility("default"))) int mb_prologue_latency(long long *out_host) {
+  long long *d;
+  double *sink;
+  cudaMalloc(&d, 12 * sizeof(long long));
+  cudaMalloc(&sink, sizeof(double));
+  PrefArgs pa;
+  memset(&pa, 0, sizeof pa);
+  pa.D = 2;
+  pa.n_terms = 2;
+  pa.G = 0;
+  pa.pmode = PM_SIN;
+  pa.S = 4;
+  pa.scale = 0.02;
+  pa.terms[0].coef = -1.0;
+  pa.terms[0].alpha[0] = 2;
+  pa.terms[0].nfac = 2;
+  pa.terms[0].fac[0] = pa.terms[0].fac[1] = 0;
+  pa.terms[1].coef = -1.0;
+  pa.terms[1].alpha[1] = 2;
+  pa.terms[1].nfac = 2;
+  pa.terms[1].fac[0] = pa.terms[1].fac[1] = 1;
+  for (int rep = 0; rep < 3; ++rep) prologue_latency_kernel<<<1, 1>>>(d, sink, 0, pa);
+  cudaMemcpy(out_host, d, 12 * sizeof(long long), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  cudaFree(sink);
   return (int)cudaGetLastError();
 }

@@ -89,6 +89,16 @@ fls_status plan_operator(const fls_operator *op, int32_t dim, int32_t n_fields, 
       return fail(FLS_EINVAL, "%s: term %d field %d (use -1 for constant)", what, t, T.field);
     }
     pl.terms[t].group = (int8_t)grp;
+    // the monomial's factors in the order the fold multiplies them (axis 0 first, alpha_0
+    // times, ...): the device loop then runs |alpha| dependent multiplies and nothing else
+    if (order <= kMaxFac) {
+      int n = 0;
+      for (int k = 0; k < dim; ++k)
+        for (int e = 0; e < T.alpha[k]; ++e) pl.terms[t].fac[n++] = (int8_t)k;
+      pl.terms[t].nfac = (int8_t)order;
+    } else {
+      pl.terms[t].nfac = -1;
+    }
     if (order & 1) any_c = true; else any_s = true;
   }
   if (!any_c) { pl.pmode = PM_SIN; pl.kmode = KM_SIN; }

@@ -189,7 +189,7 @@ __device__ __forceinline__ void phase_check_wb(const FusedBatch &fz, int qb, int
   for (int64_t j = f0; j < f1; ++j) {
 #pragma unroll
     for (int k = 0; k < D; ++k) w[k] = feat_normal(j * D + k, D, fz.fb, fz.seed);
-    prefactor_rec(fz.pre[qb], w, feat_bias(j, fz.seed), rec);
+    prefactor_rec<>(fz.pre[qb], w, feat_bias(j, fz.seed), rec);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       double h = rec[D];
@@ -298,7 +298,8 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
         }
       }
       __syncthreads();
-      for (int t = threadIdx.x; t < nfe; t += kNT) prefactor_rec(fz.pre[qb], ws + t * D, bs[t], sp + t * S);
+      for (int t = threadIdx.x; t < nfe; t += kNT)
+        prefactor_rec<GG + 1>(fz.pre[qb], ws + t * D, bs[t], sp + t * S);
     } else {
       const double2 *src = reinterpret_cast<const double2 *>(a.pf + j0 * S);
       double2 *dst = reinterpret_cast<double2 *>(sp);

@@ -68,54 +68,84 @@ __device__ __forceinline__ double feat_bias(int64_t j, uint64_t seed) {
 // Explicit _rn arithmetic: no FMA contraction, so every call site (prefactor_one,
 // features_prefactor_kernel, the fused assembly prologue) rounds identically whatever the
 // inliner does around it.
+// NG > a.G bounds the unrolled group loops (a caller that knows the variant, e.g. the fused
+// assembly kernel, passes G + 1 and saves the registers).  w: the feature's D weights (shared or
+// global memory).  Latency matters here -- this fold sits on the critical path of every
+// assembly step (tools/prologue_latency.py): each term runs only its |alpha| dependent
+// multiplies (host-expanded factor list) and the group accumulators are registers.
+template <int NG = FLS_MAX_FIELDS + 1>
 __device__ inline void prefactor_rec(const PrefArgs &a, const double *w, double bj, double *out) {
-  double Ps[FLS_MAX_FIELDS + 1], Pc[FLS_MAX_FIELDS + 1];
-  for (int g = 0; g <= FLS_MAX_FIELDS; ++g) Ps[g] = Pc[g] = 0.0;
+  double Ps[NG], Pc[NG];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) Ps[g] = Pc[g] = 0.0;
   for (int t = 0; t < a.n_terms; ++t) {
     const TermDev &T = a.terms[t];
     double m = T.coef;
     int order = 0;
-    for (int k = 0; k < a.D; ++k)
-      for (int e = 0; e < T.alpha[k]; ++e) {
-        m = __dmul_rn(m, w[k]);
-        ++order;
-      }
+    const int nf = T.nfac;
+    if (nf >= 0) {
+      for (int e = 0; e < nf; ++e) m = __dmul_rn(m, w[T.fac[e]]);
+      order = nf;
+    } else {
+      for (int k = 0; k < a.D; ++k)
+        for (int e = 0; e < T.alpha[k]; ++e) {
+          m = __dmul_rn(m, w[k]);
+          ++order;
+        }
+    }
     const int p = order & 3;  // Phi_{|alpha| mod 4}: sin, cos, -sin, -cos
     if (p & 2) m = -m;
-    if (p & 1)
-      Pc[T.group] = __dadd_rn(Pc[T.group], m);
-    else
-      Ps[T.group] = __dadd_rn(Ps[T.group], m);
+    const int grp = T.group;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      if (grp == g) {
+        if (p & 1)
+          Pc[g] = __dadd_rn(Pc[g], m);
+        else
+          Ps[g] = __dadd_rn(Ps[g], m);
+      }
+    }
   }
   for (int k = 0; k < a.D; ++k) out[k] = __dmul_rn(w[k], kInvPi);
-  double bp = bj;
-  int o = a.D + 1;
+  const double bp = bj;
+  double *q = out + a.D + 1;
+  int used = a.D + 1;
   switch (a.pmode) {
     case PM_SIN:
-      for (int g = 0; g <= a.G; ++g) out[o++] = a.scale * Ps[g];
+#pragma unroll
+      for (int g = 0; g < NG; ++g)
+        if (g <= a.G) q[g] = a.scale * Ps[g];
+      used += a.G + 1;
       out[a.D] = __dmul_rn(bp, kInvPi);
       break;
     case PM_COSSHIFT:  // cos z = sin(z + pi/2)  (App. F quarter-wave shift)
-      for (int g = 0; g <= a.G; ++g) out[o++] = a.scale * Pc[g];
+#pragma unroll
+      for (int g = 0; g < NG; ++g)
+        if (g <= a.G) q[g] = a.scale * Pc[g];
+      used += a.G + 1;
       out[a.D] = __dadd_rn(__dmul_rn(bp, kInvPi), 0.5);
       break;
     case PM_FOLD: {    // Ps sin z + Pc cos z = rho sin(z + psi)
       const double ps = a.scale * Ps[0], pc = a.scale * Pc[0];
       const double rho = hypot(ps, pc);
       const double psi = atan2(pc, ps);
-      out[o++] = rho;
+      q[0] = rho;
+      used += 1;
       out[a.D] = __dmul_rn(__dadd_rn(bp, psi), kInvPi);
       break;
     }
     default:           // PM_SINCOS
-      for (int g = 0; g <= a.G; ++g) {
-        out[o++] = a.scale * Ps[g];
-        out[o++] = a.scale * Pc[g];
-      }
+#pragma unroll
+      for (int g = 0; g < NG; ++g)
+        if (g <= a.G) {
+          q[2 * g] = a.scale * Ps[g];
+          q[2 * g + 1] = a.scale * Pc[g];
+        }
+      used += 2 * (a.G + 1);
       out[a.D] = __dmul_rn(bp, kInvPi);
       break;
   }
-  for (; o < a.S; ++o) out[o] = 0.0;
+  for (int o = used; o < a.S; ++o) out[o] = 0.0;
 }
 
 }  // namespace fls

@@ -40,12 +40,15 @@ constexpr int kFUnroll = FLS_FUNROLL;       // features per loop iteration
 constexpr int kRowsCTA = 2 * kPairs * kNT;  // rows per CTA tile
 constexpr int kFC = 128;                    // features per shared-memory chunk
 
+constexpr int kMaxFac = 22;  // factor list length kept per term (orders up to 22)
 struct TermDev {
   double coef;
   int8_t alpha[FLS_MAX_DIM];
   int8_t group;  // 0 = constant coefficient, 1..G = compacted field groups
-  int8_t pad[7];
+  int8_t nfac;   // |alpha| if <= kMaxFac, else -1
+  int8_t fac[kMaxFac];  // alpha expanded in axis order: the axis of each factor of prod W^alpha
 };
+static_assert(sizeof(TermDev) == 40, "TermDev layout");
 
 struct PrefArgs {
   const double *W;

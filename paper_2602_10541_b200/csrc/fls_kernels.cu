@@ -3,6 +3,8 @@
 // Product code.  Paper = PAPER.md (arxiv 2602.10541), cited P:L<line>.
 #include <math.h>
 
+#include <algorithm>
+
 #include "fls_device.cuh"
 #include "fls_feat.cuh"
 #include "fls_internal.h"
@@ -111,13 +113,10 @@ __global__ void prefactor_batch_kernel(const PrefBatch b) {
 
 
 __device__ void prefactor_one(const PrefArgs &a, int64_t j) {
-  double w[FLS_MAX_DIM];
+  const double *w = a.W + j * a.D;  // read in place (the fold indexes it per factor)
   bool ok = true;
-  for (int k = 0; k < a.D; ++k) {
-    w[k] = a.W[j * a.D + k];
-    ok &= finite(w[k]);
-  }
-  double bj = a.b[j];
+  for (int k = 0; k < a.D; ++k) ok &= finite(w[k]);
+  const double bj = a.b[j];
   ok &= finite(bj);
   if (!ok) atomicOr(a.err, 1u);
   prefactor_rec(a, w, bj, a.pf + j * a.S);
@@ -129,13 +128,15 @@ __device__ void prefactor_one(const PrefArgs &a, int64_t j) {
 // transcendental chains run in parallel instead of D deep per thread -- then one thread per
 // feature draws b_j and folds every block's prefactor record from the shared W row.
 constexpr int kFpFeat = 64;
-__global__ void __launch_bounds__(kFpFeat * FLS_MAX_DIM)
+__global__ void __launch_bounds__(kFpFeat * (FLS_MAX_DIM + 1))
 features_prefactor_kernel(int32_t D, int64_t F, const FeatBlocks fb, uint64_t seed, double *W,
                           double *b, const PrefBatch pb) {
   __shared__ double ws[kFpFeat * FLS_MAX_DIM];
+  __shared__ double bs[kFpFeat];
   pdl_trigger();
   const int64_t j0 = (int64_t)blockIdx.x * kFpFeat;
   const int t = threadIdx.x;
+  // phase 1: the normals (t < kFpFeat D) and the biases (next kFpFeat threads), side by side
   if (t < kFpFeat * D) {
     const int64_t m = j0 * D + t;         // normal index; pair m/2 uses raw words m&~1, m|1
     if (m < F * D) {
@@ -143,21 +144,27 @@ features_prefactor_kernel(int32_t D, int64_t F, const FeatBlocks fb, uint64_t se
       ws[t] = w;
       W[m] = w;
     }
+  } else if (t < kFpFeat * (D + 1)) {
+    const int64_t j = j0 + (t - kFpFeat * D);
+    if (j < F) {
+      const double bj = feat_bias(j, seed);
+      bs[t - kFpFeat * D] = bj;
+      b[j] = bj;
+    }
   }
   __syncthreads();
-  if (t >= kFpFeat) return;
-  const int64_t j = j0 + t;
+  // phase 2: one thread per (block, feature) folds that block's record -- the blocks' folds
+  // run side by side instead of one after another
+  if (t >= kFpFeat * pb.n) return;
+  const int q = t / kFpFeat, tj = t % kFpFeat;
+  const int64_t j = j0 + tj;
   if (j >= F) return;
-  const double bj = feat_bias(j, seed);
-  b[j] = bj;
-  double w[FLS_MAX_DIM];
-  for (int k = 0; k < D; ++k) w[k] = ws[t * D + k];
-  for (int q = 0; q < pb.n; ++q) prefactor_rec(pb.blk[q], w, bj, pb.blk[q].pf + j * pb.blk[q].S);
+  prefactor_rec(pb.blk[q], ws + tj * D, bs[tj], pb.blk[q].pf + j * pb.blk[q].S);
 }
 
 cudaError_t launch_features_prefactor(int32_t dim, int64_t F, const FeatBlocks &fb, uint64_t seed,
                                       double *W, double *b, const PrefBatch &pb, cudaStream_t st) {
-  const int nt = ((kFpFeat * (dim > 1 ? dim : 1) + 31) / 32) * 32;
+  const int nt = ((kFpFeat * std::max(dim + 1, pb.n) + 31) / 32) * 32;
   features_prefactor_kernel<<<(unsigned)((F + kFpFeat - 1) / kFpFeat), nt, 0, st>>>(dim, F, fb, seed, W, b, pb);
   return cudaGetLastError();
 }
