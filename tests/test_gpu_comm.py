@@ -158,7 +158,7 @@ def test_torch_nccl_group_world1_through_dist():
         dist.destroy_process_group()
 
 
-def _worker(rank, world, port, name, env, q):
+def _worker(rank, world, port, name, env, q, shards=None):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), **env)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -170,10 +170,14 @@ def _worker(rank, world, port, name, env, q):
         p = wl.make_problem(name, "mini")
         W, b = p.parity_features()
         F, R = p.n_features, p.n_rows
-        a, e = wl.shard_range(R, rank, world)
+        a, e = shards[rank] if shards else wl.shard_range(R, rank, world)
         ctx = fls.Context(0)
         Wd, bd = torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda()
-        Ab, lda = fls.fls_assemble(ctx, Wd, bd, _blocks(p), row_begin=a, row_end=e)
+        if e > a:
+            Ab, lda = fls.fls_assemble(ctx, Wd, bd, _blocks(p), row_begin=a, row_end=e)
+        else:                       # a rank without rows still takes part in the solve
+            lda = 4
+            Ab = torch.zeros(((F + 1) * lda,), dtype=torch.float64, device="cuda")
         try:
             beta, res = fdist.tsqr_solve(Ab, e - a, lda, F, ridge_rel=p.ridge_rel, ctx=ctx)
         except fls.FlsError as err:
@@ -187,12 +191,12 @@ def _worker(rank, world, port, name, env, q):
         dist.destroy_process_group()
 
 
-def _run(name, world, env=None):
+def _run(name, world, env=None, shards=None):
     import torch.multiprocessing as mp
     mctx = mp.get_context("spawn")
     q = mctx.Queue()
     port = _port()
-    procs = [mctx.Process(target=_worker, args=(r, world, port, name, env or {}, q))
+    procs = [mctx.Process(target=_worker, args=(r, world, port, name, env or {}, q, shards))
              for r in range(world)]
     for pr in procs:
         pr.start()
@@ -226,6 +230,30 @@ def test_p2p_tsqr_across_processes_matches_dense_and_oracle(name, world):
         assert np.array_equal(u, out[0][0]) and res == out[0][1]   # replicated
     # the residual norm is a rounding-level number on C1 (~1e-12): compare on the rhs's scale
     assert abs(out[0][1] - res_d) <= 1e-9 * max(abs(res_d), 1e-2)
+    ctx.close()
+
+
+def test_p2p_tsqr_uneven_shards_trapezoidal_and_empty_rank():
+    """rank 0 holds 200 rows (< F + 1 = 501: an upper-TRAPEZOIDAL factor), rank 1 the rest, rank 2
+    none at all -- the stack is padded to kmax rows, the empty rank sends zeros, every rank gets
+    the same beta, equal to the dense solve's"""
+    import workloads as wl
+    from paper_2602_10541_b200 import fls
+    p = wl.make_problem("c1_poisson1d", "mini")
+    R = p.n_rows
+    out = _run("c1_poisson1d", 3, shards=[(0, 200), (200, R), (R, R)])
+    W, b = p.parity_features()
+    ctx = fls.Context(0)
+    Wd, bd = torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda()
+    beta_d, _ = _dense(ctx, p, Wd, bd, _blocks(p))
+    u_d = fls.fls_eval(ctx, Wd, bd, beta_d, torch.from_numpy(p.test_points(2000)).cuda()).cpu().numpy()
+    u_o = _oracle_u(p)
+    for r in range(3):
+        u, res, used = out[r]
+        assert used == "p2p"
+        assert np.linalg.norm(u - u_o) / np.linalg.norm(u_o) <= 1e-6
+        assert np.linalg.norm(u - u_d) / np.linalg.norm(u_d) <= 1e-9
+        assert np.array_equal(u, out[0][0])
     ctx.close()
 
 
