@@ -448,7 +448,10 @@ fls_status assemble_range(fls_ctx *ctx, const AsmPlan &ap, int32_t dim, int64_t 
         fz.write_wb = first_launch ? 1 : 0;
         for (int i = 0; i < nb; ++i)
           make_pref(ctx, fz.pre[i], ap.plans[bq[i]], blocks[bq[i]], bq[i], fz.W, fz.b, dim, F, s_norm);
-        e = launch_assemble_cm_fused(dim, bG, batch, nb, fz, st);
+        // PDL behind whatever precedes: the first chunk's draws and folds overlap it (the
+        // kernel touches no global memory before its griddepcontrol.wait)
+        e = launch_assemble_cm_fused(dim, bG, batch, nb, fz, st,
+                                     pdl && !ctx->timing && entries <= kPdlMaxEntries);
       } else {
         e = launch_assemble_cm(dim, bG, bK, batch, nb, st,
                                pdl && !ctx->timing && entries <= kPdlMaxEntries);
@@ -501,8 +504,9 @@ fls_status assemble_range(fls_ctx *ctx, const AsmPlan &ap, int32_t dim, int64_t 
 // call so tuning sweeps / tests can switch it (FLS_FUSE_MAX_ENTRIES=0 turns the fusion off)
 int64_t fuse_max_entries() {
   const char *v = getenv("FLS_FUSE_MAX_ENTRIES");
-  // default 2^22: C1 (5e5 entries, graph step 10.2 -> 8.2 us); C2 (9.6e6) is slower fused
-  // (24.1 vs 20.5 us: each CTA's Box-Muller + fold chain, ~3 us, sits on its critical path)
+  // default 2^22: C1 (5e5 entries: 10-step-graph step 7.1 -> 6.1 us fused); C2 (9.6e6) is
+  // slower fused (19.8 vs 18.4 us: each CTA's Box-Muller + fold chain sits on its critical
+  // path, tools/small_step_probe.py)
   return v && *v ? (int64_t)atoll(v) : (int64_t(1) << 22);
 }
 
@@ -591,11 +595,14 @@ fls_status fls_features_assemble(fls_ctx *ctx, int32_t dim, int64_t n_features, 
       proto.W = W;
       proto.b = b;
       return assemble_range(ctx, ap, dim, F, blocks, nullptr, row_begin, row_end, A, lda, layout,
-                            rhs, ctx->stream, false, &proto, s_norm);
+                            rhs, ctx->stream, pdl_enabled(), &proto, s_norm);
     }
   }
   if (overflow) pb.n = 0;  // many blocks: fused features only, prefactors in batches below
-  cudaError_t e = launch_features_prefactor(dim, F, fb, seed, W, b, pb, ctx->stream);
+  // PDL behind whatever precedes on the stream (typically the previous step's assembly): the
+  // draws and folds overlap its tail, the writes wait for it (features_prefactor_kernel)
+  const bool pdl_fp = pdl_enabled() && !ctx->timing && n_local * F <= kPdlMaxEntries;
+  cudaError_t e = launch_features_prefactor(dim, F, fb, seed, W, b, pb, ctx->stream, pdl_fp);
   if (e != cudaSuccess) return cuda_fail(e, "features_prefactor_kernel");
   if (overflow) {
     if (fls_status s = launch_prefactors(ctx, ap, W, b, dim, F, normalize, blocks, row_begin,

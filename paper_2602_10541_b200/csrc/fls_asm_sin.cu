@@ -29,8 +29,7 @@ static cudaError_t go_sin(AsmArgs *blks, int n, cudaStream_t st, bool pdl,
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
       }
-      kern<<<(unsigned)total, kNT, smem, st>>>(bt, *fz);
-      return cudaGetLastError();
+      return asm_launch(kern, (unsigned)total, smem, st, pdl, bt, *fz);
     } else {
       return cudaErrorNotSupported;
     }
@@ -44,11 +43,11 @@ static cudaError_t go_sin(AsmArgs *blks, int n, cudaStream_t st, bool pdl,
 }
 
 cudaError_t launch_assemble_cm_fused(int D, int G, AsmArgs *blks, int n, const FusedBatch &fz,
-                                     cudaStream_t st) {
+                                     cudaStream_t st, bool pdl) {
   if (G > 1) return cudaErrorNotSupported;
 #define FLS_FG(d)                                            \
-  return G == 0 ? go_sin<d, 0>(blks, n, st, false, &fz)      \
-                : go_sin<d, 1>(blks, n, st, false, &fz);
+  return G == 0 ? go_sin<d, 0>(blks, n, st, pdl, &fz)        \
+                : go_sin<d, 1>(blks, n, st, pdl, &fz);
   switch (D) {
     case 1: FLS_FG(1)
     case 2: FLS_FG(2)

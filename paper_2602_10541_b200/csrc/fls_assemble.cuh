@@ -221,11 +221,59 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
   static_assert(S % 2 == 0, "pf stride must be even for 16-byte smem reads");
   extern __shared__ __align__(16) double sp[];
 
+  // let the next PDL launch on the stream (the next call's feature / prefactor kernel, which
+  // writes nothing before its own griddepcontrol.wait) start while this grid runs
+  pdl_trigger();
   int qb = 0;
   while (qb + 1 < bt.n && (int64_t)blockIdx.x >= bt.cta_end[qb]) ++qb;
   const AsmArgs &a = bt.blk[qb];
   const int64_t cta = (int64_t)blockIdx.x - (qb ? bt.cta_end[qb - 1] : 0);
   const int64_t tile = cta % bt.rt[qb], group = cta / bt.rt[qb];
+  // this CTA's feature range [f0, f1) (a.fpc features per CTA, chosen by the launcher), walked
+  // in shared-memory chunks of at most kFC records
+  const int64_t f0 = group * a.fpc;
+  const int64_t f1 = f0 + a.fpc < a.F ? f0 + a.fpc : a.F;
+  // phase-range guard (FLS_MAX_PHASE): |h_ij| <= ||W_j/pi||_1 ||x_i||_inf + |b'_j/pi|.  The
+  // feature side is max-reduced over the CTA's records chunk by chunk (s_guard, off the entry
+  // path); at the end a thread whose bound exceeds the limit re-checks its rows exactly.
+  __shared__ unsigned long long s_guard[2];
+  if (threadIdx.x == 0) s_guard[0] = s_guard[1] = 0ull;  // visible after the first chunk sync
+
+  // fused: a1 -- the chunk's normals and biases, one draw per thread (the
+  // features_prefactor_kernel draws: bit-identical) into shared memory after the records, both
+  // Philox chains side by side; a2 -- one thread per feature folds its record.  Reads nothing
+  // from global memory; writes W, b only when wr.
+  bool wr = false;
+  if constexpr (kFused) wr = fz.write_wb && qb == 0 && tile == 0;
+  auto fused_chunk = [&](int64_t j0, int nfe, bool write_wb) {
+    if constexpr (kFused) {
+      double *ws = sp + kFC * S;      // normals (nfe * D), then biases (nfe)
+      double *bs = ws + kFC * D;
+      for (int t = threadIdx.x; t < nfe * (D + 1); t += kNT) {
+        if (t < nfe * D) {
+          const int64_t m = j0 * D + t;
+          const double w = feat_normal(m, D, fz.fb, fz.seed);
+          ws[t] = w;
+          if (write_wb) fz.W[m] = w;
+        } else {
+          const int64_t j = j0 + (t - nfe * D);
+          const double bj = feat_bias(j, fz.seed);
+          bs[t - nfe * D] = bj;
+          if (write_wb) fz.b[j] = bj;
+        }
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < nfe; t += kNT)
+        prefactor_rec<GG + 1>(fz.pre[qb], ws + t * D, bs[t], sp + t * S);
+    }
+  };
+  const int nfe0 = (f1 - f0) < kFC ? (int)(f1 - f0) : kFC;
+  // the first chunk's records before the wait: with programmatic dependent launch they are
+  // drawn while the previous kernel on the stream still runs
+  if (kFused && f0 < f1) fused_chunk(f0, nfe0, false);
+  // no global memory is read or written above this line: the kernel may run ahead of its
+  // predecessor (PDL), which may still be producing X / fields / values or reading A, W, b
+  pdl_wait();
 
   // local rows (A-relative) of this thread: rbase + p*2*kNT + {0, 1}; rbase is even.
   // The block's points map to local rows [lr0, lr1): point i = pt0 + (r - lr0).
@@ -258,48 +306,24 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
     }
   }
   if (bad) atomicOr(a.err, kErrNonFinite);
-  // phase-range guard (FLS_MAX_PHASE): |h_ij| <= ||W_j/pi||_1 ||x_i||_inf + |b'_j/pi|.  The
-  // feature side is max-reduced over the CTA's records chunk by chunk (s_guard, off the entry
-  // path); at the end a thread whose bound exceeds the limit re-checks its rows exactly.
-  __shared__ unsigned long long s_guard[2];
   double xinf = 0.0;
 #pragma unroll
   for (int q = 0; q < NQ; ++q)
 #pragma unroll
     for (int k = 0; k < D; ++k) xinf = fmax(xinf, fabs(x[q][k]));
-  if (threadIdx.x == 0) s_guard[0] = s_guard[1] = 0ull;  // visible after the first chunk sync
-  pdl_wait();  // the prefactor records of the preceding launch are complete from here on
+  if constexpr (kFused) {
+    if (wr && f0 < f1) {  // the first chunk's W, b (drawn before the wait) go out now
+      const double *ws = sp + kFC * S, *bs = ws + kFC * D;
+      for (int t = threadIdx.x; t < nfe0 * D; t += kNT) fz.W[f0 * D + t] = ws[t];
+      for (int t = threadIdx.x; t < nfe0; t += kNT) fz.b[f0 + t] = bs[t];
+    }
+  }
 
-  // this CTA's feature range [f0, f1) (a.fpc features per CTA, chosen by the launcher), walked
-  // in shared-memory chunks of at most kFC records
-  const int64_t f0 = group * a.fpc;
-  const int64_t f1 = f0 + a.fpc < a.F ? f0 + a.fpc : a.F;
   for (int64_t j0 = f0; j0 < f1; j0 += kFC) {
     const int nfe = (f1 - j0) < kFC ? (int)(f1 - j0) : kFC;
     __syncthreads();  // previous chunk's records no longer in use
     if constexpr (kFused) {
-      // a1: the chunk's normals and biases, one draw per thread (the features_prefactor_kernel
-      // draws: bit-identical) into shared memory after the records -- both Philox chains run
-      // side by side; a2: one thread per feature folds its record
-      double *ws = sp + kFC * S;      // normals (nfe * D), then biases (nfe)
-      double *bs = ws + kFC * D;
-      const bool wr = fz.write_wb && qb == 0 && tile == 0;
-      for (int t = threadIdx.x; t < nfe * (D + 1); t += kNT) {
-        if (t < nfe * D) {
-          const int64_t m = j0 * D + t;
-          const double w = feat_normal(m, D, fz.fb, fz.seed);
-          ws[t] = w;
-          if (wr) fz.W[m] = w;
-        } else {
-          const int64_t j = j0 + (t - nfe * D);
-          const double bj = feat_bias(j, fz.seed);
-          bs[t - nfe * D] = bj;
-          if (wr) fz.b[j] = bj;
-        }
-      }
-      __syncthreads();
-      for (int t = threadIdx.x; t < nfe; t += kNT)
-        prefactor_rec<GG + 1>(fz.pre[qb], ws + t * D, bs[t], sp + t * S);
+      if (j0 != f0) fused_chunk(j0, nfe, wr);
     } else {
       const double2 *src = reinterpret_cast<const double2 *>(a.pf + j0 * S);
       double2 *dst = reinterpret_cast<double2 *>(sp);

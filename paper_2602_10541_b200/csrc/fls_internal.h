@@ -151,12 +151,15 @@ struct FusedBatch {
 // for the others)
 inline bool fused_variant(int D, int G, int kmode) { return kmode == KM_SIN && G <= 1 && D >= 1 && D <= FLS_MAX_DIM; }
 cudaError_t launch_assemble_cm_fused(int D, int G, AsmArgs *blks, int n, const FusedBatch &fz,
-                                     cudaStream_t st);
+                                     cudaStream_t st, bool pdl);
 
 cudaError_t launch_prefactor(const PrefArgs &a, cudaStream_t st);
 cudaError_t launch_prefactor_batch(const PrefBatch &b, int64_t F, cudaStream_t st);
+// pdl: launch behind the previous kernel with programmatic dependent launch (the kernel writes
+// nothing before griddepcontrol.wait, so it may overlap whatever precedes it on the stream)
 cudaError_t launch_features_prefactor(int32_t dim, int64_t F, const FeatBlocks &fb, uint64_t seed,
-                                      double *W, double *b, const PrefBatch &pb, cudaStream_t st);
+                                      double *W, double *b, const PrefBatch &pb, cudaStream_t st,
+                                      bool pdl);
 // blks: n (<= kMaxBatch) blocks of one variant; fpc is set per block by the launcher
 // pdl: launch with programmatic dependent launch (only right after this call's prefactor launch)
 cudaError_t launch_assemble_cm(int D, int G, int kmode, AsmArgs *blks, int n, cudaStream_t st,

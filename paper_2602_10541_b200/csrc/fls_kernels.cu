@@ -122,51 +122,69 @@ __device__ void prefactor_one(const PrefArgs &a, int64_t j) {
   prefactor_rec(a, w, bj, a.pf + j * a.S);
 }
 
-// a1 + a2 fused (fls_features_assemble).  A CTA covers kFpFeat features: first one thread per
-// NORMAL (feature j, axis k; normal index m = j*D + k) draws it exactly as features_kernel does
-// (same Philox words, same Box-Muller arithmetic -> bit-identical W) into shared memory -- the
-// transcendental chains run in parallel instead of D deep per thread -- then one thread per
-// feature draws b_j and folds every block's prefactor record from the shared W row.
+// a1 + a2 fused (fls_features_assemble).  A CTA covers kFpFeat features: one thread per NORMAL
+// (feature j, axis k; normal index m = j*D + k) draws it exactly as features_kernel does (same
+// Philox words, same Box-Muller arithmetic -> bit-identical W) and, beside them, one thread per
+// feature draws b_j; then one thread per (block, feature) folds that block's record.  Everything
+// is computed in shared memory FIRST and written to W, b and the record arrays only after
+// griddepcontrol.wait: launched with programmatic dependent launch behind the previous call's
+// assembly (which triggers at its start), the draws and folds of step k+1 overlap the tail of
+// step k's assembly, and nothing the running kernel reads is overwritten early.  Without the
+// PDL attribute the wait is a no-op.
 constexpr int kFpFeat = 64;
+constexpr int kSrec = pf_stride(FLS_MAX_DIM, FLS_MAX_FIELDS, KM_SINCOS);
 __global__ void __launch_bounds__(kFpFeat * (FLS_MAX_DIM + 1))
 features_prefactor_kernel(int32_t D, int64_t F, const FeatBlocks fb, uint64_t seed, double *W,
-                          double *b, const PrefBatch pb) {
+                          double *b, const PrefBatch pb, int32_t smax) {
   __shared__ double ws[kFpFeat * FLS_MAX_DIM];
   __shared__ double bs[kFpFeat];
+  extern __shared__ double sr[];  // records: [block q][feature tj][smax]
   pdl_trigger();
   const int64_t j0 = (int64_t)blockIdx.x * kFpFeat;
+  const int nf = (int)((F - j0) < kFpFeat ? (F - j0) : kFpFeat);
   const int t = threadIdx.x;
   // phase 1: the normals (t < kFpFeat D) and the biases (next kFpFeat threads), side by side
   if (t < kFpFeat * D) {
-    const int64_t m = j0 * D + t;         // normal index; pair m/2 uses raw words m&~1, m|1
-    if (m < F * D) {
-      const double w = feat_normal(m, D, fb, seed);
-      ws[t] = w;
-      W[m] = w;
-    }
+    if (t < nf * D) ws[t] = feat_normal(j0 * D + t, D, fb, seed);  // normal pair m/2: words m&~1, m|1
   } else if (t < kFpFeat * (D + 1)) {
-    const int64_t j = j0 + (t - kFpFeat * D);
-    if (j < F) {
-      const double bj = feat_bias(j, seed);
-      bs[t - kFpFeat * D] = bj;
-      b[j] = bj;
-    }
+    const int tj = t - kFpFeat * D;
+    if (tj < nf) bs[tj] = feat_bias(j0 + tj, seed);
   }
   __syncthreads();
   // phase 2: one thread per (block, feature) folds that block's record -- the blocks' folds
   // run side by side instead of one after another
-  if (t >= kFpFeat * pb.n) return;
-  const int q = t / kFpFeat, tj = t % kFpFeat;
-  const int64_t j = j0 + tj;
-  if (j >= F) return;
-  prefactor_rec(pb.blk[q], ws + tj * D, bs[tj], pb.blk[q].pf + j * pb.blk[q].S);
+  if (t < kFpFeat * pb.n) {
+    const int q = t / kFpFeat, tj = t % kFpFeat;
+    if (tj < nf) prefactor_rec(pb.blk[q], ws + tj * D, bs[tj], sr + (q * kFpFeat + tj) * smax);
+  }
+  __syncthreads();
+  pdl_wait();  // the previous kernel on the stream is complete (and its memory visible) here
+  for (int i = t; i < nf * D; i += blockDim.x) W[j0 * D + i] = ws[i];
+  for (int i = t; i < nf; i += blockDim.x) b[j0 + i] = bs[i];
+  for (int q = 0; q < pb.n; ++q) {
+    const int S = pb.blk[q].S;
+    double *dst = pb.blk[q].pf + j0 * S;
+    for (int i = t; i < nf * S; i += blockDim.x) dst[i] = sr[(q * kFpFeat + i / S) * smax + i % S];
+  }
 }
 
 cudaError_t launch_features_prefactor(int32_t dim, int64_t F, const FeatBlocks &fb, uint64_t seed,
-                                      double *W, double *b, const PrefBatch &pb, cudaStream_t st) {
-  const int nt = ((kFpFeat * std::max(dim + 1, pb.n) + 31) / 32) * 32;
-  features_prefactor_kernel<<<(unsigned)((F + kFpFeat - 1) / kFpFeat), nt, 0, st>>>(dim, F, fb, seed, W, b, pb);
-  return cudaGetLastError();
+                                      double *W, double *b, const PrefBatch &pb, cudaStream_t st,
+                                      bool pdl) {
+  int smax = 2;
+  for (int q = 0; q < pb.n; ++q) smax = std::max(smax, pb.blk[q].S);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((F + kFpFeat - 1) / kFpFeat));
+  cfg.blockDim = dim3(((kFpFeat * std::max(dim + 1, pb.n) + 31) / 32) * 32);
+  cfg.dynamicSmemBytes = sizeof(double) * (size_t)std::max(pb.n, 1) * kFpFeat * smax;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, features_prefactor_kernel, dim, F, fb, seed, W, b, pb,
+                            (int32_t)smax);
 }
 
 cudaError_t launch_prefactor(const PrefArgs &a, cudaStream_t st) {

@@ -889,3 +889,32 @@ def test_eval_phase_beyond_limit_reports_unsupported(ctx):
                      torch.ones(W.shape[0], dtype=torch.float64, device="cuda"), torch.from_numpy(X).cuda())
     with pytest.raises(FlsError, match="EUNSUPPORTED"):
         fls.fls_sync(ctx)
+
+
+def test_back_to_back_calls_with_pdl_overlap_keep_stream_order(ctx):
+    """the feature / prefactor kernel of call k+1 starts (programmatic dependent launch) while
+    call k's assembly still runs, and call k+1's assembly launches early too: every write of
+    call k+1 must still land after call k's.  Alternate two sets of rhs values (and two seeds)
+    into the SAME [A | b] many times; the buffer must always hold the last call's result."""
+    p = wl.make_problem("c2_poisson2d", "full")
+    d, F, R = p.dim, p.n_features, p.n_rows
+    base = dev_blocks(p)
+    alt = [fls.Block(b.X, b.terms, b.weight, -3.0 * b.values + 1.0, b.fields) for b in base]
+    sets = [fls.BlockSet(base, d), fls.BlockSet(alt, d)]
+    lda = fls.round_up(R, 4)
+    refs = []
+    for k in range(2):
+        W, b, A, _ = fls.fls_features_assemble(ctx, d, F, p.sigma, k, sets[k], lda=lda)
+        fls.fls_sync(ctx)
+        refs.append((W.clone(), b.clone(), A[: (F + 1) * lda].clone()))
+    A = torch.empty(((F + 1) * lda,), dtype=torch.float64, device="cuda")
+    W = torch.empty((F, d), dtype=torch.float64, device="cuda")
+    b = torch.empty((F,), dtype=torch.float64, device="cuda")
+    for n in (1, 2, 3, 8, 15):
+        for i in range(n):
+            fls.fls_features_assemble(ctx, d, F, p.sigma, i % 2, sets[i % 2], W=W, b=b, A=A, lda=lda)
+        fls.fls_sync(ctx)
+        last = (n - 1) % 2
+        assert torch.equal(W, refs[last][0]) and torch.equal(b, refs[last][1])
+        V, Vr = A.view(F + 1, lda)[:, :R], refs[last][2].view(F + 1, lda)[:, :R]
+        assert torch.equal(V, Vr), n
