@@ -259,7 +259,7 @@ def e2e_measure(args, p, ctx, W, b, a, e, world, local):
     step()                                   # warm-up (staging allocation, first touch)
     times = []
     for _ in range(args.e2e_steps):
-        if world > 1:
+        if dist.is_initialized():
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -267,7 +267,7 @@ def e2e_measure(args, p, ctx, W, b, a, e, world, local):
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
     t = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=_cdev())
-    if world > 1:
+    if dist.is_initialized():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     s_step = float(t.item())
     h2d = in_bytes_points + n_calls * 8 * (F * d + F)
@@ -328,7 +328,7 @@ def solve_measure(args, world, rank, local):
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
 
     def run():
-        if world > 1:
+        if torch.distributed.is_initialized():
             torch.distributed.barrier()
         torch.cuda.synchronize()
         ev[0].record(st)
@@ -347,7 +347,7 @@ def solve_measure(args, world, rank, local):
     u, res = run()
     ph = [ev[k].elapsed_time(ev[k + 1]) for k in range(4)]
     t = torch.tensor(ph, dtype=torch.float64, device=_cdev())
-    if world > 1:
+    if torch.distributed.is_initialized():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ph = [float(v) for v in t.tolist()]
     us = p.u_star(Xt.cpu().numpy())
@@ -724,7 +724,10 @@ def run_ranks(args) -> int:
         sys.stderr.write(f"bench.py: rank {rank} has LOCAL_RANK {local} but the node has {have} GPUs\n")
         return 2
     backend = "gloo" if shared else eng_cls.backend
-    if world > 1:
+    # a process group whenever a launcher started us (also at world size 1: the timing
+    # collectives then run through NCCL exactly as at N > 1)
+    pg = "WORLD_SIZE" in os.environ and "MASTER_ADDR" in os.environ
+    if pg:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -733,7 +736,7 @@ def run_ranks(args) -> int:
     cdev = "cpu" if backend == "gloo" else eng.coll_device()
     # one device per rank: count the distinct devices behind the ranks
     ids = [eng.device_id()]
-    if world > 1:
+    if pg:
         ids = [None] * world
         dist.all_gather_object(ids, eng.device_id())
     n_gpus = len(set(ids))
@@ -741,29 +744,29 @@ def run_ranks(args) -> int:
         if rank == 0:
             sys.stderr.write(f"bench.py: {world} ranks share {n_gpus} device(s); one GPU per rank "
                              f"is required\n")
-        if world > 1:
+        if pg:
             dist.destroy_process_group()
         return 2
     for _ in range(args.warmup):
         eng.step()
     eng.sync()
     eng.begin_timed()
-    if world > 1:
+    if pg:
         dist.barrier()
     eng.start()
     for _ in range(args.steps):
         eng.step()
     ms_total = eng.stop()
-    if world > 1:
+    if pg:
         dist.barrier()
     eng.end_timed()
     t = torch.tensor([ms_total], dtype=torch.float64, device=cdev)
-    if world > 1:
+    if pg:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = float(t.item()) / args.steps
     mine = eng.kernel_report(args.steps)
     per_rank = [mine]
-    if world > 1:
+    if pg:
         per_rank = [None] * world
         dist.all_gather_object(per_rank, mine)
     line = {"metric": METRIC, "value": eng.entries_total / (ms_step / 1e3), "unit": UNIT,
@@ -775,7 +778,7 @@ def run_ranks(args) -> int:
     if rank == 0:
         print(json.dumps(line), flush=True)
     eng.close()
-    if world > 1:
+    if pg:
         dist.destroy_process_group()
     return 0
 

@@ -106,3 +106,17 @@ def test_world_size_must_match_gpus_and_devices_must_be_distinct():
     r = _bench(["--gpus", "2", "--steps", "2", "--warmup", "3"],
                dict(FAKE, FAKE_GPUS="2", FAKE_SAME_DEVICE="1"))
     assert r.returncode != 0 and "share 1 device" in r.stderr and not _json_lines(r.stdout)
+
+
+def test_launcher_at_world_size_one_runs_the_collective_path():
+    """under torchrun with one rank the process group is created too (the timing collectives
+    then run exactly as at N > 1)"""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env.update(FAKE, FAKE_GPUS="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "1", "--master-addr", "127.0.0.1", "--master-port",
+                        str(_port()), "bench.py", "--gpus", "1", "--steps", "2", "--warmup", "3"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = _json_lines(r.stdout)
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 1 and lines[0]["ranks"] == 1
