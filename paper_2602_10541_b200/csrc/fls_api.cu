@@ -928,11 +928,14 @@ fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int6
   if (!(ridge_rel >= 0.0) || !std::isfinite(ridge_rel))
     return fail(FLS_EINVAL, "ridge_rel must be >= 0 and finite");
   DeviceGuard g(ctx->device);
-  if (fls_status s = fls_sync(ctx)) return s;  // surface pending async errors first
+  // surface pending async errors first -- with a communicator the status is agreed with the
+  // other ranks inside comm_solve (returning here alone would leave them waiting)
+  const fls_status pending = fls_sync(ctx);
   bool handled = false;
   fls_status cs = comm_solve(ctx, Ab, n_rows, lda, n_features, ridge_rel, -1.0, beta, resid_norm,
-                             &handled);
+                             &handled, pending);
   if (handled) return cs;
+  if (pending) return pending;
   double sqrt_mu = 0.0;
   if (ridge_rel > 0.0) {  // reading A16: sqrt(mu) = tau ||A||_F (A without the rhs column)
     if (lda < n_rows) return fail(FLS_EINVAL, "lda < n_rows");
@@ -951,11 +954,12 @@ fls_status fls_solve_mu(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, i
   if (n_rows < 0) return fail(FLS_EINVAL, "n_rows < 0");
   if (!(sqrt_mu >= 0.0) || !std::isfinite(sqrt_mu)) return fail(FLS_EINVAL, "sqrt_mu must be >= 0");
   DeviceGuard g(ctx->device);
-  if (fls_status s = fls_sync(ctx)) return s;
+  const fls_status pending = fls_sync(ctx);
   bool handled = false;
   fls_status cs = comm_solve(ctx, Ab, n_rows, lda, n_features, 0.0, sqrt_mu, beta, resid_norm,
-                             &handled);
+                             &handled, pending);
   if (handled) return cs;
+  if (pending) return pending;
   return solve_local(ctx, Ab, n_rows, lda, n_features, sqrt_mu, beta, resid_norm);
 }
 

@@ -410,7 +410,7 @@ void comm_destroy(fls_ctx *ctx) {
 
 fls_status comm_solve(fls_ctx *ctx, double *Ab, int64_t n_local, int64_t lda, int64_t F,
                       double ridge_rel, double sqrt_mu_abs, double *beta, double *resid_norm,
-                      bool *handled) {
+                      bool *handled, fls_status pending) {
   Comm *c = ctx->comm;
   *handled = false;
   if (!c || (c->nranks == 1 && !c->force_tsqr)) return FLS_OK;
@@ -422,8 +422,9 @@ fls_status comm_solve(fls_ctx *ctx, double *Ab, int64_t n_local, int64_t lda, in
   pl.nc = F + 1;
   pl.k = std::min<int64_t>(n_local, pl.nc);
   // step 0: local argument check and the local ||A_r||_F^2, then agree on sizes and the ridge
-  fls_status st = FLS_OK;
-  if (lda < n_local) st = fail(FLS_EINVAL, "lda %lld < n_local %lld", (long long)lda, (long long)n_local);
+  fls_status st = pending;  // (its message is already in fls_last_error)
+  if (st == FLS_OK && lda < n_local)
+    st = fail(FLS_EINVAL, "lda %lld < n_local %lld", (long long)lda, (long long)n_local);
   double fro2 = 0.0;
   if (st == FLS_OK && relative && ridge_rel > 0.0 && n_local > 0)
     st = frob2_host(ctx, Ab, n_local, lda, F, &fro2);
@@ -438,7 +439,8 @@ fls_status comm_solve(fls_ctx *ctx, double *Ab, int64_t n_local, int64_t lda, in
   for (int r = 0; r < pl.P; ++r) {
     if (all[r].status != FLS_OK) {
       if (r == c->rank) return fail(st, "%s", keep.c_str());
-      return fail((fls_status)all[r].status, "fls_solve: argument error on rank %d", r);
+      return fail((fls_status)all[r].status, "fls_solve failed on rank %d (%s there)", r,
+                  fls_status_string((fls_status)all[r].status));
     }
     if (all[r].F != F || all[r].ridge != h.ridge)
       return fail(FLS_EINVAL, "fls_solve: n_features / ridge differ between ranks (rank %d)", r);

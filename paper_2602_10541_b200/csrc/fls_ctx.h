@@ -82,9 +82,11 @@ fls_status solve_stacked_impl(fls_ctx *ctx, const double *S, int32_t P, int64_t 
                               double *resid_norm);
 // multi-rank solve when a communicator is attached (fls_comm.cu); *handled = false when the
 // ctx has no communicator (or one rank and no forced TSQR) so the caller solves locally
+// pending: this rank's status before the call (e.g. a pending FLS_ENONFINITE), agreed with the
+// other ranks so that a local failure is returned everywhere instead of leaving peers waiting
 fls_status comm_solve(fls_ctx *ctx, double *Ab, int64_t n_local, int64_t lda, int64_t F,
                       double ridge_rel, double sqrt_mu_abs, double *beta, double *resid_norm,
-                      bool *handled);
+                      bool *handled, fls_status pending = FLS_OK);
 void comm_destroy(fls_ctx *ctx);
 
 }  // namespace fls

@@ -173,8 +173,11 @@ def _worker(rank, world, port, name, env, q, shards=None):
         a, e = shards[rank] if shards else wl.shard_range(R, rank, world)
         ctx = fls.Context(0)
         Wd, bd = torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda()
+        blocks = _blocks(p)
+        if os.environ.get("NAN_ON_RANK") == str(rank):   # a pending FLS_ENONFINITE on this rank
+            blocks[0].X[3, 0] = float("nan")
         if e > a:
-            Ab, lda = fls.fls_assemble(ctx, Wd, bd, _blocks(p), row_begin=a, row_end=e)
+            Ab, lda = fls.fls_assemble(ctx, Wd, bd, blocks, row_begin=a, row_end=e)
         else:                       # a rank without rows still takes part in the solve
             lda = 4
             Ab = torch.zeros(((F + 1) * lda,), dtype=torch.float64, device="cuda")
@@ -255,6 +258,13 @@ def test_p2p_tsqr_uneven_shards_trapezoidal_and_empty_rank():
         assert np.linalg.norm(u - u_d) / np.linalg.norm(u_d) <= 1e-9
         assert np.array_equal(u, out[0][0])
     ctx.close()
+
+
+def test_pending_error_on_one_rank_is_returned_on_every_rank():
+    """rank 1's assembly saw a NaN (FLS_ENONFINITE pending at its fls_solve): the status is agreed
+    with the peers inside the solve -- every rank returns an error, none waits forever"""
+    out = _run("c1_poisson1d", 2, {"NAN_ON_RANK": "1"}, shards=[(0, 2), (2, 1002)])
+    assert out[1][1] == "FLS_ENONFINITE" and out[0][1] == "FLS_ENONFINITE"
 
 
 def test_p2p_unavailable_without_nccl_errors_on_every_rank():
