@@ -292,6 +292,64 @@ def e2e_measure(args, p, ctx, W, b, a, e, world, local):
             "note": f"pinned host ring of {ring} rows x {F + 1} columns, {n_calls} calls per step"}
 
 
+def e2e_device_measure(args, eng):
+    """The metric end to end with A kept where the solve consumes it (device memory): every step
+    copies this rank's inputs (points, coefficient fields, rhs values) from pinned host memory,
+    runs the bench's call (fls_features_assemble) into the device [A | b], and reads the step's
+    rhs column back to pinned host memory (the device-resident workflow: assemble, then solve
+    on the GPU).  Reported beside `e2e` (every entry to the host), not instead of it."""
+    import torch
+    import torch.distributed as dist
+    from paper_2602_10541_b200 import fls
+
+    p, a, e = eng.p, eng.a, eng.e
+    F, d, n_local, lda = p.n_features, p.dim, eng.n_local, eng.lda
+    pairs, blocks, h2d = [], [], 0
+    for blk, o in zip(p.blocks, p.block_offsets()):
+        lo, hi = max(a, o), min(e, o + blk.n)
+        if hi <= lo:
+            continue
+        sl = slice(lo - o, hi - o)
+        hx = torch.from_numpy(np.ascontiguousarray(blk.X[sl])).pin_memory()
+        hv = torch.from_numpy(np.ascontiguousarray(blk.values[sl])).pin_memory()
+        hf = (torch.from_numpy(np.ascontiguousarray(blk.fields[sl])).pin_memory()
+              if blk.fields is not None else None)
+        dx, dv = torch.empty_like(hx, device="cuda"), torch.empty_like(hv, device="cuda")
+        df = torch.empty_like(hf, device="cuda") if hf is not None else None
+        pairs += [(dx, hx), (dv, hv)] + ([(df, hf)] if hf is not None else [])
+        h2d += 8 * (hx.numel() + hv.numel() + (hf.numel() if hf is not None else 0))
+        blocks.append(fls.Block(dx, blk.terms, blk.weight, dv, df))
+    bset = fls.BlockSet(blocks, d)
+    rhs_h = torch.empty((n_local,), dtype=torch.float64).pin_memory()
+    rhs_d = eng.Ab[F * lda: F * lda + n_local]
+
+    def step():
+        for dv_, hv_ in pairs:
+            dv_.copy_(hv_, non_blocking=True)
+        fls.fls_features_assemble(eng.ctx, d, F, p.sigma, p.seed, bset, W=eng.W, b=eng.b, A=eng.Ab,
+                                  lda=lda)
+        rhs_h.copy_(rhs_d, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(max(2, args.e2e_steps)):
+        if dist.is_initialized():
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step()
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    t = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=_cdev())
+    if dist.is_initialized():
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    s_step = float(t.item())
+    return {"value": p.n_rows * F / s_step, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": 8 * n_local, "s_per_step": s_step, "steps": len(times),
+            "api": "fls_features_assemble (device [A | b]; inputs H2D, rhs D2H every step)"}
+
+
 def solve_measure(args, world, rank, local):
     """End-to-end solve (BASELINE metric "end-to-end solve ms"), per phase, Algorithm 1 lines
     1-6: features + assembly + least squares (QR; TSQR over the ranks) + eval at 10,000
@@ -649,6 +707,8 @@ class FlsEngine:
         end-to-end solve, per-config numbers and the CPU oracle (rank 0, N = 1)"""
         torch = self.torch
         out = {}
+        if not args.no_e2e:
+            out["e2e_device_resident"] = e2e_device_measure(args, self)
         del self.Ab
         torch.cuda.empty_cache()
         if not args.no_e2e:
