@@ -918,3 +918,52 @@ def test_back_to_back_calls_with_pdl_overlap_keep_stream_order(ctx):
         assert torch.equal(W, refs[last][0]) and torch.equal(b, refs[last][1])
         V, Vr = A.view(F + 1, lda)[:, :R], refs[last][2].view(F + 1, lda)[:, :R]
         assert torch.equal(V, Vr), n
+
+
+def test_maximum_operator_sizes(ctx):
+    """the limits of the ABI at once: d = 8 (FLS_MAX_DIM), 64 terms (FLS_MAX_TERMS), 4 coefficient
+    fields (FLS_MAX_FIELDS), and terms of order > 22 whose monomial the fold multiplies out
+    axis by axis instead of from the host-expanded factor list -- vs the oracle, both folds
+    (constant coefficients and per-field)"""
+    g = np.random.default_rng(11)
+    d, n_fields = 8, 4
+    terms = []
+    for t in range(64):
+        alpha = [0] * d
+        if t == 0:
+            alpha = [3, 3, 3, 3, 3, 3, 3, 3]          # order 24 > kMaxFac
+        elif t == 1:
+            alpha = [0, 0, 0, 0, 0, 0, 0, 26]          # order 26 on one axis
+        else:
+            for _ in range(int(g.integers(0, 5))):
+                alpha[int(g.integers(0, d))] += 1
+        field = int(g.integers(-1, n_fields)) if t > 1 else -1
+        terms.append((tuple(alpha), float(g.normal()), field))
+    fields = g.uniform(0.5, 1.5, (501, n_fields))
+    g2 = np.random.default_rng(12)
+    W = g2.normal(0, 0.9, (97, d))                     # |W| < ~3: |W|^26 stays finite
+    b = g2.uniform(0, 2 * math.pi, 97)
+    X = g2.random((501, d)) * 0.5
+
+    class B:
+        pass
+    h = B()
+    h.X, h.terms, h.weight, h.values, h.fields = X, terms, 2.0, g2.normal(size=501), fields
+    dv = fls.Block(torch.from_numpy(X).cuda(), terms, 2.0, torch.from_numpy(h.values).cuda(),
+                   torch.from_numpy(fields).cuda())
+    Ab, lda = fls.fls_assemble(ctx, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(), [dv])
+    fls.fls_sync(ctx)
+    Ao, ro, S = oracle.assemble(W, b, [h])
+    Ag, rg = rows_from_colmajor(Ab, lda, 97, np.arange(501))
+    emax, _ = scaled_err(Ag, Ao, S)
+    assert emax <= ENTRY_TOL, emax
+    assert np.array_equal(rg, ro)
+    # the same operator with constant coefficients only (amplitude/phase fold path)
+    const = [(a, c, -1) for a, c, _ in terms]
+    h.terms, h.fields = const, None
+    dv = fls.Block(torch.from_numpy(X).cuda(), const, 2.0, torch.from_numpy(h.values).cuda())
+    Ab, lda = fls.fls_assemble(ctx, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(), [dv])
+    fls.fls_sync(ctx)
+    Ao, ro, S = oracle.assemble(W, b, [h])
+    Ag, rg = rows_from_colmajor(Ab, lda, 97, np.arange(501))
+    assert scaled_err(Ag, Ao, S)[0] <= ENTRY_TOL
