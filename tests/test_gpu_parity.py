@@ -281,6 +281,41 @@ def test_no_out_of_bounds_writes(ctx, d, G, mixed):
         assert not torch.isnan(V[:, :m]).any()
 
 
+@pytest.mark.parametrize("fuse", ["0", "1000000000000"])
+@pytest.mark.parametrize("d,G", [(1, 0), (3, 1), (5, 0), (8, 1)])
+def test_no_out_of_bounds_writes_features_assemble(ctx, d, G, fuse, monkeypatch):
+    """the same sentinel guard for fls_features_assemble, whose draws write W and b too -- the
+    two-launch path (feature / prefactor kernel under PDL, then the assembly) and the ONE-launch
+    path (the assembly CTAs draw, fold and write W, b themselves)"""
+    monkeypatch.setenv("FLS_FUSE_MAX_ENTRIES", fuse)
+    g = np.random.default_rng(d * 10 + G + 7)
+    F, n = 261, 2051
+    X = torch.from_numpy(g.random((n, d))).cuda()
+    fields = torch.from_numpy(g.normal(size=(n, max(G, 1)))).cuda() if G else None
+    terms = [(tuple([2 if k == 0 else 0 for k in range(d)]), -1.0, -1)]
+    for q in range(G):
+        terms.append((tuple([0] * d), 1.0 + q, q))
+    blk = [fls.Block(X, terms, 1.0, torch.ones(n, dtype=torch.float64, device="cuda"), fields)]
+    guard = 4096
+    for (r0, r1) in [(0, n), (1, n - 3), (513, 1500)]:
+        m = r1 - r0
+        lda = m + 5
+        buf = torch.full((guard + (F + 1) * lda + guard,), float("nan"), dtype=torch.float64,
+                         device="cuda")
+        wbuf = torch.full((guard + F * d + guard,), float("nan"), dtype=torch.float64, device="cuda")
+        bbuf = torch.full((guard + F + guard,), float("nan"), dtype=torch.float64, device="cuda")
+        A, W, b = buf[guard: -guard], wbuf[guard: -guard].view(F, d), bbuf[guard: -guard]
+        fls.fls_features_assemble(ctx, d, F, 2.0, 5, blk, W=W, b=b, row_begin=r0, row_end=r1, A=A,
+                                  lda=lda)
+        fls.fls_sync(ctx)
+        for bb in (buf, wbuf, bbuf):
+            assert torch.isnan(bb[:guard]).all() and torch.isnan(bb[-guard:]).all()
+        assert not torch.isnan(W).any() and not torch.isnan(b).any()
+        V = A.view(F + 1, lda)
+        assert torch.isnan(V[:, m:]).all()
+        assert not torch.isnan(V[:, :m]).any()
+
+
 def test_mode_cos_only_shift(ctx):
     _mode_case(ctx, wl.op_advection([0.5, -1.0, 2.0]))               # all odd orders
 
