@@ -42,7 +42,7 @@ def main():
                         torch.from_numpy(blk.values).cuda()) for blk in p.blocks]
     Wd, bd = torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda()
     newton.solve_nonlinear(ctx, Wd, bd, blocks[0], blocks[1:], *p.nl, max_iter=2, tol=0.0)
-    for nm in ["fls_eval", "fls_nl_residual", "fls_assemble", "fls_solve", "fls_axpy"]:
+    for nm in ["fls_eval", "fls_nl_residual", "fls_assemble", "fls_solve_mu", "fls_axpy"]:
         setattr(newton.fls, nm, wrap(nm, getattr(fls, nm)))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
