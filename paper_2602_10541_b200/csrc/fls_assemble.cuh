@@ -270,16 +270,19 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
   const int nfe0 = (f1 - f0) < kFC ? (int)(f1 - f0) : kFC;
   // the first chunk's records before the wait: with programmatic dependent launch they are
   // drawn while the previous kernel on the stream still runs
-  if (kFused && f0 < f1) fused_chunk(f0, nfe0, false);
-  // no global memory is read or written above this line: the kernel may run ahead of its
-  // predecessor (PDL), which may still be producing X / fields / values or reading A, W, b
-  pdl_wait();
+  if constexpr (kFused) {
+    if (f0 < f1) fused_chunk(f0, nfe0, false);
+    // the fused kernel runs ahead of an ARBITRARY predecessor (PDL), which may still be producing
+    // X / fields / values or reading A, W, b: no global memory is touched above this line
+    pdl_wait();
+  }
 
   // local rows (A-relative) of this thread: rbase + p*2*kNT + {0, 1}; rbase is even.
   // The block's points map to local rows [lr0, lr1): point i = pt0 + (r - lr0).
   const int64_t rbase = (a.lr0 & ~int64_t(kRowAlign - 1)) + tile * kRowsCTA + kRowAlign * threadIdx.x;
   double x[NQ][D];
   double c[NQ][GG];
+  double rv[NQ];
   bool in[NQ];
   bool bad = false;
   bool full = a.vec;
@@ -299,10 +302,22 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
       c[q][g] = (G > 0 && in[q]) ? __ldg(a.fields + i * a.nf + a.gfield[g]) : 0.0;
       bad |= !finite(c[q][g]);
     }
+    rv[q] = 0.0;
     if (group == 0 && a.rhs != nullptr && in[q]) {
       const double v = a.values ? __ldg(a.values + i) : 0.0;
       bad |= !finite(v);
-      a.rhs[r] = a.weight * v;
+      rv[q] = a.weight * v;
+    }
+  }
+  // the two-launch path: this grid is launched (PDL) once the prefactor kernel before it has
+  // triggered, which it does only after everything ahead of it on the stream completed -- so
+  // the points above were safe to read; the records it writes are safe to read from here on
+  if constexpr (!kFused) pdl_wait();
+  if (group == 0 && a.rhs != nullptr) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int64_t r = kQuad ? rbase + q : rbase + (q >> 1) * (2 * kNT) + (q & 1);
+      if (in[q]) a.rhs[r] = rv[q];
     }
   }
   if (bad) atomicOr(a.err, kErrNonFinite);

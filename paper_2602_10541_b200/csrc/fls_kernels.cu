@@ -129,8 +129,9 @@ __device__ void prefactor_one(const PrefArgs &a, int64_t j) {
 // is computed in shared memory FIRST and written to W, b and the record arrays only after
 // griddepcontrol.wait: launched with programmatic dependent launch behind the previous call's
 // assembly (which triggers at its start), the draws and folds of step k+1 overlap the tail of
-// step k's assembly, and nothing the running kernel reads is overwritten early.  Without the
-// PDL attribute the wait is a no-op.
+// step k's assembly, and nothing the running kernel reads is overwritten early.  It triggers its
+// own dependents (the assembly) only after that wait.  Without the PDL attribute the wait is a
+// no-op.
 constexpr int kFpFeat = 64;
 constexpr int kSrec = pf_stride(FLS_MAX_DIM, FLS_MAX_FIELDS, KM_SINCOS);
 __global__ void __launch_bounds__(kFpFeat * (FLS_MAX_DIM + 1))
@@ -139,7 +140,6 @@ features_prefactor_kernel(int32_t D, int64_t F, const FeatBlocks fb, uint64_t se
   __shared__ double ws[kFpFeat * FLS_MAX_DIM];
   __shared__ double bs[kFpFeat];
   extern __shared__ double sr[];  // records: [block q][feature tj][smax]
-  pdl_trigger();
   const int64_t j0 = (int64_t)blockIdx.x * kFpFeat;
   const int nf = (int)((F - j0) < kFpFeat ? (F - j0) : kFpFeat);
   const int t = threadIdx.x;
@@ -159,6 +159,9 @@ features_prefactor_kernel(int32_t D, int64_t F, const FeatBlocks fb, uint64_t se
   }
   __syncthreads();
   pdl_wait();  // the previous kernel on the stream is complete (and its memory visible) here
+  // trigger only now: the assembly that follows may then read the caller's points before its
+  // own wait, since everything ahead of this kernel on the stream has completed
+  pdl_trigger();
   for (int i = t; i < nf * D; i += blockDim.x) W[j0 * D + i] = ws[i];
   for (int i = t; i < nf; i += blockDim.x) b[j0 + i] = bs[i];
   for (int q = 0; q < pb.n; ++q) {
