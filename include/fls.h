@@ -217,7 +217,11 @@ FLS_API fls_status fls_assemble(fls_ctx *ctx, const double *W, const double *b, 
 
 /* Alg. 1 lines 1 + 3-5 in one call: fls_features(ctx, dim, n_features, sigma, seed, W, b)
  * followed by fls_assemble(ctx, W, b, ...), with the feature draw and the per-block prefactor
- * fold fused into one kernel (saves a launch on latency-bound problems).  W and b are written
+ * fold fused into one kernel ahead of the assembly -- or, for column-major calls of at most
+ * FLS_FUSE_MAX_ENTRIES local entries (environment, default 2^22), into the assembly kernel
+ * itself (ONE launch: each CTA draws and folds its own features).  Consecutive calls on a
+ * stream overlap (programmatic dependent launch: the next call's draws run while this call's
+ * assembly finishes; every write still lands in stream order).  W and b are written
  * (bit-identical to fls_features) and must be device buffers of n_features x dim and
  * n_features.  Other arguments, errors and asynchrony as fls_assemble. */
 FLS_API fls_status fls_features_assemble(fls_ctx *ctx, int32_t dim, int64_t n_features,
