@@ -77,3 +77,17 @@ def test_adamw_trajectory_matches_oracle(ctx):
         s -= lr * (m / (1 - 0.9 ** t)) / (math.sqrt(v / (1 - 0.999 ** t)) + 1e-8)
     assert abs(Lg[0][0] - s) <= 1e-7 * s
     assert hist[-1]["loss"] < hist[0]["loss"]
+
+
+def test_bandwidth_gradient_with_ridge_matches_oracle(ctx):
+    """Tikhonov inner solve (sqrt_mu > 0): the ridge-augmented outer loss and its exact envelope
+    gradient (reading B2) vs the oracle, which is pinned to central FD of the same loss"""
+    p, W_hat, b = _setup()
+    L = [[3.0, 0.0], [0.7, 4.0]]
+    sq = 3e-2
+    loss_o, G_o, _ = ol.outer_grad(np.array(L), W_hat, b, p.blocks, sqrt_mu=sq)
+    loss, G, _ = outer_loss_and_grad(ctx, L, torch.from_numpy(W_hat).cuda(),
+                                     torch.from_numpy(b).cuda(), dev_blocks(p), sqrt_mu=sq)
+    G = np.array(G)
+    assert abs(loss - loss_o) <= 1e-8 * loss_o
+    assert np.abs(G - G_o).max() <= 1e-7 * np.abs(G_o).max(), (G, G_o)

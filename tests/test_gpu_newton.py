@@ -98,3 +98,49 @@ def test_udu_residual_kernel(ctx):
     assert np.allclose(neg.cpu().numpy(), ref, rtol=1e-14, atol=1e-14)
     assert np.allclose(dNu.cpu().numpy(), 0.7 * Du, rtol=1e-15, atol=0)
     assert np.allclose(dNd.cpu().numpy(), 0.7 * u, rtol=1e-15, atol=0)
+
+
+def test_newton_uses_the_bc_operator_in_residual_and_jacobian(ctx):
+    """a Robin boundary operator (u + 0.3 du/dx on the x-edges): with N = 0 the linear warm start
+    is already the Tikhonov least-squares solution, so Newton must stop there -- its residual is
+    evaluated with the same BC operator the Jacobian rows use (a residual taken with the identity
+    would move beta away).  Compared with one direct solve of the stacked system."""
+    import math
+    g = np.random.default_rng(3)
+    n, nb, F = 900, 120, 250
+    Xi_h = g.random((n, 2))
+    Xb_h = np.stack([np.repeat([0.0, 1.0], nb // 2), g.random(nb)], 1)
+    # manufactured u* = sin(x + 0.5) cos(y): -Lap u* = 2 u*, Robin data u* + 0.3 du*/dx
+    us = lambda X: np.sin(X[:, 0] + 0.5) * np.cos(X[:, 1])
+    usx = lambda X: np.cos(X[:, 0] + 0.5) * np.cos(X[:, 1])
+    Xi, Xb = torch.from_numpy(Xi_h).cuda(), torch.from_numpy(Xb_h).cuda()
+    f = torch.from_numpy(2.0 * us(Xi_h)).cuda()
+    gb = torch.from_numpy(us(Xb_h) + 0.3 * usx(Xb_h)).cuda()
+    lap = [((2, 0), -1.0, -1), ((0, 2), -1.0, -1)]
+    robin = [((0, 0), 1.0, -1), ((1, 0), 0.3, -1)]
+    # Dirichlet (identity) rows on the y-edges complete the boundary
+    Xd_h = np.stack([g.random(nb), np.repeat([0.0, 1.0], nb // 2)], 1)
+    Xd = torch.from_numpy(Xd_h).cuda()
+    pde = fls.Block(Xi, lap, 1.0, f)
+    bc = fls.Block(Xb, robin, 10.0, gb)
+    bcd = fls.Block(Xd, [((0, 0), 1.0, -1)], 10.0, torch.from_numpy(us(Xd_h)).cuda())
+    W, b = fls.fls_features(ctx, 2, F, 3.0, 0)
+    beta, hist = solve_nonlinear(ctx, W, b, pde, [bc, bcd], "poly", [0.0], mu=1e-10, max_iter=3)
+    R = n + 2 * nb
+    lda = fls.round_up(R + F, 4)
+    Ab = torch.empty(((F + 1) * lda,), dtype=torch.float64, device="cuda")
+    fls.fls_assemble(ctx, W, b, [pde, bc, bcd], A=Ab, lda=lda)
+    beta_d, res_d = fls.fls_solve_mu(ctx, Ab, R, lda, F, math.sqrt(1e-10))
+    Xt_h = g.random((2000, 2))
+    Xt = torch.from_numpy(Xt_h).cuda()
+    u = fls.fls_eval(ctx, W, b, beta, Xt).cpu().numpy()
+    u_d = fls.fls_eval(ctx, W, b, beta_d, Xt).cpu().numpy()
+    assert np.linalg.norm(u_d - us(Xt_h)) <= 1e-5 * np.linalg.norm(us(Xt_h))   # well posed
+    assert np.linalg.norm(u - u_d) <= 1e-6 * np.linalg.norm(u_d)    # an identity-BC residual moves it O(1)
+    # the residual Newton reports at its warm start (= beta_d) is ||A beta - b|| of the stacked
+    # system WITH the Robin rows -- A beta from fls_eval_block, i.e. the assembled operators
+    r2 = 0.0
+    for blk in (pde, bc, bcd):
+        Ab_ = fls.fls_eval_block(ctx, W, b, beta_d, blk).cpu().numpy()
+        r2 += float(np.sum((Ab_ - blk.weight * blk.values.cpu().numpy()) ** 2))
+    assert abs(hist[0]["resid"] - math.sqrt(r2)) <= 1e-6 * math.sqrt(r2)
