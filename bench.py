@@ -651,7 +651,9 @@ class FlsEngine:
                     fp64[f"peak_tops_{tag}"] = pk
                     fp64[f"frac_{tag}"] = ach / pk
         power = None
-        pm = os.path.join(ROOT, "profiles", "r01_power_model.json")
+        pm = os.path.join(ROOT, "profiles", "r02_power_model.json")
+        if not os.path.exists(pm):
+            pm = os.path.join(ROOT, "profiles", "r01_power_model.json")
         if os.path.exists(pm) and p.name == "c5_biharm3d":
             try:
                 m = json.load(open(pm))["model"]
@@ -671,7 +673,7 @@ class FlsEngine:
                          "sustained_reference": {
                              "frac": m.get("c5_assembly_frac_of_power_bound"),
                              "what": "the same kernel back to back for 4 s at 995 W of 1000 W"},
-                         "source": "profiles/r01_power_model.json (tools/power_model.py)"}
+                         "source": os.path.relpath(pm, ROOT) + " (tools/power_model.py)"}
             except Exception:
                 power = None
         tot_bytes = sum(r["bytes_per_step"] for r in per_rank)
