@@ -679,6 +679,28 @@ class FlsEngine:
                          "source": os.path.relpath(pm, ROOT) + " (tools/power_model.py)"}
             except Exception:
                 power = None
+        # north_star's roofline: "the slower of HBM bandwidth and the fp64 sincos issue rate".
+        # The FP64 side is the measured register-only rate of the C5 per-entry arithmetic
+        # (microbench entry kernel, no memory traffic) at full clock, scaled to the SM clock
+        # the timed region actually ran at (the board lowers it under sw_power_cap)
+        co_bound = None
+        if os.path.exists(pm) and p.name == "c5_biharm3d" and clocks.get("sm_mhz"):
+            try:
+                mm = json.load(open(pm))
+                alu_full, mhz_full = mm["c5_alu"]["entries_per_s"], mm["c5_alu"]["clocks"]["sm_mhz"]
+                alu_now = alu_full * clocks["sm_mhz"] / mhz_full
+                n_ent = mine["bytes_per_step"] / 8.0
+                t_hbm = mine["bytes_per_step"] / (hbm_peak * 1e9) * 1e3
+                t_fp64 = n_ent / alu_now * 1e3
+                t_kern = mine["kernel_ms_per_step"]
+                co_bound = {"bound": "fp64" if t_fp64 > t_hbm else "hbm",
+                            "t_hbm_ms": t_hbm, "t_fp64_ms_at_median_clock": t_fp64,
+                            "kernel_ms": t_kern, "frac": max(t_hbm, t_fp64) / t_kern,
+                            "fp64_entries_per_s_full_clock": alu_full,
+                            "median_sm_mhz": clocks["sm_mhz"],
+                            "source": os.path.relpath(pm, ROOT) + " (c5_alu)"}
+            except Exception:
+                co_bound = None
         tot_bytes = sum(r["bytes_per_step"] for r in per_rank)
         slowest = max(r["kernel_ms_per_step"] for r in per_rank)
         agg = tot_bytes / (slowest / 1e3) / 1e9
@@ -696,6 +718,7 @@ class FlsEngine:
                          "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
                          "kernel": "assemble_rm_kernel" if self.row_major else "assemble_cm_kernel",
                          "kernel_ms_avg": mine["kernel_ms_avg"], "fp64_pipe": fp64, "power": power,
+                         "co_bound": co_bound,
                          "scope": "rank 0's GPU (per-GPU kernel roofline)",
                          "per_rank": [{"rank": i, "achieved": r["achieved"],
                                        "frac": r["achieved"] / hbm_peak} for i, r in enumerate(per_rank)],
