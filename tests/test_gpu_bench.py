@@ -26,7 +26,8 @@ def test_bench_line_contract_small():
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    j = _run("--workload", "c3_poisson5d", "--e2e-steps", "1", "--e2e-ring-rows", "8192")
+    j = _run("--workload", "c3_poisson5d", "--e2e-steps", "1", "--e2e-ring-rows", "8192",
+             "--per-config-budget", "3")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
               "roofline", "gpu_launches", "clocks", "e2e", "solve"):
@@ -40,6 +41,13 @@ def test_bench_line_contract_small():
     assert j["e2e"]["value"] > 0 and j["e2e"]["d2h_bytes_per_step"] > 0
     assert j["solve"]["ms"] > 0
     assert "sm_mhz" in j["clocks"] and "reasons" in j["clocks"]
+    assert j["e2e_device_resident"]["value"] > 0 and j["e2e_device_resident"]["h2d_bytes_per_step"] > 0
+    pc = j["per_config"]                       # bounded: later configs may be skipped
+    assert set(pc) == {"c1_poisson1d", "c2_poisson2d", "c3_poisson5d", "c4_heat2d", "c5_biharm3d"}
+    c1 = pc["c1_poisson1d"]
+    assert c1["graph_us_per_step"] > 0 and 0 < c1["frac_of_copy_peak"] < 1.5
+    assert c1["solve_ms"]["ms"] > 0 and c1["rel_l2_vs_u_star"] < 1e-6
+    assert all(("skipped" in v) or v["graph_us_per_step"] > 0 for v in pc.values())
 
 
 def test_cli_solves_a_config():
