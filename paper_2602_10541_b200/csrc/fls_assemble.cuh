@@ -25,6 +25,9 @@
 #include "fls_feat.cuh"
 #include "fls_internal.h"
 
+#ifndef FLS_FLIP_OUTPUT
+#define FLS_FLIP_OUTPUT 0
+#endif
 #ifndef FLS_MINB
 #define FLS_MINB 4   // 4 CTAs x 256 threads per SM -> <= 64 registers
 #endif
@@ -60,7 +63,14 @@ struct EntryMath {
       double P = rec[D + 1];
 #pragma unroll
       for (int g = 0; g < G; ++g) P = fma(c[g], rec[D + 2 + g], P);
+      // (-1)^n on the argument, after u = f^2 is formed: sin is odd, so P sin(pi (-1)^n f) is
+      // bit-identical to (-1)^n P sin(pi f), and the XOR then rewrites f's high word in place
+      // (the result's register pair feeds the 16-byte store without a move)
+#if FLS_FLIP_OUTPUT  // A/B build: the round-1 form (sign applied to the product)
       return flipsign(P * sinpi_core(f, u), sgn);
+#else
+      return P * sinpi_core(flipsign(f, sgn), u);
+#endif
     } else {
       double Ps = rec[D + 1], Pc = rec[D + 2];
 #pragma unroll
