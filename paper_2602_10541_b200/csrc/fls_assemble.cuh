@@ -25,6 +25,9 @@
 #include "fls_feat.cuh"
 #include "fls_internal.h"
 
+#ifndef FLS_WIDE_C5
+#define FLS_WIDE_C5 1  // 0: the C5 class keeps the default 2 features / 4 CTAs (A/B builds)
+#endif
 #ifndef FLS_FLIP_OUTPUT
 #define FLS_FLIP_OUTPUT 0
 #endif
@@ -86,8 +89,23 @@ struct EntryMath {
 // resident CTAs per SM the register budget is sized for (checked against ptxas -v spills):
 // sin-only with G <= 1, D + G <= 4 fits 64 registers (4 CTAs: C1, C2, C4, C5), D + G <= 5
 // fits 80 (3 CTAs: C3); wider ones get 128 (2 CTAs) or 255 (1 CTA)
+// the C5 class (d = 3, one coefficient field, sin family): 4 features per loop iteration at 80
+// registers / 3 CTAs per SM (no spills; the 64-register default spilled 20 B) -- interleaved
+// sustained 200-step A/B, 3 rounds on one box (tools/ab_variants.sh base narrow):
+// 7.020-7.033e11 vs 6.961-6.962e11 entries/s (+0.9%); the same change costs C3 (d = 5) 17%
+// and C2 6%, so it is limited to this class
+template <int D, int G, int KM>
+__host__ __device__ constexpr bool asm_wide_unroll() {
+  return FLS_WIDE_C5 && FLS_FUNROLL == 2 && FLS_MINB == 4 && KM == KM_SIN && G == 1 && D == 3;
+}
+template <int D, int G, int KM>
+__host__ __device__ constexpr int asm_funroll() {
+  return asm_wide_unroll<D, G, KM>() ? 4 : kFUnroll;
+}
+
 template <int D, int G, int KM>
 constexpr int asm_min_blocks() {
+  if (asm_wide_unroll<D, G, KM>()) return 3;
   if (KM != KM_SIN) return D + G >= 9 ? 1 : 2;
   if (G <= 1 && D + G <= 4) return FLS_MINB;
   if (D + G <= 5) return FLS_MINB5;
@@ -367,17 +385,18 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
     double *colp = a.A + j0 * a.lda + rbase;
     if (full) {
       int jj = 0;
-      for (; jj + kFUnroll <= nfe; jj += kFUnroll, colp += kFUnroll * a.lda) {
-        double o[kFUnroll][NQ];
+      constexpr int FU = asm_funroll<D, G, KM>();
+      for (; jj + FU <= nfe; jj += FU, colp += FU * a.lda) {
+        double o[FU][NQ];
 #pragma unroll
-        for (int u = 0; u < kFUnroll; ++u) {
+        for (int u = 0; u < FU; ++u) {
           double rec[S];
           M::record(sp + (jj + u) * S, rec);
 #pragma unroll
           for (int q = 0; q < NQ; ++q) o[u][q] = M::entry(rec, x[q], c[q]);
         }
 #pragma unroll
-        for (int u = 0; u < kFUnroll; ++u) store_full(colp + u * a.lda, o[u]);
+        for (int u = 0; u < FU; ++u) store_full(colp + u * a.lda, o[u]);
       }
       for (; jj < nfe; ++jj, colp += a.lda) {
         double rec[S];
