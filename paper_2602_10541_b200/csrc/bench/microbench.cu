@@ -5,7 +5,8 @@
 //                   (16-byte st.global.cs, 512 contiguous bytes per warp instruction)
 //   mb_dfma_rate    register-only DFMA throughput (8 independent chains per thread)
 //   mb_entry_rate   register-only throughput of the assembly kernel's per-entry arithmetic
-//                   (d = 3 phase, half-turn reduction, degree-13 sin, one coefficient field)
+//                   (d = 3 phase, half-turn reduction, degree-13 sin, one coefficient field),
+//                   with the C5-class kernel's ILP (4 rows x 4 features per iteration)
 //                   = the FP64-pipe ceiling of the C5 kernel with no memory traffic at all
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -38,29 +39,36 @@ __global__ void __launch_bounds__(256) dfma_kernel(double *out, int iters, doubl
   if (s == 12345.678) out[threadIdx.x] = s;  // never true; keeps the chains alive
 }
 
-// per thread: 4 rows in registers (as the assembly kernel), loop over `nfeat` synthetic
-// features; accumulate instead of storing
-__global__ void __launch_bounds__(256) entry_kernel(double *out, int nfeat, double w0, double w1,
-                                                    double w2) {
+// per thread: 4 rows in registers and 4 features per iteration (as the C5-class assembly
+// kernel: 16 independent entries in flight), the entry arithmetic exactly as EntryMath (phase,
+// half-turn reduction, (-1)^n on the argument, degree-13 sin, one coefficient field); each
+// result is folded into an integer XOR (one LOP3, standing in for the kernel's store) so no
+// floating-point dependency links the entries
+__global__ void __launch_bounds__(256, 3) entry_kernel(double *out, int nfeat, double w0, double w1,
+                                                       double w2) {
   const double x[4][3] = {{0.1 + threadIdx.x * 1e-4, 0.2, 0.3}, {0.4, 0.5 + blockIdx.x * 1e-6, 0.6},
                           {0.7, 0.8, 0.9}, {0.15, 0.25, 0.35}};
   const double c[4] = {1.1, 1.2, 1.3, 1.4};
-  double acc[4] = {0, 0, 0, 0};
+  int bits = 0;
   double wa = w0, wb = w1, wc = w2, bp = 0.1, P0 = 2.0, P1 = 3.0;
-  for (int j = 0; j < nfeat; ++j) {
+  for (int j = 0; j < nfeat; j += 4) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      double h = fma(wc, x[q][2], fma(wb, x[q][1], fma(wa, x[q][0], bp)));
-      int sgn;
-      const double f = halfturn(h, sgn);
-      const double P = fma(c[q], P1, P0);
-      acc[q] += P * sinpi_core(flipsign(f, sgn), f * f);
+    for (int u = 0; u < 4; ++u) {
+      const double wau = wa + 1e-3 * u, bpu = bp + 2e-3 * u;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double h = fma(wc, x[q][2], fma(wb, x[q][1], fma(wau, x[q][0], bpu)));
+        int sgn;
+        const double f = halfturn(h, sgn);
+        const double u2 = f * f;
+        const double P = fma(c[q], P1, P0);
+        bits ^= __double2hiint(P * sinpi_core(flipsign(f, sgn), u2));
+      }
     }
-    wa += 1e-3;  // integer-free per-feature change (models the smem record load)
-    bp += 2e-3;
+    wa += 4e-3;  // per-iteration change (the kernel's smem record loads)
+    bp += 8e-3;
   }
-  const double s = acc[0] + acc[1] + acc[2] + acc[3];
-  if (s == 12345.678) out[threadIdx.x] = s;
+  if (bits == 0x12345678) out[threadIdx.x] = bits;
 }
 
 // the assembly kernel's exact tile/store pattern with no arithmetic: 1024-row x 128-column
