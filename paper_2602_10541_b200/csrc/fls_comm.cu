@@ -214,8 +214,9 @@ fls_status tsqr_p2p(fls_ctx *ctx, const Plan &pl, double *Ab, int64_t lda, fls_s
       if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
       cudaIpcMemHandle_t h;
       if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, S);
-      // test hook: FLS_TEST_NO_IPC=1 makes the export fail (e.g. a VMM allocator) so the
-      // fallback paths run on a machine where IPC works
+      // test hook: FLS_TEST_NO_IPC=1 makes the export fail (e.g. a VMM allocator), =2 makes
+      // the other ranks' mapping fail (no peer access), so the fallback paths run on a machine
+      // where IPC works
       const char *no_ipc = getenv("FLS_TEST_NO_IPC");
       if (e == cudaSuccess && no_ipc && *no_ipc == '1') e = cudaErrorNotSupported;
       if (e != cudaSuccess) {
@@ -244,7 +245,9 @@ fls_status tsqr_p2p(fls_ctx *ctx, const Plan &pl, double *Ab, int64_t lda, fls_s
     cudaIpcMemHandle_t h;
     std::memcpy(&h, hs[pl.root].h, sizeof h);
     void *p = nullptr;
-    if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    const char *no_ipc = getenv("FLS_TEST_NO_IPC");
+    if ((no_ipc && *no_ipc == '2') ||
+        cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
       cudaGetLastError();
       ipc_ok = 0;
     } else {

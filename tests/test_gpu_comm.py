@@ -267,8 +267,12 @@ def test_pending_error_on_one_rank_is_returned_on_every_rank():
     assert out[1][1] == "FLS_ENONFINITE" and out[0][1] == "FLS_ENONFINITE"
 
 
-def test_p2p_unavailable_without_nccl_errors_on_every_rank():
-    out = _run("c1_poisson1d", 2, {"FLS_TEST_NO_IPC": "1"})
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_p2p_unavailable_without_nccl_errors_on_every_rank(mode):
+    """the root cannot export its stack (mode 1, e.g. a VMM allocator) or a peer cannot map it
+    (mode 2, e.g. no peer access): with a host control plane there is no NCCL to fall back to,
+    so every rank returns FLS_EUNSUPPORTED -- none is left waiting"""
+    out = _run("c1_poisson1d", 2, {"FLS_TEST_NO_IPC": mode})
     assert out[0][1] == out[1][1] == "FLS_EUNSUPPORTED"
 
 
