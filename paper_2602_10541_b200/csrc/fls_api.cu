@@ -544,6 +544,7 @@ fls_status fls_features_assemble(fls_ctx *ctx, int32_t dim, int64_t n_features, 
                                  const fls_block *blocks, int32_t n_blocks, int64_t row_begin,
                                  int64_t row_end, double *A, int64_t lda, int32_t layout,
                                  double *rhs) {
+  NvtxRange nvtx_("fls_features_assemble");
   if (fls_status s = check_ctx(ctx)) return s;
   if (!(sigma > 0.0) || !std::isfinite(sigma)) return fail(FLS_EINVAL, "sigma must be > 0 and finite");
   static thread_local AsmPlan ap;
@@ -618,6 +619,7 @@ fls_status fls_assemble(fls_ctx *ctx, const double *W, const double *b, int32_t 
                         int64_t n_features, int32_t normalize, const fls_block *blocks,
                         int32_t n_blocks, int64_t row_begin, int64_t row_end, double *A,
                         int64_t lda, int32_t layout, double *rhs) {
+  NvtxRange nvtx_("fls_assemble");
   if (fls_status s = check_ctx(ctx)) return s;
   static thread_local AsmPlan ap;
   if (fls_status s = validate_assemble(dim, n_features, W, b, blocks, n_blocks, row_begin, row_end,
@@ -636,6 +638,7 @@ fls_status fls_assemble_host(fls_ctx *ctx, const double *W, const double *b, int
                              int64_t n_features, int32_t normalize, const fls_block *blocks,
                              int32_t n_blocks, int64_t row_begin, int64_t row_end, double *A,
                              int64_t lda, double *rhs, int64_t chunk_rows) {
+  NvtxRange nvtx_("fls_assemble_host");
   if (fls_status s = check_ctx(ctx)) return s;
   static thread_local AsmPlan ap;
   if (fls_status s = validate_assemble(dim, n_features, W, b, blocks, n_blocks, row_begin, row_end,
@@ -921,6 +924,7 @@ extern "C" {
 
 fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int64_t n_features,
                      double ridge_rel, double *beta, double *resid_norm) {
+  NvtxRange nvtx_("fls_solve");
   if (fls_status s = check_ctx(ctx)) return s;
   if (!Ab || !beta) return fail(FLS_EINVAL, "Ab or beta is NULL");
   if (n_features < 1) return fail(FLS_EINVAL, "n_features < 1");
@@ -948,6 +952,7 @@ fls_status fls_solve(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int6
 
 fls_status fls_solve_mu(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, int64_t n_features,
                         double sqrt_mu, double *beta, double *resid_norm) {
+  NvtxRange nvtx_("fls_solve_mu");
   if (fls_status s = check_ctx(ctx)) return s;
   if (!Ab || !beta) return fail(FLS_EINVAL, "Ab or beta is NULL");
   if (n_features < 1) return fail(FLS_EINVAL, "n_features < 1");
@@ -966,6 +971,7 @@ fls_status fls_solve_mu(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_t lda, i
 fls_status fls_solve_stacked(fls_ctx *ctx, const double *S, int32_t n_blocks, int64_t kb,
                              int64_t lds, int64_t n_features, double sqrt_mu, double *beta,
                              double *resid_norm) {
+  NvtxRange nvtx_("fls_solve_stacked");
   if (fls_status s = check_ctx(ctx)) return s;
   if (!S || !beta) return fail(FLS_EINVAL, "S or beta is NULL");
   if (n_features < 1 || n_blocks < 1 || kb < 1) return fail(FLS_EINVAL, "bad sizes");
@@ -991,6 +997,7 @@ extern "C" {
 
 fls_status fls_qr_factor(fls_ctx *ctx, const double *A, int64_t n_rows, int64_t lda,
                          int64_t n_features, double sqrt_mu, fls_qr **out) {
+  NvtxRange nvtx_("fls_qr_factor");
   if (fls_status s = check_ctx(ctx)) return s;
   if (!A || !out) return fail(FLS_EINVAL, "A or out is NULL");
   *out = nullptr;
@@ -1047,6 +1054,7 @@ fls_status fls_qr_factor(fls_ctx *ctx, const double *A, int64_t n_rows, int64_t 
 
 fls_status fls_qr_solve(fls_ctx *ctx, const fls_qr *q, const double *B, int64_t ldb, int64_t nrhs,
                         double *Beta, int64_t ldbeta) {
+  NvtxRange nvtx_("fls_qr_solve");
   if (fls_status s = check_ctx(ctx)) return s;
   if (!q || !B || !Beta) return fail(FLS_EINVAL, "qr, B or Beta is NULL");
   if (nrhs < 1 || ldb < q->m_rows || ldbeta < q->n) return fail(FLS_EINVAL, "bad sizes");
@@ -1094,6 +1102,7 @@ fls_status fls_qr_destroy(fls_qr *q) {
 
 fls_status fls_geqrf(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda, int64_t n_cols,
                      double *tau) {
+  NvtxRange nvtx_("fls_geqrf");
   if (fls_status s = check_ctx(ctx)) return s;
   if (!M || !tau) return fail(FLS_EINVAL, "M or tau is NULL");
   if (n_rows < 1 || n_cols < 1 || lda < n_rows)
@@ -1154,6 +1163,7 @@ fls_status fls_ipc_close(fls_ctx *ctx, void *dev_ptr) {
 
 fls_status fls_qr_r(fls_ctx *ctx, double *M, int64_t n_rows, int64_t lda, int64_t n_cols,
                     double *R, int64_t ldr) {
+  NvtxRange nvtx_("fls_qr_r");
   if (fls_status s = check_ctx(ctx)) return s;
   if (!M || !R) return fail(FLS_EINVAL, "M or R is NULL");
   if (n_rows < 1 || n_cols < 1 || lda < n_rows)
@@ -1249,6 +1259,7 @@ fls_status fls_bandwidth_grad(fls_ctx *ctx, const double *W, const double *W_hat
                               int32_t dim, int64_t n_features, int32_t normalize,
                               const fls_block *blocks, int32_t n_blocks, const double *beta,
                               double *G) {
+  NvtxRange nvtx_("fls_bandwidth_grad");
   if (fls_status s = check_ctx(ctx)) return s;
   if (!W_hat || !beta || !G) return fail(FLS_EINVAL, "W_hat, beta or G is NULL");
   static thread_local AsmPlan ap;
@@ -1476,6 +1487,7 @@ static fls_status eval_common(fls_ctx *ctx, const double *W, const double *b, in
 fls_status fls_eval(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
                     int64_t n_features, int32_t normalize, const double *beta,
                     const fls_operator *op, const double *X, int64_t n_points, double *out) {
+  NvtxRange nvtx_("fls_eval");
   return eval_common(ctx, W, b, dim, n_features, normalize, beta, op, X, n_points, nullptr, 0, 1.0,
                      out, false);
 }
@@ -1483,6 +1495,7 @@ fls_status fls_eval(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
 fls_status fls_eval_block(fls_ctx *ctx, const double *W, const double *b, int32_t dim,
                           int64_t n_features, int32_t normalize, const double *beta,
                           const fls_block *block, double *out) {
+  NvtxRange nvtx_("fls_eval_block");
   if (!block) return fail(FLS_EINVAL, "block is NULL");
   if (!block->op) return fail(FLS_EINVAL, "block operator is NULL");
   if (block->n_fields < 0 || block->n_fields > 64) return fail(FLS_EINVAL, "n_fields out of range");

@@ -418,6 +418,7 @@ fls_status comm_solve(fls_ctx *ctx, double *Ab, int64_t n_local, int64_t lda, in
   *handled = false;
   if (!c || (c->nranks == 1 && !c->force_tsqr)) return FLS_OK;
   *handled = true;
+  NvtxRange nvtx_("fls_solve TSQR");
   const bool relative = sqrt_mu_abs < 0.0;
   Plan pl;
   pl.P = c->nranks;

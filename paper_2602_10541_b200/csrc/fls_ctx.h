@@ -4,6 +4,7 @@
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; ranges cost nothing unless a tool is attached
 
 #include <vector>
 
@@ -52,6 +53,14 @@ fls_status check_ctx(fls_ctx *ctx);
     cudaError_t e_ = (call);                                   \
     if (e_ != cudaSuccess) return ::fls::cuda_fail(e_, #call); \
   } while (0)
+
+// NVTX range for the duration of a libfls call (nsys / ncu --nvtx timelines)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 struct DeviceGuard {
   int prev = -1;
