@@ -34,6 +34,9 @@
 #ifndef FLS_FLIP_OUTPUT
 #define FLS_FLIP_OUTPUT 0
 #endif
+#ifndef FLS_XOR_SIGN
+#define FLS_XOR_SIGN FLS_FLIP_OUTPUT  // 1: the (-1)^n flip as shift + XOR (A/B builds)
+#endif
 #ifndef FLS_MINB
 #define FLS_MINB 4   // 4 CTAs x 256 threads per SM -> <= 64 registers
 #endif
@@ -62,8 +65,13 @@ struct EntryMath {
     double h = rec[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) h = fma(rec[k], x[k], h);
+#if FLS_XOR_SIGN  // A/B build: shift + XOR sign flip
     int sgn;
     const double f = halfturn(h, sgn);
+#else
+    int nlo;
+    const double f = halfturn_n(h, nlo);
+#endif
     const double u = f * f;
     if constexpr (KM == KM_SIN) {
       double P = rec[D + 1];
@@ -74,8 +82,10 @@ struct EntryMath {
       // (the result's register pair feeds the 16-byte store without a move)
 #if FLS_FLIP_OUTPUT  // A/B build: the round-1 form (sign applied to the product)
       return flipsign(P * sinpi_core(f, u), sgn);
-#else
+#elif FLS_XOR_SIGN
       return P * sinpi_core(flipsign(f, sgn), u);
+#else
+      return P * sinpi_core(addsign(f, nlo), u);
 #endif
     } else {
       double Ps = rec[D + 1], Pc = rec[D + 2];
@@ -84,7 +94,11 @@ struct EntryMath {
         Ps = fma(c[g], rec[D + 3 + 2 * g], Ps);
         Pc = fma(c[g], rec[D + 4 + 2 * g], Pc);
       }
+#if FLS_XOR_SIGN
       return flipsign(fma(Ps, sinpi_core(f, u), Pc * cospi_core(u)), sgn);
+#else
+      return addsign(fma(Ps, sinpi_core(f, u), Pc * cospi_core(u)), nlo);
+#endif
     }
   }
 };

@@ -76,6 +76,21 @@ __device__ __forceinline__ double flipsign(double x, int sgn) {
   return __hiloint2double(__double2hiint(x) ^ sgn, __double2loint(x));
 }
 
+// the same reduction returning n mod 2^32 (the low word of t) instead of the sign mask
+__device__ __forceinline__ double halfturn_n(double h, int &nlo) {
+  const double t = __dadd_rn(h, kMagic);
+  nlo = __double2loint(t);
+  const double n = __dsub_rn(t, kMagic);
+  return __dsub_rn(h, n);
+}
+
+// (-1)^n x: adding (n << 31) to the high word flips its sign bit exactly when n is odd (the
+// carry out of bit 31 is discarded), bit-identical to the XOR form, and the shift-and-add is a
+// single LEA where the XOR form needs a shift and a LOP3
+__device__ __forceinline__ double addsign(double x, int nlo) {
+  return __hiloint2double(__double2hiint(x) + (nlo << 31), __double2loint(x));
+}
+
 // sin(pi h) for any |h| < 2^51
 __device__ __forceinline__ double sin_halfturns(double h) {
   int sgn;
