@@ -34,6 +34,12 @@
 #ifndef FLS_FLIP_OUTPUT
 #define FLS_FLIP_OUTPUT 0
 #endif
+#ifndef FLS_HOIST
+#define FLS_HOIST 0
+#endif
+#ifndef FLS_C5_FU
+#define FLS_C5_FU 4
+#endif
 #ifndef FLS_XOR_SIGN
 #define FLS_XOR_SIGN FLS_FLIP_OUTPUT  // 1: the (-1)^n flip as shift + XOR (A/B builds)
 #endif
@@ -117,7 +123,7 @@ __host__ __device__ constexpr bool asm_wide_unroll() {
 }
 template <int D, int G, int KM>
 __host__ __device__ constexpr int asm_funroll() {
-  return asm_wide_unroll<D, G, KM>() ? 4 : kFUnroll;
+  return asm_wide_unroll<D, G, KM>() ? FLS_C5_FU : kFUnroll;
 }
 
 template <int D, int G, int KM>
@@ -410,17 +416,25 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
     if (full) {
       int jj = 0;
       constexpr int FU = asm_funroll<D, G, KM>();
+#if FLS_HOIST
+      const int64_t lda = a.lda;  // a is this block's entry of bt (dynamic index)
+      const double *rp = sp;
+      for (; jj + FU <= nfe; jj += FU, colp += FU * lda, rp += FU * S) {
+#else
+      const int64_t lda = a.lda;
       for (; jj + FU <= nfe; jj += FU, colp += FU * a.lda) {
+        const double *rp = sp + jj * S;
+#endif
         double o[FU][NQ];
 #pragma unroll
         for (int u = 0; u < FU; ++u) {
           double rec[S];
-          M::record(sp + (jj + u) * S, rec);
+          M::record(rp + u * S, rec);
 #pragma unroll
           for (int q = 0; q < NQ; ++q) o[u][q] = M::entry(rec, x[q], c[q]);
         }
 #pragma unroll
-        for (int u = 0; u < FU; ++u) store_full(colp + u * a.lda, o[u]);
+        for (int u = 0; u < FU; ++u) store_full(colp + u * lda, o[u]);
       }
       for (; jj < nfe; ++jj, colp += a.lda) {
         double rec[S];
