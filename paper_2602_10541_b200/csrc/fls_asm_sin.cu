@@ -11,17 +11,7 @@ static cudaError_t go_sin(AsmArgs *blks, int n, cudaStream_t st, bool pdl,
   // fused: the chunk's normals and biases follow the records in shared memory
   const size_t smem = (size_t)kFC * (S + (fz ? D + 1 : 0)) * sizeof(double);
   AsmBatch bt;
-  bt.n = n;
-  int64_t total = 0, span = 0;
-  for (int q = 0; q < n; ++q) span += blks[q].lr1 - (blks[q].lr0 & ~int64_t(kRowAlign - 1));
-  for (int q = 0; q < n; ++q) blks[q].batch_span = span;
-  for (int q = 0; q < n; ++q) {
-    const dim3 g = asm_grid<D, G, KM_SIN>(blks[q]);  // sets blks[q].fpc
-    bt.blk[q] = blks[q];
-    bt.rt[q] = g.x;
-    total += (int64_t)g.x * g.y;
-    bt.cta_end[q] = total;
-  }
+  const int64_t total = asm_plan<D, G, KM_SIN>(blks, n, bt);
   if (fz) {
     if constexpr (G <= 1) {
       auto kern = assemble_cm_kernel<D, G, KM_SIN, FusedBatch>;

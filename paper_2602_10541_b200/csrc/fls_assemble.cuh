@@ -34,6 +34,9 @@
 #ifndef FLS_FLIP_OUTPUT
 #define FLS_FLIP_OUTPUT 0
 #endif
+#ifndef FLS_STORE_POLICY
+#define FLS_STORE_POLICY 0  // full-tile stores: 0 streaming (.cs), 1 write-back, 2 .cg (A/B builds)
+#endif
 #ifndef FLS_HOIST
 #define FLS_HOIST 0
 #endif
@@ -194,6 +197,93 @@ inline dim3 asm_grid(AsmArgs &a) {
   return dim3((unsigned)rt, (unsigned)((a.F + a.fpc - 1) / a.fpc));
 }
 
+// Launch plan of a batch (one launch, n row blocks sharing the variant): each block's grid from
+// asm_grid, then -- for small launches (<= 2^25 entries, latency-bound: a thread's serial chain
+// of fpc features x its rows sets a CTA's time) -- a joint correction, because asm_grid sizes
+// each block against the whole wave on its own: C1's 2-row BC block got 63 CTAs of 8 features
+// while its 1,000-row PDE block ran 250 CTAs of 2, so the BC CTAs were the critical path.
+// FLS_BATCH_PLAN (A/B; tools/ab_small.sh, 10-step graphs, 3 interleaved rounds):
+//   1 (default) cap every block's features per CTA at the largest block's: C1 5.92 -> 4.92 us,
+//     C2 unchanged (its BC CTAs already carry fewer features than its PDE CTAs);
+//   0 per-block grids only;
+//   2 one feature count for all blocks, the smallest even one whose CTAs fit one wave: C1 4.92,
+//     C2 17.9 -> 19.7 us (C2's PDE CTAs grow from 14 to 18 features);
+//   3 equal entries per CTA, relaxed until the CTAs fit one wave: C2 20.5, C1 87 us (its 2-row
+//     BC CTAs get 424 features each).
+template <int D, int G, int KM>
+inline int64_t asm_plan(AsmArgs *blks, int n, AsmBatch &bt) {
+  static int strategy = -1;
+  if (strategy < 0) {
+    const char *e = getenv("FLS_BATCH_PLAN");
+    strategy = e ? atoi(e) : 1;
+  }
+  int64_t span = 0;
+  for (int q = 0; q < n; ++q) span += blks[q].lr1 - (blks[q].lr0 & ~int64_t(kRowAlign - 1));
+  dim3 g[kMaxBatch];
+  for (int q = 0; q < n; ++q) {
+    blks[q].batch_span = span;
+    g[q] = asm_grid<D, G, KM>(blks[q]);  // sets blks[q].fpc
+  }
+  const int64_t F = blks[0].F;
+  bool same_f = true;
+  for (int q = 1; q < n; ++q) same_f = same_f && blks[q].F == F;
+  if (n > 1 && strategy > 0 && same_f && F > 0 && span * F <= (int64_t(1) << 25) &&
+      !getenv("FLS_ASM_WAVES")) {
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+    const int64_t resident = (int64_t)sms * asm_min_blocks<D, G, KM>();
+    int64_t rt_sum = 0;
+    for (int q = 0; q < n; ++q) rt_sum += g[q].x;
+    auto even_up = [&](int64_t v) { v = v < 2 ? 2 : v; return (v + 1) & ~int64_t(1); };
+    int64_t fpc[kMaxBatch];
+    bool ok = false;
+    if (strategy == 1) {
+      int big = 0;
+      for (int q = 1; q < n; ++q)
+        if (blks[q].lr1 - blks[q].lr0 > blks[big].lr1 - blks[big].lr0) big = q;
+      for (int q = 0; q < n; ++q) fpc[q] = blks[q].fpc < blks[big].fpc ? blks[q].fpc : blks[big].fpc;
+      ok = true;
+    } else if (strategy == 2) {
+      for (int64_t f = 2; f <= even_up(F) && !ok; f += 2) {
+        if (rt_sum * ((F + f - 1) / f) <= resident) {
+          for (int q = 0; q < n; ++q) fpc[q] = f;
+          ok = true;
+        }
+      }
+    } else {
+      for (int64_t E = (span * F + resident - 1) / resident; !ok && E <= 2 * span * F; E += E / 32 + 1) {
+        int64_t total = 0;
+        for (int q = 0; q < n; ++q) {
+          const int64_t sq = blks[q].lr1 - (blks[q].lr0 & ~int64_t(kRowAlign - 1));
+          const int64_t rows = sq < kRowsCTA ? sq : kRowsCTA;
+          int64_t f = even_up((E + rows - 1) / rows);
+          if (f > even_up(F)) f = even_up(F);
+          fpc[q] = f;
+          total += (int64_t)g[q].x * ((F + f - 1) / f);
+        }
+        ok = total <= resident;
+      }
+    }
+    if (ok) {
+      for (int q = 0; q < n; ++q) {
+        blks[q].fpc = fpc[q];
+        g[q].y = (unsigned)((F + fpc[q] - 1) / fpc[q]);
+      }
+    }
+  }
+  bt.n = n;
+  int64_t total = 0;
+  for (int q = 0; q < n; ++q) {
+    bt.blk[q] = blks[q];
+    bt.rt[q] = g[q].x;
+    total += (int64_t)g[q].x * g[q].y;
+    bt.cta_end[q] = total;
+  }
+  return total;
+}
+
 // full-tile store of one feature column's entries of this thread: two 16-byte streaming stores
 // (row pairs 2*kNT apart) or, with kQuad, one 32-byte store of 4 consecutive rows
 template <int NQ>
@@ -211,8 +301,16 @@ __device__ __forceinline__ void store_full(double *colp, const double (&o)[NQ]) 
                  : "memory");
   } else {
 #pragma unroll
-    for (int pr = 0; pr < NQ / 2; ++pr)
-      __stcs(reinterpret_cast<double2 *>(colp + pr * (2 * kNT)), make_double2(o[2 * pr], o[2 * pr + 1]));
+    for (int pr = 0; pr < NQ / 2; ++pr) {
+      double2 *p = reinterpret_cast<double2 *>(colp + pr * (2 * kNT));
+#if FLS_STORE_POLICY == 1
+      *p = make_double2(o[2 * pr], o[2 * pr + 1]);
+#elif FLS_STORE_POLICY == 2
+      __stcg(p, make_double2(o[2 * pr], o[2 * pr + 1]));
+#else
+      __stcs(p, make_double2(o[2 * pr], o[2 * pr + 1]));
+#endif
+    }
   }
 }
 
