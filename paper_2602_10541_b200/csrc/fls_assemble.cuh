@@ -37,6 +37,9 @@
 #ifndef FLS_STORE_POLICY
 #define FLS_STORE_POLICY 0  // full-tile stores: 0 streaming (.cs), 1 write-back, 2 .cg (A/B builds)
 #endif
+#ifndef FLS_C2_FU1
+#define FLS_C2_FU1 1  // 0: the C2 class keeps 2 features per iteration (A/B builds)
+#endif
 #ifndef FLS_HOIST
 #define FLS_HOIST 0
 #endif
@@ -124,9 +127,16 @@ template <int D, int G, int KM>
 __host__ __device__ constexpr bool asm_wide_unroll() {
   return FLS_WIDE_C5 && FLS_FUNROLL == 2 && FLS_MINB == 4 && KM == KM_SIN && G == 1 && D == 3;
 }
+// the C2 class (d = 2, constant coefficients, sin family): 1 feature per iteration -- at 64
+// registers the compiler runs the 2-feature body's 8 entries nearly one chain at a time anyway,
+// and the 4 outputs of one feature are stored (freeing their registers) before the next;
+// 10-step graph, 3 interleaved rounds (tools/ab_small.sh, FLS_FUNROLL=1 build): C2 17.92 ->
+// 17.48 us, C1 (d = 1) unchanged, so limited to d = 2
 template <int D, int G, int KM>
 __host__ __device__ constexpr int asm_funroll() {
-  return asm_wide_unroll<D, G, KM>() ? FLS_C5_FU : kFUnroll;
+  return asm_wide_unroll<D, G, KM>() ? FLS_C5_FU
+         : (FLS_C2_FU1 && FLS_FUNROLL == 2 && D == 2 && G == 0 && KM == KM_SIN) ? 1
+                                                                               : kFUnroll;
 }
 
 template <int D, int G, int KM>
