@@ -27,6 +27,7 @@ from __future__ import annotations
 import argparse
 import datetime
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -430,7 +431,8 @@ def per_config(names=("c1_poisson1d", "c2_poisson2d", "c3_poisson5d", "c4_heat2d
                budget_s=60.0, known_solves=None):
     """For each config: the bench's step (fls_features_assemble) captured in a CUDA graph of 10
     consecutive steps and replayed (the launch-latency-bound C1/C2 measured without host
-    gaps) -> steady-state entries/s and fraction of the copy peak; the single-shot latency
+    gaps) -> steady-state entries/s and fraction of the copy peak, over the short window and
+    again over >= 0.5 s (`sustained`: what the board's power limiter allows); the single-shot latency
     (host call -> kernels done); the end-to-end solve by phase (known_solves: results already
     measured in this run, e.g. the headline workload's, reused instead of re-solved).  Bounded to
     about budget_s."""
@@ -489,8 +491,22 @@ def per_config(names=("c1_poisson1d", "c2_poisson2d", "c3_poisson5d", "c4_heat2d
                 g.replay()
             e1.record(s)
             torch.cuda.synchronize()
+            window_ms = e0.elapsed_time(e1)
+            # the window above is short (tens of ms): the board's power limiter (sw_power_cap)
+            # reacts over ~0.1-1 s, so the HBM-heavy configs are re-timed over >= 0.5 s
+            n_sus = max(1, reps // per_graph)
+            if window_ms < 400.0:
+                n_sus = max(1, int(math.ceil(n_sus * 500.0 / max(window_ms, 1e-3))))
+            e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e2.record(s)
+            for _ in range(n_sus):
+                g.replay()
+            e3.record(s)
+            torch.cuda.synchronize()
+            sus_window_ms = e2.elapsed_time(e3)
         fls.fls_sync(ctx)
-        ms = e0.elapsed_time(e1) / (max(1, reps // per_graph) * per_graph)
+        ms = window_ms / (max(1, reps // per_graph) * per_graph)
+        ms_sus = sus_window_ms / (n_sus * per_graph)
         del g, Ab
         ctx.close()
         torch.cuda.empty_cache()
@@ -505,6 +521,9 @@ def per_config(names=("c1_poisson1d", "c2_poisson2d", "c3_poisson5d", "c4_heat2d
                      "graph_us_per_step": 1e3 * ms, "entries_per_s": R * F / (ms / 1e3),
                      "hbm_write_gbs": 8.0 * R * (F + 1) / (ms / 1e3) / 1e9,
                      "frac_of_copy_peak": 8.0 * R * F / (ms / 1e3) / 1e9 / hbm_peak,
+                     "window_ms": window_ms,
+                     "sustained": {"window_ms": sus_window_ms, "graph_us_per_step": 1e3 * ms_sus,
+                                   "frac_of_copy_peak": 8.0 * R * F / (ms_sus / 1e3) / 1e9 / hbm_peak},
                      "single_shot_us": statistics.median(singles),
                      "solve_ms": {k: sol[k] for k in ("ms", "features_ms", "assemble_ms",
                                                       "lstsq_ms", "eval_ms")},
