@@ -222,11 +222,8 @@ inline dim3 asm_grid(AsmArgs &a) {
 //     BC CTAs get 424 features each).
 template <int D, int G, int KM>
 inline int64_t asm_plan(AsmArgs *blks, int n, AsmBatch &bt) {
-  static int strategy = -1;
-  if (strategy < 0) {
-    const char *e = getenv("FLS_BATCH_PLAN");
-    strategy = e ? atoi(e) : 1;
-  }
+  const char *plan_env = getenv("FLS_BATCH_PLAN");  // read per call: tests switch it
+  const int strategy = plan_env && *plan_env ? atoi(plan_env) : 1;
   int64_t span = 0;
   for (int q = 0; q < n; ++q) span += blks[q].lr1 - (blks[q].lr0 & ~int64_t(kRowAlign - 1));
   dim3 g[kMaxBatch];

@@ -788,6 +788,35 @@ def test_features_assemble_fused_bit_identical(ctx, name, fuse, monkeypatch):
         fls.fls_features_assemble(ctx, d, F, -1.0, seed, base)
 
 
+@pytest.mark.parametrize("fuse", ["0", "1000000000000"])
+@pytest.mark.parametrize("name,size", [("c1_poisson1d", "full"), ("c2_poisson2d", "full"),
+                                       ("c4_heat2d", "mini")])
+def test_batch_plan_does_not_change_entries(ctx, name, size, fuse, monkeypatch):
+    """the joint launch plan of a multi-block batch (FLS_BATCH_PLAN 0-3: per-block grids, capped
+    features per CTA, one feature count, equal entries) only moves work between CTAs: [A | b]
+    is bit-identical for every strategy, fused and unfused, and matches the oracle"""
+    monkeypatch.setenv("FLS_FUSE_MAX_ENTRIES", fuse)
+    p = wl.make_problem(name, size)
+    F, d = p.n_features, p.dim
+    bs = fls.BlockSet(dev_blocks(p), d)
+    R = bs.total
+    outs = []
+    for plan in ("0", "1", "2", "3"):
+        monkeypatch.setenv("FLS_BATCH_PLAN", plan)
+        Wd, bd, Ab, lda = fls.fls_features_assemble(ctx, d, F, float(p.sigma), int(p.seed), bs)
+        fls.fls_sync(ctx)
+        outs.append(Ab[: (F + 1) * lda].view(F + 1, lda)[:, :R].clone())
+    for k in range(1, 4):
+        assert torch.equal(outs[k], outs[0]), k
+    W, b = Wd.cpu().numpy(), bd.cpu().numpy()   # the entries' parity for the drawn features
+    rows = np.unique(np.linspace(0, R - 1, 64).astype(np.int64))
+    Ao, ro, S = oracle.assemble(W, b, p.blocks, rows=rows)
+    M = outs[0].cpu().numpy()
+    emax, _ = scaled_err(M[:F, rows].T, Ao, S)
+    assert emax <= ENTRY_TOL, emax
+    assert np.array_equal(M[F, rows], ro)
+
+
 def test_pdl_off_gives_identical_entries(ctx, tmp_path):
     """FLS_PDL=0 (assembly launched without programmatic dependent launch, read once per
     process) writes the same bits as the default PDL launch, for the fused and unfused calls"""
