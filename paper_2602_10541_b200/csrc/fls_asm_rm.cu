@@ -71,18 +71,37 @@ __global__ void __launch_bounds__(kRmNT, asm_min_blocks<D, G, KM>()) assemble_rm
       }
     }
     __syncthreads();
-    for (int rr = 0; rr < nrow; ++rr) {
+    auto row = [&](int rr, double &o0, double &o1) {
       double x[D], c[GG];
 #pragma unroll
       for (int k = 0; k < D; ++k) x[k] = xs[rr * RS + k];
 #pragma unroll
       for (int g = 0; g < GG; ++g) c[g] = G > 0 ? xs[rr * RS + D + g] : 0.0;
-      const double o0 = M::entry(rec0, x, c);
-      const double o1 = M::entry(rec1, x, c);
-      double *dst = a.A + (rc + rr) * a.lda + j;
-      if (pair_ok) {
+      o0 = M::entry(rec0, x, c);
+      o1 = M::entry(rec1, x, c);
+    };
+    double *dst = a.A + rc * a.lda + j;
+    const int64_t lda = a.lda;
+    if (pair_ok) {
+      // the common case, branch-free: two rows per iteration (4 independent entries), one
+      // 16-byte store per row
+      int rr = 0;
+      for (; rr + 2 <= nrow; rr += 2, dst += 2 * lda) {
+        double o0, o1, o2, o3;
+        row(rr, o0, o1);
+        row(rr + 1, o2, o3);
         __stcs(reinterpret_cast<double2 *>(dst), make_double2(o0, o1));
-      } else {
+        __stcs(reinterpret_cast<double2 *>(dst + lda), make_double2(o2, o3));
+      }
+      if (rr < nrow) {
+        double o0, o1;
+        row(rr, o0, o1);
+        __stcs(reinterpret_cast<double2 *>(dst), make_double2(o0, o1));
+      }
+    } else {
+      for (int rr = 0; rr < nrow; ++rr, dst += lda) {
+        double o0, o1;
+        row(rr, o0, o1);
         if (jin0) __stcs(dst, o0);
         if (jin1) __stcs(dst + 1, o1);
       }
