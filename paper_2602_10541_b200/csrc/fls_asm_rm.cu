@@ -8,6 +8,10 @@
 // kernel, so both layouts hold bit-identical entries.
 #include "fls_assemble.cuh"
 
+#ifndef FLS_RM_ROWS
+#define FLS_RM_ROWS 2  // rows per iteration of the pair-store loop
+#endif
+
 namespace fls {
 
 constexpr int kRmNT = 256;
@@ -85,15 +89,17 @@ __global__ void __launch_bounds__(kRmNT, asm_min_blocks<D, G, KM>()) assemble_rm
     if (pair_ok) {
       // the common case, branch-free: two rows per iteration (4 independent entries), one
       // 16-byte store per row
+      constexpr int RU = FLS_RM_ROWS;
       int rr = 0;
-      for (; rr + 2 <= nrow; rr += 2, dst += 2 * lda) {
-        double o0, o1, o2, o3;
-        row(rr, o0, o1);
-        row(rr + 1, o2, o3);
-        __stcs(reinterpret_cast<double2 *>(dst), make_double2(o0, o1));
-        __stcs(reinterpret_cast<double2 *>(dst + lda), make_double2(o2, o3));
+      for (; rr + RU <= nrow; rr += RU, dst += RU * lda) {
+        double o[RU][2];
+#pragma unroll
+        for (int u = 0; u < RU; ++u) row(rr + u, o[u][0], o[u][1]);
+#pragma unroll
+        for (int u = 0; u < RU; ++u)
+          __stcs(reinterpret_cast<double2 *>(dst + u * lda), make_double2(o[u][0], o[u][1]));
       }
-      if (rr < nrow) {
+      for (; rr < nrow; ++rr, dst += lda) {
         double o0, o1;
         row(rr, o0, o1);
         __stcs(reinterpret_cast<double2 *>(dst), make_double2(o0, o1));
