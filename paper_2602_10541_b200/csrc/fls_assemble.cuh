@@ -17,6 +17,7 @@
 //   kFUnroll features per loop iteration (2*kPairs*kFUnroll independent entries per thread)
 //   for FP64-pipe ILP; full tiles run a predicate-free loop, ragged tiles a masked one.
 #pragma once
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <type_traits>
@@ -280,6 +281,14 @@ inline int64_t asm_plan(AsmArgs *blks, int n, AsmBatch &bt) {
       }
     }
   }
+  // FLS_PLAN_DEBUG=1 prints each launch's plan (read once).  Measured and rejected: giving every
+  // block of a large multi-wave launch the largest block's features per CTA (C3 141.7 -> 145.2
+  // us, C4 664 -> 713 us; per_config, 2 rounds)
+  static const bool plan_debug = getenv("FLS_PLAN_DEBUG") != nullptr;
+  if (plan_debug)
+    for (int q = 0; q < n; ++q)
+      fprintf(stderr, "fls plan: block %d rows %lld tiles %u groups %u fpc %lld\n", q,
+              (long long)(blks[q].lr1 - blks[q].lr0), g[q].x, g[q].y, (long long)blks[q].fpc);
   bt.n = n;
   int64_t total = 0;
   for (int q = 0; q < n; ++q) {
