@@ -59,6 +59,8 @@ def lib():
         L.orc_diff.argtypes =[C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_assemble.argtypes = [C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
                                    C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.orc_assemble_truth.argtypes = [C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_int,
+                                         C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]
         L.orc_lstsq.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_double,
                                 C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_lstsq_mu.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_double,
@@ -194,6 +196,23 @@ def assemble(W, b, blocks, rows: Optional[np.ndarray] = None, normalize: bool = 
     if st != 0:
         raise ValueError(f"orc_assemble status {st}")
     return A, rhs, S
+
+
+def assemble_truth(W, b, blocks, rows: Optional[np.ndarray] = None, normalize: bool = True):
+    """orc_assemble_truth: the definition in long double, rounded to double at the end (tiny
+    inputs; the near-exact reference of SURVEY §8(c) item 6).  Returns A (n_rows, F)."""
+    W = _f64(W)
+    b = _f64(b)
+    F, d = W.shape
+    total = sum(blk.X.shape[0] for blk in blocks)
+    rows = np.arange(total, dtype=np.int64) if rows is None else np.ascontiguousarray(rows, np.int64)
+    A = np.zeros((rows.size, F))
+    keep = _BlockKeep(blocks)
+    st = lib().orc_assemble_truth(d, F, _p(W), _p(b), int(bool(normalize)), C.addressof(keep.arr),
+                                  len(blocks), _p(rows), rows.size, _p(A))
+    if st != 0:
+        raise ValueError(f"orc_assemble_truth status {st}")
+    return A
 
 
 def lstsq(A, bvec, ridge_rel: float = 0.0):

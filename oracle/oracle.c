@@ -20,6 +20,8 @@
  *   orc_assemble        A_ij = L[phi_j](x_i), term by term, then the
  *                       weighted row blocks [A_pde; lam A_bc; ...]
  *                       and rhs [f; lam g; ...]                     P:L118-124 (Eq.3), Alg.1 l.3-5
+ *   orc_assemble_truth  the same definition in long double (tiny inputs: the
+ *                       near-exact reference both fp64 paths are measured against)
  *   orc_lstsq           argmin ||A beta - b||^2 + mu ||beta||^2 by
  *                       unblocked Householder QR of [A | b] with
  *                       sqrt(mu) I rows appended (GVL Alg. 5.2.1),
@@ -268,6 +270,59 @@ int orc_assemble(int dim, int64_t n_features, const double *W, const double *b, 
         }
     }
     return status;
+}
+
+/*
+ * "Truth" mode for tiny inputs: orc_assemble's definition, same term-by-term
+ * order, carried out in long double (x87 80-bit: 64-bit significand, unit roundoff 5.4e-20) with
+ * sinl / cosl, rounded to double only at the end.  Measures how far the fp64 oracle AND the GPU
+ * path sit from near-exact values (tests/test_oracle_pins.py, tests/test_gpu_parity.py); pinned
+ * itself to mpmath's numerical derivatives of sin(W.x + b) at 40 digits.
+ */
+static long double Phi_l(int32_t p, long double z) {
+    switch (p) {
+        case 0: return sinl(z);
+        case 1: return cosl(z);
+        case 2: return -sinl(z);
+        default: return -cosl(z);
+    }
+}
+
+int orc_assemble_truth(int dim, int64_t n_features, const double *W, const double *b, int normalize,
+                       const orc_block *blocks, int n_blocks, const int64_t *rows, int64_t n_rows,
+                       double *A) {
+    const long double s = normalize ? 1.0L / sqrtl((long double)n_features) : 1.0L;
+    int64_t total = 0;
+    for (int q = 0; q < n_blocks; ++q) total += blocks[q].n_points;
+    for (int64_t r = 0; r < n_rows; ++r) {
+        int64_t g = rows[r];
+        if (g < 0 || g >= total) return -1;
+        int q = 0;
+        int64_t i = g;
+        while (i >= blocks[q].n_points) { i -= blocks[q].n_points; ++q; }
+        const orc_block *B = &blocks[q];
+        const double *x = B->X + i * dim;
+        for (int64_t j = 0; j < n_features; ++j) {
+            const double *w = W + j * dim;
+            long double z = 0.0L;
+            for (int k = 0; k < dim; ++k) z = z + (long double)w[k] * (long double)x[k];
+            z = z + (long double)b[j];
+            long double acc = 0.0L;
+            for (int t = 0; t < B->n_terms; ++t) {
+                const orc_term *T = &B->terms[t];
+                int32_t e[ORC_MAX_DIM], p;
+                orc_diff(dim, T->alpha, e, &p);
+                long double mono = 1.0L;
+                for (int k = 0; k < dim; ++k)
+                    for (int32_t n = 0; n < e[k]; ++n) mono = mono * (long double)w[k];
+                long double c = T->coef;
+                if (T->field >= 0) c = c * (long double)B->coef_fields[i * B->n_fields + T->field];
+                acc = acc + c * mono * Phi_l(p, z);
+            }
+            A[r * n_features + j] = (double)((long double)B->weight * (s * acc));
+        }
+    }
+    return 0;
 }
 
 /* ------------------------------------------------------------------------- */

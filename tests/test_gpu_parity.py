@@ -1031,3 +1031,24 @@ def test_maximum_operator_sizes(ctx):
     Ao, ro, S = oracle.assemble(W, b, [h])
     Ag, rg = rows_from_colmajor(Ab, lda, 97, np.arange(501))
     assert scaled_err(Ag, Ao, S)[0] <= ENTRY_TOL
+
+
+@pytest.mark.parametrize("name", wl.CONFIG_NAMES)
+def test_entries_against_long_double_truth(ctx, name):
+    """both fp64 paths against the long-double truth mode on sampled rows
+    of the reduced configs: the GPU entries within the 1e-12 bar of the A14 scale, and the
+    oracle (the parity reference) an order of magnitude closer still"""
+    p = wl.make_problem(name, "mini")
+    W, b = p.parity_features()
+    F = p.n_features
+    Ab, lda = fls.fls_assemble(ctx, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(),
+                               fls.BlockSet(dev_blocks(p), p.dim))
+    fls.fls_sync(ctx)
+    rows = np.unique(np.linspace(0, p.n_rows - 1, 24).astype(np.int64))
+    Ag, _ = rows_from_colmajor(Ab, lda, F, rows)
+    Ao, _, S = oracle.assemble(W, b, p.blocks, rows=rows)
+    At = oracle.assemble_truth(W, b, p.blocks, rows=rows)
+    e_gpu, _ = scaled_err(Ag, At, S)
+    e_orc, _ = scaled_err(Ao, At, S)
+    assert e_gpu <= ENTRY_TOL, e_gpu
+    assert e_orc <= 2e-14, e_orc

@@ -493,3 +493,58 @@ def test_sample_box_uniform_ks_per_axis():
         assert stats.kstest(X[:, k], "uniform", args=(lo[k], hi[k] - lo[k])).pvalue > 1e-4
     Cm = np.corrcoef(X.T)
     assert np.max(np.abs(Cm - np.eye(dim))) < 5.0 / math.sqrt(n)
+
+
+# ----------------------------------------------------------------------------- truth mode
+def _mp_deriv(Wj, bj, x, alpha):
+    """D^alpha sin(W_j.x + b_j) at x by mpmath's numerical differentiation (40 digits): an
+    independent brute-force value, no derivative cycle involved"""
+    import mpmath as mp
+    d = len(x)
+    f = lambda *xs: mp.sin(mp.fsum(mp.mpf(float(Wj[k])) * xs[k] for k in range(d)) + mp.mpf(float(bj)))
+    pt = tuple(mp.mpf(float(v)) for v in x)
+    if sum(alpha) == 0:
+        return f(*pt)
+    return mp.diff(f, pt, tuple(int(a) for a in alpha))
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_truth_mode_matches_mpmath_derivatives(d):
+    """pin: the long-double 'truth' assembly equals mpmath's 40-digit
+    numerical derivatives of the plain feature to the final rounding to double (<= 2 ulp of
+    the A14 scale), for every alpha with |alpha| <= 4 (a sample for d = 3), several points"""
+    import mpmath as mp
+    mp.mp.dps = 40
+    W, b = rand_basis(d, 5, 3.0, 40 + d)
+    g = np.random.default_rng(100 + d)
+    alphas = [a for a in itertools.product(range(5), repeat=d) if sum(a) <= 4]
+    if len(alphas) > 16:
+        alphas = [alphas[i] for i in g.choice(len(alphas), 16, replace=False)]
+    for alpha in alphas:
+        X = g.random((2, d))
+        terms = [(tuple(alpha), 1.0, -1)]
+        At = oracle.assemble_truth(W, b, [Blk(X, terms)], normalize=False)
+        _, S = col(W, b, X, terms)
+        for i in range(X.shape[0]):
+            for j in range(W.shape[0]):
+                ref = _mp_deriv(W[j], b[j], X[i], alpha)
+                err = abs(mp.mpf(float(At[i, j])) - ref) / mp.mpf(float(S[i, j]))
+                assert err <= 3e-16, (alpha, i, j, float(err))
+
+
+def test_fp64_oracle_error_against_truth():
+    """the fp64 oracle's own error on the configs' operators, measured against truth mode: it
+    stays ~1e-15 of the A14 scale at the configs' phase range -- far below the 1e-12 parity
+    bar, so the oracle is a sound reference for the GPU path"""
+    worst = 0.0
+    for name in wl.CONFIG_NAMES:
+        p = wl.make_problem(name, "mini")
+        W, b = p.parity_features()
+        R = p.n_rows
+        rows = np.linspace(0, R - 1, 12).astype(np.int64)
+        A, _, S = oracle.assemble(W, b, p.blocks, rows=rows)
+        At = oracle.assemble_truth(W, b, p.blocks, rows=rows)
+        e = float((np.abs(A - At) / S).max())
+        worst = max(worst, e)
+        assert e <= 2e-14, (name, e)
+    assert worst > 0.0   # the two differ (fp64 vs long double): the comparison is not vacuous
