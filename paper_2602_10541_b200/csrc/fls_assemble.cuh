@@ -41,6 +41,9 @@
 #ifndef FLS_C2_FU1
 #define FLS_C2_FU1 1  // 0: the C2 class keeps 2 features per iteration (A/B builds)
 #endif
+#ifndef FLS_C3_FU1
+#define FLS_C3_FU1 1  // 0: the C3 class (d = 5) keeps 2 features per iteration (A/B builds)
+#endif
 #ifndef FLS_HOIST
 #define FLS_HOIST 0
 #endif
@@ -132,11 +135,14 @@ __host__ __device__ constexpr bool asm_wide_unroll() {
 // registers the compiler runs the 2-feature body's 8 entries nearly one chain at a time anyway,
 // and the 4 outputs of one feature are stored (freeing their registers) before the next;
 // 10-step graph, 3 interleaved rounds (tools/ab_small.sh, FLS_FUNROLL=1 build): C2 17.92 ->
-// 17.48 us, C1 (d = 1) unchanged, so limited to d = 2
+// 17.48 us, C1 (d = 1) unchanged, so limited to d = 2; the C3 class (d = 5, 80 registers) too:
+// per_config C3 141.6 -> 139.9 us (short window), 167.3 -> 165.9 us sustained (3 rounds,
+// tools/per_config_probe.py)
 template <int D, int G, int KM>
 __host__ __device__ constexpr int asm_funroll() {
   return asm_wide_unroll<D, G, KM>() ? FLS_C5_FU
          : (FLS_C2_FU1 && FLS_FUNROLL == 2 && D == 2 && G == 0 && KM == KM_SIN) ? 1
+         : (FLS_C3_FU1 && FLS_FUNROLL == 2 && D == 5 && G == 0 && KM == KM_SIN) ? 1
                                                                                : kFUnroll;
 }
 
