@@ -44,6 +44,9 @@
 #ifndef FLS_C3_FU1
 #define FLS_C3_FU1 1  // 0: the C3 class (d = 5) keeps 2 features per iteration (A/B builds)
 #endif
+#ifndef FLS_FU1_ALL_G0
+#define FLS_FU1_ALL_G0 0  // 1: every d >= 2 constant-coefficient sin class (C4's d = 3 fold) (A/B)
+#endif
 #ifndef FLS_HOIST
 #define FLS_HOIST 0
 #endif
@@ -143,6 +146,7 @@ __host__ __device__ constexpr int asm_funroll() {
   return asm_wide_unroll<D, G, KM>() ? FLS_C5_FU
          : (FLS_C2_FU1 && FLS_FUNROLL == 2 && D == 2 && G == 0 && KM == KM_SIN) ? 1
          : (FLS_C3_FU1 && FLS_FUNROLL == 2 && D == 5 && G == 0 && KM == KM_SIN) ? 1
+         : (FLS_FU1_ALL_G0 && FLS_FUNROLL == 2 && D >= 2 && G == 0 && KM == KM_SIN) ? 1
                                                                                : kFUnroll;
 }
 
