@@ -11,7 +11,7 @@ static cudaError_t go_sin(AsmArgs *blks, int n, cudaStream_t st, bool pdl,
   // fused: the chunk's normals and biases follow the records in shared memory
   const size_t smem = (size_t)kFC * (S + (fz ? D + 1 : 0)) * sizeof(double);
   AsmBatch bt;
-  const int64_t total = asm_plan<D, G, KM_SIN>(blks, n, bt);
+  const int64_t total = asm_plan<D, G, KM_SIN>(blks, n, bt, fz != nullptr);
   if (fz) {
     if constexpr (G <= 1) {
       auto kern = assemble_cm_kernel<D, G, KM_SIN, FusedBatch>;
@@ -77,3 +77,12 @@ cudaError_t launch_assemble_cm_sin(int D, int G, AsmArgs *blks, int n, cudaStrea
 }
 
 }  // namespace fls
+
+#if FLS_DIAG_CTATIME
+// diagnostic builds only: copy the per-CTA timestamps of the KM_SIN kernels to the host
+extern "C" __attribute__((visibility("default"))) int fls_diag_cta(void *host, long long n) {
+  const long long cap = (long long)fls::kDiagSlots * fls::kDiagCTAs * 8;
+  if (n > cap) n = cap;
+  return (int)cudaMemcpyFromSymbol(host, fls::g_cta_diag, (size_t)n);
+}
+#endif

@@ -59,11 +59,32 @@
 #ifndef FLS_MINB
 #define FLS_MINB 4   // 4 CTAs x 256 threads per SM -> <= 64 registers
 #endif
+#ifndef FLS_DIAG_CTATIME
+#define FLS_DIAG_CTATIME 0  // 1: diagnostic build recording per-CTA timestamps (never a product)
+#endif
 #ifndef FLS_MINB5
 #define FLS_MINB5 3  // d + G = 5 (C3): 3 CTAs -> <= 80 registers
 #endif
 
 namespace fls {
+
+#if FLS_DIAG_CTATIME
+// per CTA: entry, after the records' wait, after the first chunk's records, end (globaltimer ns),
+// SM id, row block -- read back by fls_diag_cta (tools/cta_timeline.py)
+constexpr int kDiagSlots = 6, kDiagCTAs = 65536;
+static __device__ unsigned long long g_cta_diag[kDiagSlots * kDiagCTAs];
+__device__ __forceinline__ unsigned long long diag_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void diag_mark(int slot, unsigned long long v) {
+  if (threadIdx.x == 0 && blockIdx.x < kDiagCTAs) g_cta_diag[blockIdx.x * kDiagSlots + slot] = v;
+}
+#define FLS_DIAG(slot, v) diag_mark(slot, v)
+#else
+#define FLS_DIAG(slot, v) ((void)0)
+#endif
 
 template <int D, int G, int KM>
 struct EntryMath {
@@ -232,7 +253,7 @@ inline dim3 asm_grid(AsmArgs &a) {
 //   3 equal entries per CTA, relaxed until the CTAs fit one wave: C2 20.5, C1 87 us (its 2-row
 //     BC CTAs get 424 features each).
 template <int D, int G, int KM>
-inline int64_t asm_plan(AsmArgs *blks, int n, AsmBatch &bt) {
+inline int64_t asm_plan(AsmArgs *blks, int n, AsmBatch &bt, bool fused = false) {
   const char *plan_env = getenv("FLS_BATCH_PLAN");  // read per call: tests switch it
   const int strategy = plan_env && *plan_env ? atoi(plan_env) : 1;
   int64_t span = 0;
@@ -291,20 +312,64 @@ inline int64_t asm_plan(AsmArgs *blks, int n, AsmBatch &bt) {
       }
     }
   }
+  // segments: block q's features [0, F) as one segment (the plan above), or -- guided tail,
+  // FLS_TAIL_PCT percent of its features, FLS_TAIL_FPC features per CTA -- a main segment and
+  // a tail segment of narrower CTAs; every tail follows every main segment in the grid, so the
+  // hardware dispatches the narrow CTAs last, into the SM slots the main CTAs free.  The
+  // per-CTA timeline of C2 (tools/cta_timeline.py: FLS_DIAG_CTATIME build) shows why: the warp
+  // schedulers favour the oldest CTAs, so an SM's four first-wave CTAs end at 40-100% of the
+  // window and the busy slots fall from 592 to 65 over its last 40%.  Interleaved A/B
+  // (tools/ab_tail.py, 10-step graphs, 4 rounds): C2 17.52 -> 17.24 us at 10% / 4 features
+  // (5% / 4: 17.41, 10% / 6: 17.43, 10% / 8: 17.63, 20% / 4: 18.35); the fused C1 gets slower
+  // (4.94 -> 5.21 us) and so do the multi-wave launches (C3 141 -> 155 us, C4 664 -> 716 us at
+  // 10% / 4: their narrow CTAs' prologues cost more than the drain they shorten), so the
+  // default tail is for unfused launches of 2^22 .. 2^25 entries (C2) only.
+  const char *tp_env = getenv("FLS_TAIL_PCT");
+  const char *tf_env = getenv("FLS_TAIL_FPC");
+  const bool tail_class = !fused && span * F > (int64_t(1) << 22) && span * F <= (int64_t(1) << 25);
+  const int64_t tail_pct = tp_env && *tp_env ? atoll(tp_env) : (tail_class ? 10 : 0);
+  const int64_t tail_fpc = tf_env && *tf_env ? atoll(tf_env) : 4;
+  AsmArgs seg[kMaxSeg];
+  dim3 sg[kMaxSeg];
+  int nseg = n;
+  for (int q = 0; q < n; ++q) {
+    seg[q] = blks[q];
+    seg[q].f_begin = 0;
+    seg[q].f_end = blks[q].F;
+    seg[q].pre_idx = q;
+    sg[q] = g[q];
+  }
+  if (tail_pct > 0 && tail_fpc > 0) {
+    for (int q = 0; q < n; ++q) {
+      const int64_t Fq = blks[q].F, T = (Fq * tail_pct / 100) & ~int64_t(1);
+      if (T < tail_fpc || Fq - T < blks[q].fpc) continue;
+      seg[q].f_end = Fq - T;
+      sg[q].y = (unsigned)((Fq - T + blks[q].fpc - 1) / blks[q].fpc);
+      AsmArgs &t = seg[nseg];
+      t = seg[q];
+      t.f_begin = Fq - T;
+      t.f_end = Fq;
+      t.fpc = tail_fpc;
+      t.rhs = nullptr;
+      sg[nseg] = dim3(g[q].x, (unsigned)((T + tail_fpc - 1) / tail_fpc));
+      ++nseg;
+    }
+  }
   // FLS_PLAN_DEBUG=1 prints each launch's plan (read once).  Measured and rejected: giving every
   // block of a large multi-wave launch the largest block's features per CTA (C3 141.7 -> 145.2
   // us, C4 664 -> 713 us; per_config, 2 rounds)
   static const bool plan_debug = getenv("FLS_PLAN_DEBUG") != nullptr;
   if (plan_debug)
-    for (int q = 0; q < n; ++q)
-      fprintf(stderr, "fls plan: block %d rows %lld tiles %u groups %u fpc %lld\n", q,
-              (long long)(blks[q].lr1 - blks[q].lr0), g[q].x, g[q].y, (long long)blks[q].fpc);
-  bt.n = n;
+    for (int q = 0; q < nseg; ++q)
+      fprintf(stderr, "fls plan: block %d rows %lld tiles %u groups %u fpc %lld features [%lld, %lld)\n",
+              seg[q].pre_idx, (long long)(seg[q].lr1 - seg[q].lr0), sg[q].x, sg[q].y,
+              (long long)seg[q].fpc, (long long)seg[q].f_begin, (long long)seg[q].f_end);
+  bt.n = nseg;
   int64_t total = 0;
-  for (int q = 0; q < n; ++q) {
-    bt.blk[q] = blks[q];
-    bt.rt[q] = g[q].x;
-    total += (int64_t)g[q].x * g[q].y;
+  for (int q = 0; q < nseg; ++q) {
+    bt.blk[q] = seg[q];
+    bt.rt[q] = sg[q].x;
+    total += (int64_t)sg[q].x * sg[q].y;
     bt.cta_end[q] = total;
   }
   return total;
@@ -363,7 +428,7 @@ __device__ __forceinline__ void phase_check(const double *pf, int64_t f0, int64_
 
 // the fused kernel's exact check: records recomputed per feature (rare path)
 template <int D, int NQ>
-__device__ __forceinline__ void phase_check_wb(const FusedBatch &fz, int qb, int64_t f0, int64_t f1,
+__device__ __forceinline__ void phase_check_wb(const FusedBatch &fz, int pq, int64_t f0, int64_t f1,
                                                const double (&x)[NQ][D], const bool (&in)[NQ],
                                                unsigned *err) {
   double rec[pf_stride(FLS_MAX_DIM, FLS_MAX_FIELDS, KM_SINCOS)];
@@ -371,7 +436,7 @@ __device__ __forceinline__ void phase_check_wb(const FusedBatch &fz, int qb, int
   for (int64_t j = f0; j < f1; ++j) {
 #pragma unroll
     for (int k = 0; k < D; ++k) w[k] = feat_normal(j * D + k, D, fz.fb, fz.seed);
-    prefactor_rec<>(fz.pre[qb], w, feat_bias(j, fz.seed), rec);
+    prefactor_rec<>(fz.pre[pq], w, feat_bias(j, fz.seed), rec);
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       double h = rec[D];
@@ -406,6 +471,7 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
   // let the next PDL launch on the stream (the next call's feature / prefactor kernel, which
   // writes nothing before its own griddepcontrol.wait) start while this grid runs
   pdl_trigger();
+  FLS_DIAG(0, diag_now());
   int qb = 0;
   while (qb + 1 < bt.n && (int64_t)blockIdx.x >= bt.cta_end[qb]) ++qb;
   const AsmArgs &a = bt.blk[qb];
@@ -413,8 +479,8 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
   const int64_t tile = cta % bt.rt[qb], group = cta / bt.rt[qb];
   // this CTA's feature range [f0, f1) (a.fpc features per CTA, chosen by the launcher), walked
   // in shared-memory chunks of at most kFC records
-  const int64_t f0 = group * a.fpc;
-  const int64_t f1 = f0 + a.fpc < a.F ? f0 + a.fpc : a.F;
+  const int64_t f0 = a.f_begin + group * a.fpc;
+  const int64_t f1 = f0 + a.fpc < a.f_end ? f0 + a.fpc : a.f_end;
   // phase-range guard (FLS_MAX_PHASE): |h_ij| <= ||W_j/pi||_1 ||x_i||_inf + |b'_j/pi|.  The
   // feature side is max-reduced over the CTA's records chunk by chunk (s_guard, off the entry
   // path); at the end a thread whose bound exceeds the limit re-checks its rows exactly.
@@ -426,7 +492,7 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
   // Philox chains side by side; a2 -- one thread per feature folds its record.  Reads nothing
   // from global memory; writes W, b only when wr.
   bool wr = false;
-  if constexpr (kFused) wr = fz.write_wb && qb == 0 && tile == 0;
+  if constexpr (kFused) wr = fz.write_wb && a.pre_idx == 0 && tile == 0;
   auto fused_chunk = [&](int64_t j0, int nfe, bool write_wb) {
     if constexpr (kFused) {
       double *ws = sp + kFC * S;      // normals (nfe * D), then biases (nfe)
@@ -446,7 +512,7 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
       }
       __syncthreads();
       for (int t = threadIdx.x; t < nfe; t += kNT)
-        prefactor_rec<GG + 1>(fz.pre[qb], ws + t * D, bs[t], sp + t * S);
+        prefactor_rec<GG + 1>(fz.pre[a.pre_idx], ws + t * D, bs[t], sp + t * S);
     }
   };
   const int nfe0 = (f1 - f0) < kFC ? (int)(f1 - f0) : kFC;
@@ -495,6 +561,7 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
   // triggered, which it does only after everything ahead of it on the stream completed -- so
   // the points above were safe to read; the records it writes are safe to read from here on
   if constexpr (!kFused) pdl_wait();
+  FLS_DIAG(1, diag_now());
   if (group == 0 && a.rhs != nullptr) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -528,6 +595,7 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
       for (int t = threadIdx.x; t < n2; t += kNT) dst[t] = __ldg(src + t);
     }
     __syncthreads();
+    if (j0 == f0) FLS_DIAG(2, diag_now());
     if (threadIdx.x < nfe) {
       const double *r = sp + threadIdx.x * S;
       double w1 = 0.0;
@@ -595,13 +663,22 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
     }
   }
   __syncthreads();
+#if FLS_DIAG_CTATIME
+  {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    FLS_DIAG(3, diag_now());
+    FLS_DIAG(4, smid);
+    FLS_DIAG(5, qb);
+  }
+#endif
   const double bound = fma(__longlong_as_double((long long)s_guard[0]), xinf,
                            __longlong_as_double((long long)s_guard[1]));
   if (bound > kMaxHalfTurns) {
     if constexpr (kFused) {
       // no record array in global memory: the records are recomputed (prefactor_rec, the same
       // draw and fold, so h is bit-identical to the entry's)
-      phase_check_wb<D, NQ>(fz, qb, f0, f1, x, in, a.err);
+      phase_check_wb<D, NQ>(fz, a.pre_idx, f0, f1, x, in, a.err);
     } else {
       phase_check<D, S, NQ>(a.pf, f0, f1, x, in, a.err);
     }

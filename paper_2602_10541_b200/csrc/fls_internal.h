@@ -83,6 +83,8 @@ struct AsmArgs {
   int64_t fpc;                   // features per CTA (set by the launcher)
   int64_t batch_span;            // rows of all blocks in this launch (set by the launcher)
   int32_t gfield[FLS_MAX_FIELDS];// field id of group g+1
+  int64_t f_begin, f_end;        // feature range of this launch segment (set by the launcher)
+  int32_t pre_idx;               // the segment's row block within the launch (fused fold args)
 };
 
 struct EvalArgs {
@@ -126,11 +128,14 @@ struct SampleArgs {
 cudaError_t launch_sample(const SampleArgs &a, cudaStream_t st);
 // several row blocks sharing a kernel variant in one launch
 constexpr int kMaxBatch = 4;
+// a launch's segments: each row block's feature range split into a main part and a tail of
+// narrower CTAs dispatched last (asm_plan)
+constexpr int kMaxSeg = 2 * kMaxBatch;
 struct AsmBatch {
   int32_t n;
-  int64_t cta_end[kMaxBatch];  // prefix sums of the blocks' CTA counts
-  int64_t rt[kMaxBatch];       // row tiles per block
-  AsmArgs blk[kMaxBatch];
+  int64_t cta_end[kMaxSeg];  // prefix sums of the segments' CTA counts
+  int64_t rt[kMaxSeg];       // row tiles per segment
+  AsmArgs blk[kMaxSeg];
 };
 struct PrefBatch {
   int32_t n;

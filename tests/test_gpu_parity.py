@@ -817,6 +817,56 @@ def test_batch_plan_does_not_change_entries(ctx, name, size, fuse, monkeypatch):
     assert np.array_equal(M[F, rows], ro)
 
 
+@pytest.mark.parametrize("fuse", ["0", "1000000000000"])
+@pytest.mark.parametrize("name,size", [("c1_poisson1d", "full"), ("c2_poisson2d", "full"),
+                                       ("c3_poisson5d", "mini"), ("c4_heat2d", "mini")])
+def test_guided_tail_does_not_change_entries(ctx, name, size, fuse, monkeypatch):
+    """the launch plan's guided tail (each block's last FLS_TAIL_PCT % of features in narrower
+    CTAs dispatched after every main CTA; default on for unfused launches of 2^22..2^25
+    entries) only moves work between CTAs: [A | b] and W, b are bit-identical with and without
+    it, fused and unfused, for tails that split feature chunks unevenly (odd per-CTA counts,
+    a tail narrower than one CTA), and the entries match the oracle"""
+    monkeypatch.setenv("FLS_FUSE_MAX_ENTRIES", fuse)
+    p = wl.make_problem(name, size)
+    F, d = p.n_features, p.dim
+    bs = fls.BlockSet(dev_blocks(p), d)
+    R = bs.total
+    outs = []
+    for pct, fpc in (("0", "4"), ("10", "4"), ("5", "3"), ("33", "2"), ("50", "1000")):
+        monkeypatch.setenv("FLS_TAIL_PCT", pct)
+        monkeypatch.setenv("FLS_TAIL_FPC", fpc)
+        Wd, bd, Ab, lda = fls.fls_features_assemble(ctx, d, F, float(p.sigma), int(p.seed), bs)
+        fls.fls_sync(ctx)
+        outs.append((Ab[: (F + 1) * lda].view(F + 1, lda)[:, :R].clone(), Wd.clone(), bd.clone()))
+    for k in range(1, len(outs)):
+        for t in range(3):
+            assert torch.equal(outs[k][t], outs[0][t]), (k, t)
+    W, b = outs[0][1].cpu().numpy(), outs[0][2].cpu().numpy()
+    rows = np.unique(np.linspace(0, R - 1, 64).astype(np.int64))
+    Ao, ro, S = oracle.assemble(W, b, p.blocks, rows=rows)
+    M = outs[0][0].cpu().numpy()
+    emax, _ = scaled_err(M[:F, rows].T, Ao, S)
+    assert emax <= ENTRY_TOL, emax
+    assert np.array_equal(M[F, rows], ro)
+
+
+def test_guided_tail_keeps_the_phase_guard(ctx, monkeypatch):
+    """a phase out of range inside a tail segment's features still raises FLS_EUNSUPPORTED"""
+    monkeypatch.setenv("FLS_TAIL_PCT", "25")
+    monkeypatch.setenv("FLS_TAIL_FPC", "2")
+    p = wl.make_problem("c2_poisson2d", "mini")
+    F, d = p.n_features, p.dim
+    W, b = p.parity_features()
+    W = W.copy()
+    W[F - 1, :] = 5e4          # the last feature sits in the tail: |W.x| > FLS_MAX_PHASE
+    bs = fls.BlockSet(dev_blocks(p), d)
+    from paper_2602_10541_b200._abi import FlsError
+    fls.fls_assemble(ctx, torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda(), bs)
+    with pytest.raises(FlsError, match="EUNSUPPORTED"):
+        fls.fls_sync(ctx)
+    fls.fls_sync(ctx)                                        # flag cleared
+
+
 def test_pdl_off_gives_identical_entries(ctx, tmp_path):
     """FLS_PDL=0 (assembly launched without programmatic dependent launch, read once per
     process) writes the same bits as the default PDL launch, for the fused and unfused calls"""
