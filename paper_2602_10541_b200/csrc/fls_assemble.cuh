@@ -70,8 +70,9 @@ namespace fls {
 
 #if FLS_DIAG_CTATIME
 // per CTA: entry, after the records' wait, after the first chunk's records, end (globaltimer ns),
-// SM id, row block -- read back by fls_diag_cta (tools/cta_timeline.py)
-constexpr int kDiagSlots = 6, kDiagCTAs = 65536;
+// SM id, launch segment, (unused), points loaded -- read back by fls_diag_cta
+// (tools/cta_timeline.py)
+constexpr int kDiagSlots = 8, kDiagCTAs = 65536;
 static __device__ unsigned long long g_cta_diag[kDiagSlots * kDiagCTAs];
 __device__ __forceinline__ unsigned long long diag_now() {
   unsigned long long t;
@@ -85,6 +86,23 @@ __device__ __forceinline__ void diag_mark(int slot, unsigned long long v) {
 #else
 #define FLS_DIAG(slot, v) ((void)0)
 #endif
+
+#ifndef FLS_X_EVICT_LAST
+#define FLS_X_EVICT_LAST 0  // 1: point loads with an L2 evict_last policy (A/B builds)
+#endif
+// the prologue's 16-byte point loads
+__device__ __forceinline__ double2 ldg_points(const double2 *p) {
+#if FLS_X_EVICT_LAST
+  double2 v;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
 
 template <int D, int G, int KM>
 struct EntryMath {
@@ -539,17 +557,54 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
     const int64_t r = kQuad ? rbase + q : rbase + (q >> 1) * (2 * kNT) + (q & 1);
     in[q] = (r >= a.lr0) && (r < a.lr1);
     full = full && in[q];
+  }
+  // the points of a row pair are 2 D contiguous doubles: D 16-byte loads per pair instead of
+  // 2 D 8-byte ones when the pair's first point sits on a 16-byte boundary (X aligned and
+  // (pt0 - lr0) D even; rbase is even).  The CTA prologue's point loads were its longest step
+  // (C2: 1.6 us of per-CTA latency at the start of each step, tools/cta_timeline.py)
+  const int64_t podd = (a.pt0 - a.lr0) & 1;
+  const bool xvec = !kQuad && ((reinterpret_cast<uintptr_t>(a.X) & 15) == 0) && ((podd * D) & 1) == 0;
+  const bool cvec = !kQuad && G == 1 && a.nf == 1 && a.gfield[0] == 0 &&
+                    ((reinterpret_cast<uintptr_t>(a.fields) & 15) == 0) && podd == 0;
+#pragma unroll
+  for (int pr = 0; pr < NQ / 2; ++pr) {
+    const int q0 = 2 * pr;
+    const int64_t r0 = kQuad ? rbase + q0 : rbase + pr * (2 * kNT);
+    const int64_t i0 = a.pt0 + (r0 - a.lr0);
+    if (xvec && in[q0] && in[q0 + 1]) {
+      const double2 *xp = reinterpret_cast<const double2 *>(a.X + i0 * D);
+#pragma unroll
+      for (int m = 0; m < D; ++m) {
+        const double2 v = ldg_points(xp + m);
+        x[q0 + (2 * m) / D][(2 * m) % D] = v.x;
+        x[q0 + (2 * m + 1) / D][(2 * m + 1) % D] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < D; ++k) x[q0 + h][k] = in[q0 + h] ? __ldg(a.X + (i0 + h) * D + k) : 0.0;
+    }
+    if (G > 0 && cvec && in[q0] && in[q0 + 1]) {
+      const double2 v = __ldg(reinterpret_cast<const double2 *>(a.fields + i0));
+      c[q0][0] = v.x;
+      c[q0 + 1][0] = v.y;
+    } else {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int g = 0; g < GG; ++g)
+          c[q0 + h][g] = (G > 0 && in[q0 + h]) ? __ldg(a.fields + (i0 + h) * a.nf + a.gfield[g]) : 0.0;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) bad |= !finite(x[q][k]);
+#pragma unroll
+    for (int g = 0; g < GG; ++g) bad |= !finite(c[q][g]);
+    const int64_t r = kQuad ? rbase + q : rbase + (q >> 1) * (2 * kNT) + (q & 1);
     const int64_t i = a.pt0 + (r - a.lr0);
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-      x[q][k] = in[q] ? __ldg(a.X + i * D + k) : 0.0;
-      bad |= !finite(x[q][k]);
-    }
-#pragma unroll
-    for (int g = 0; g < GG; ++g) {
-      c[q][g] = (G > 0 && in[q]) ? __ldg(a.fields + i * a.nf + a.gfield[g]) : 0.0;
-      bad |= !finite(c[q][g]);
-    }
     rv[q] = 0.0;
     if (group == 0 && a.rhs != nullptr && in[q]) {
       const double v = a.values ? __ldg(a.values + i) : 0.0;
@@ -560,6 +615,7 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
   // the two-launch path: this grid is launched (PDL) once the prefactor kernel before it has
   // triggered, which it does only after everything ahead of it on the stream completed -- so
   // the points above were safe to read; the records it writes are safe to read from here on
+  FLS_DIAG(6, diag_now() + (bad ? 1 : 0));  // (the points have arrived: bad depends on them)
   if constexpr (!kFused) pdl_wait();
   FLS_DIAG(1, diag_now());
   if (group == 0 && a.rhs != nullptr) {

@@ -201,6 +201,49 @@ def test_unaligned_lda_and_pointer_scalar_path(ctx):
     assert torch.isnan(A2[lda2 - 1])                # padding row untouched
 
 
+@pytest.mark.parametrize("d", [1, 2, 3, 5])
+def test_point_loads_vector_and_scalar_paths(ctx, d):
+    """the CTA prologue loads a row pair's points (and a single coefficient field) as 16-byte
+    vectors when the pair starts on a 16-byte boundary, else element by element: blocks that
+    start at odd rows, X / field arrays 8 bytes off a 16-byte boundary and a ragged tail give
+    bit-identical entries to the aligned layout and match the oracle"""
+    F = 37
+    g = np.random.default_rng(d)
+    W = g.normal(0, 2, (F, d))
+    b = g.uniform(0, 2 * math.pi, F)
+    Wd, bd = torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda()
+    sizes = [3, 1030, 517]                       # blocks start at rows 0, 3 (odd), 1033 (odd)
+    Xs = [g.random((n, d)) for n in sizes]
+    fs = [1.0 + g.random((n, 1)) for n in sizes]
+    vals = [g.random(n) for n in sizes]
+    terms = [((2,) + (0,) * (d - 1), -1.0, -1), ((0,) * d, 4.0, 0)]   # -u_xx + 4 c(x) u
+
+    def dev(t, off):
+        """contiguous device copy whose data pointer is `off` doubles past a 16-byte boundary"""
+        flat = torch.empty(t.size + 2, dtype=torch.float64, device="cuda")
+        v = flat[off: off + t.size]
+        v.copy_(torch.from_numpy(np.ascontiguousarray(t).ravel()))
+        return v.view(t.shape)
+
+    outs = []
+    for off in (0, 1):
+        blocks = [fls.Block(dev(X, off), terms, 1.0, dev(v, off), dev(f, off))
+                  for X, v, f in zip(Xs, vals, fs)]
+        Ab, lda = fls.fls_assemble(ctx, Wd, bd, blocks)
+        fls.fls_sync(ctx)
+        R = sum(sizes)
+        outs.append(Ab[: (F + 1) * lda].view(F + 1, lda)[:, :R].clone())
+    assert torch.equal(outs[0], outs[1])
+
+    class B:
+        def __init__(s, X, v, f):
+            s.X, s.terms, s.weight, s.values, s.fields = X, terms, 1.0, v, f
+    Ao, ro, S = oracle.assemble(W, b, [B(X, v, f) for X, v, f in zip(Xs, vals, fs)])
+    M = outs[0].cpu().numpy()
+    assert scaled_err(M[:F].T, Ao, S)[0] <= ENTRY_TOL
+    assert np.array_equal(M[F], ro)
+
+
 def test_empty_and_ragged_blocks(ctx):
     d, F = 3, 131
     g = np.random.default_rng(0)

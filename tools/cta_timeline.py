@@ -25,7 +25,7 @@ sys.path.insert(0, ROOT)
 import workloads as wl  # noqa: E402
 from paper_2602_10541_b200 import _abi, fls  # noqa: E402
 
-SLOTS = 6
+SLOTS = 8
 
 
 def main(names):
@@ -79,6 +79,8 @@ def main(names):
                 key = f"block{q}"
                 phases.setdefault(key + "_ctas", []).append(int(m.sum()))
                 phases.setdefault(key + "_wait_us", []).append(float(np.median(tq[:, 1] - tq[:, 0])) / 1e3)
+                t6 = r[m, 6].astype(np.int64) - t0
+                phases.setdefault(key + "_points_us", []).append(float(np.median(t6 - tq[:, 0])) / 1e3)
                 phases.setdefault(key + "_records_us", []).append(float(np.median(tq[:, 2] - tq[:, 1])) / 1e3)
                 phases.setdefault(key + "_body_us", []).append(float(np.median(tq[:, 3] - tq[:, 2])) / 1e3)
                 phases.setdefault(key + "_start_p0_p50_p100_us", []).append(
