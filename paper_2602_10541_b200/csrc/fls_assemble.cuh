@@ -597,19 +597,40 @@ assemble_cm_kernel(const AsmBatch bt, const Z fz) {
           c[q0 + h][g] = (G > 0 && in[q0 + h]) ? __ldg(a.fields + (i0 + h) * a.nf + a.gfield[g]) : 0.0;
     }
   }
+  if constexpr (kFused) {
+    // the rhs values are requested with the points, before anything waits for either (C1
+    // 10-step graph 4.91 -> 4.79 us; the same order makes the unfused C2 launch slower,
+    // 16.41 -> 16.68 us, so that one keeps the order below -- tools/ab_lib.sh, 3 rounds)
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) {
+    for (int q = 0; q < NQ; ++q) {
+      const int64_t r = kQuad ? rbase + q : rbase + (q >> 1) * (2 * kNT) + (q & 1);
+      const int64_t i = a.pt0 + (r - a.lr0);
+      rv[q] = (group == 0 && a.rhs != nullptr && in[q] && a.values) ? __ldg(a.values + i) : 0.0;
+    }
 #pragma unroll
-    for (int k = 0; k < D; ++k) bad |= !finite(x[q][k]);
+    for (int q = 0; q < NQ; ++q) {
 #pragma unroll
-    for (int g = 0; g < GG; ++g) bad |= !finite(c[q][g]);
-    const int64_t r = kQuad ? rbase + q : rbase + (q >> 1) * (2 * kNT) + (q & 1);
-    const int64_t i = a.pt0 + (r - a.lr0);
-    rv[q] = 0.0;
-    if (group == 0 && a.rhs != nullptr && in[q]) {
-      const double v = a.values ? __ldg(a.values + i) : 0.0;
-      bad |= !finite(v);
-      rv[q] = a.weight * v;
+      for (int k = 0; k < D; ++k) bad |= !finite(x[q][k]);
+#pragma unroll
+      for (int g = 0; g < GG; ++g) bad |= !finite(c[q][g]);
+      bad |= !finite(rv[q]);
+      rv[q] *= a.weight;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) bad |= !finite(x[q][k]);
+#pragma unroll
+      for (int g = 0; g < GG; ++g) bad |= !finite(c[q][g]);
+      const int64_t r = kQuad ? rbase + q : rbase + (q >> 1) * (2 * kNT) + (q & 1);
+      const int64_t i = a.pt0 + (r - a.lr0);
+      rv[q] = 0.0;
+      if (group == 0 && a.rhs != nullptr && in[q]) {
+        const double v = a.values ? __ldg(a.values + i) : 0.0;
+        bad |= !finite(v);
+        rv[q] = a.weight * v;
+      }
     }
   }
   // the two-launch path: this grid is launched (PDL) once the prefactor kernel before it has
