@@ -18,13 +18,23 @@ constexpr int kRmNT = 256;
 constexpr int kRmTileF = 2 * kRmNT;   // features per CTA
 constexpr int kRmChunk = 64;          // rows staged per shared-memory chunk
 
+__device__ __forceinline__ void rm_cp_async8(double *smem, const double *gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void rm_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void rm_cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 template <int D, int G, int KM>
 __global__ void __launch_bounds__(kRmNT, asm_min_blocks<D, G, KM>()) assemble_rm_kernel(const AsmArgs a) {
   using M = EntryMath<D, G, KM>;
   constexpr int S = M::S;
   constexpr int GG = G > 0 ? G : 1;
   constexpr int RS = D + GG;          // staged doubles per row
-  __shared__ double xs[kRmChunk * RS];
+  // two staging buffers: the rows of chunk c + 1 are copied (cp.async, no registers) while
+  // chunk c is computed, so the CTA never waits on a global round trip between chunks
+  __shared__ __align__(16) double xs[2][kRmChunk * RS];
 
   const int64_t j = (int64_t)blockIdx.x * kRmTileF + 2 * threadIdx.x;
   const bool jin0 = j < a.F, jin1 = j + 1 < a.F;
@@ -36,7 +46,8 @@ __global__ void __launch_bounds__(kRmNT, asm_min_blocks<D, G, KM>()) assemble_rm
   }
   const bool pair_ok = a.vec && jin1;
   // phase-range guard (FLS_MAX_PHASE): feature side from the thread's two records, row side
-  // max-reduced over the staged rows (s_xinf); exact re-check only past the bound
+  // max-reduced over the staged rows (per thread, then per warp into s_xinf); exact re-check
+  // only past the bound
   __shared__ unsigned long long s_xinf;
   double w1 = 0.0, bb = 0.0;
   {
@@ -53,18 +64,33 @@ __global__ void __launch_bounds__(kRmNT, asm_min_blocks<D, G, KM>()) assemble_rm
   const int64_t r0 = a.lr0 + (int64_t)blockIdx.y * a.fpc;
   const int64_t r1 = r0 + a.fpc < a.lr1 ? r0 + a.fpc : a.lr1;
   bool bad = false;
-  for (int64_t rc = r0; rc < r1; rc += kRmChunk) {
+  double xmax = 0.0;
+  auto stage = [&](int64_t rc, int buf) {
     const int nrow = (r1 - rc) < kRmChunk ? (int)(r1 - rc) : kRmChunk;
-    __syncthreads();
     for (int t = threadIdx.x; t < nrow * RS; t += kRmNT) {
       const int rr = t / RS, k = t % RS;
       const int64_t i = a.pt0 + (rc + rr - a.lr0);
-      double v;
-      if (k < D) v = __ldg(a.X + i * D + k);
-      else v = G > 0 ? __ldg(a.fields + i * a.nf + a.gfield[k - D]) : 0.0;
+      if (k < D) rm_cp_async8(&xs[buf][t], a.X + i * D + k);
+      else if (G > 0) rm_cp_async8(&xs[buf][t], a.fields + i * a.nf + a.gfield[k - D]);
+      else xs[buf][t] = 0.0;
+    }
+    rm_cp_commit();
+  };
+  if (r0 < r1) stage(r0, 0);
+  int buf = 0;
+  for (int64_t rc = r0; rc < r1; rc += kRmChunk, buf ^= 1) {
+    const int nrow = (r1 - rc) < kRmChunk ? (int)(r1 - rc) : kRmChunk;
+    if (rc + kRmChunk < r1) {
+      stage(rc + kRmChunk, buf ^ 1);  // its buffer was last read before the previous barrier
+      rm_cp_wait<1>();
+    } else {
+      rm_cp_wait<0>();
+    }
+    __syncthreads();  // chunk rc staged by every thread
+    for (int t = threadIdx.x; t < nrow * RS; t += kRmNT) {
+      const double v = xs[buf][t];
       bad |= !finite(v);
-      xs[t] = v;
-      if (k < D) atomicMax(&s_xinf, (unsigned long long)__double_as_longlong(fabs(v)));
+      if (t % RS < D) xmax = fmax(xmax, fabs(v));
     }
     if (blockIdx.x == 0 && a.rhs != nullptr) {
       for (int rr = threadIdx.x; rr < nrow; rr += kRmNT) {
@@ -74,13 +100,13 @@ __global__ void __launch_bounds__(kRmNT, asm_min_blocks<D, G, KM>()) assemble_rm
         a.rhs[rc + rr] = a.weight * v;
       }
     }
-    __syncthreads();
+    const double *xb = xs[buf];
     auto row = [&](int rr, double &o0, double &o1) {
       double x[D], c[GG];
 #pragma unroll
-      for (int k = 0; k < D; ++k) x[k] = xs[rr * RS + k];
+      for (int k = 0; k < D; ++k) x[k] = xb[rr * RS + k];
 #pragma unroll
-      for (int g = 0; g < GG; ++g) c[g] = G > 0 ? xs[rr * RS + D + g] : 0.0;
+      for (int g = 0; g < GG; ++g) c[g] = G > 0 ? xb[rr * RS + D + g] : 0.0;
       o0 = M::entry(rec0, x, c);
       o1 = M::entry(rec1, x, c);
     };
@@ -112,8 +138,12 @@ __global__ void __launch_bounds__(kRmNT, asm_min_blocks<D, G, KM>()) assemble_rm
         if (jin1) __stcs(dst + 1, o1);
       }
     }
+    __syncthreads();  // chunk rc's buffer free for the chunk after next
   }
   if (bad) atomicOr(a.err, kErrNonFinite);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) xmax = fmax(xmax, __shfl_xor_sync(0xffffffffu, xmax, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(&s_xinf, (unsigned long long)__double_as_longlong(xmax));
   __syncthreads();
   if (fma(w1, __longlong_as_double((long long)s_xinf), bb) > kMaxHalfTurns) {
     for (int64_t r = r0; r < r1; ++r) {   // exact re-check of this thread's two features
