@@ -137,6 +137,42 @@ def test_row_major_and_shards_bit_identical(ctx):
     fls.fls_sync(ctx)
 
 
+def test_row_major_multi_chunk_staging(ctx):
+    """row-major CTAs that stage several 64-row chunks of points (double-buffered cp.async)
+    with a ragged last chunk, a coefficient field (G = 1), an odd feature count (the last
+    thread's second feature is out of range) and a block starting at an odd row: bit-identical
+    to the column-major layout, sampled rows within the entry tolerance of the oracle"""
+    d, F = 3, 101
+    g = np.random.default_rng(7)
+    W = g.normal(0, 3, (F, d))
+    b = g.uniform(0, 2 * math.pi, F)
+    Wd, bd = torch.from_numpy(W).cuda(), torch.from_numpy(b).cuda()
+    sizes = [299_999, 1_003]
+    terms = wl.op_biharmonic(3) + [((0, 0, 0), 16.0, 0)]
+    Xs = [g.random((n, d)) for n in sizes]
+    fs = [1.0 + g.random((n, 1)) for n in sizes]
+    vals = [g.random(n) for n in sizes]
+    blocks = [fls.Block(torch.from_numpy(X).cuda(), terms, w, torch.from_numpy(v).cuda(),
+                        torch.from_numpy(f).cuda()) for X, v, f, w in zip(Xs, vals, fs, (1.0, 3.0))]
+    R = sum(sizes)
+    Ab, lda = fls.fls_assemble(ctx, Wd, bd, blocks)
+    Arm, rrm = fls.fls_assemble(ctx, Wd, bd, blocks, layout=fls.FLS_ROW_MAJOR)
+    fls.fls_sync(ctx)
+    full = Ab[: (F + 1) * lda].view(F + 1, lda)[:, :R]
+    assert torch.equal(Arm[:, :F], full[:F].T) and torch.equal(rrm, full[F])
+
+    class B:
+        def __init__(s, X, v, f, w):
+            s.X, s.terms, s.weight, s.values, s.fields = X, terms, w, v, f
+    rows = np.unique(np.concatenate([np.linspace(0, R - 1, 97).astype(np.int64),
+                                     np.arange(299_990, 300_010)]))
+    Ao, ro, S = oracle.assemble(W, b, [B(X, v, f, w) for X, v, f, w in zip(Xs, vals, fs, (1.0, 3.0))],
+                                rows=rows)
+    Mr = Arm[torch.from_numpy(rows).cuda()].cpu().numpy()
+    assert scaled_err(Mr[:, :F], Ao, S)[0] <= ENTRY_TOL
+    assert np.array_equal(rrm.cpu().numpy()[rows], ro)
+
+
 def test_user_stream_and_timing_hook(ctx):
     """a ctx on a user stream produces the same entries; the timing hook counts the assembly
     launches (one per batch of blocks sharing a kernel variant) and resets on read"""
