@@ -754,21 +754,36 @@ class FlsEngine:
         end-to-end solve, per-config numbers and the CPU oracle (rank 0, N = 1)"""
         torch = self.torch
         out = {}
+
+        def leg(key, fn):
+            # at N = 1 a failing auxiliary leg is recorded and the headline line still prints;
+            # at N > 1 it propagates (a rank that skipped a leg's collectives would desynchronise
+            # the others)
+            if self.world > 1:
+                out[key] = fn()
+                return
+            try:
+                out[key] = fn()
+            except Exception as ex:  # noqa: BLE001 -- reported in the JSON line
+                out[key] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
+                sys.stderr.write(f"bench.py: leg {key} failed: {ex}\n")
+
         if not args.no_e2e:
-            out["e2e_device_resident"] = e2e_device_measure(args, self)
+            leg("e2e_device_resident", lambda: e2e_device_measure(args, self))
         del self.Ab
         torch.cuda.empty_cache()
         if not args.no_e2e:
-            out["e2e"] = e2e_measure(args, self.p, self.ctx, self.W, self.b, self.a, self.e,
-                                     self.world, self.local)
+            leg("e2e", lambda: e2e_measure(args, self.p, self.ctx, self.W, self.b, self.a, self.e,
+                                           self.world, self.local))
         if not args.no_solve and args.rows is None:
-            out["solve"] = solve_measure(args, self.world, self.rank, self.local)
+            leg("solve", lambda: solve_measure(args, self.world, self.rank, self.local))
+        solve_ok = "solve" in out and "error" not in out["solve"]
         if self.world == 1 and args.rows is None and not args.no_per_config:
-            out["per_config"] = per_config(
+            leg("per_config", lambda: per_config(
                 budget_s=args.per_config_budget,
-                known_solves={self.p.name: out["solve"]} if "solve" in out else None)
+                known_solves={self.p.name: out["solve"]} if solve_ok else None))
         if self.rank == 0 and self.world == 1 and not args.no_cpu:
-            out["cpu_baseline"] = cpu_baseline(self.p)
+            leg("cpu_baseline", lambda: cpu_baseline(self.p))
         return out
 
     def close(self):
