@@ -1113,6 +1113,58 @@ def test_back_to_back_calls_with_pdl_overlap_keep_stream_order(ctx):
         assert torch.equal(V, Vr), n
 
 
+@pytest.mark.parametrize("name,size", [("c1_poisson1d", "full"), ("c2_poisson2d", "full"),
+                                       ("c3_poisson5d", "mini")])
+def test_cuda_graph_replay_matches_eager_calls(name, size):
+    """bench.py's per_config times the bench's call replayed in CUDA graphs of 10 steps (the
+    fused single launch for C1, the two launches with programmatic dependent launch for C2/C3):
+    a captured sequence alternating seeds and rhs values into ONE [A | b] (and a second buffer)
+    leaves, after every replay, exactly the bits of the eager calls -- the last call's in the
+    shared buffer"""
+    p = wl.make_problem(name, size)
+    d, F, R = p.dim, p.n_features, p.n_rows
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx = fls.Context(stream=s)
+        base = dev_blocks(p)
+        alt = [fls.Block(b.X, b.terms, b.weight, 2.0 * b.values - 1.0, b.fields) for b in base]
+        sets = [fls.BlockSet(base, d), fls.BlockSet(alt, d)]
+        lda = fls.round_up(R, 4)
+        refs = []
+        for k in range(2):
+            W, b, A, _ = fls.fls_features_assemble(ctx, d, F, p.sigma, k, sets[k], lda=lda)
+            fls.fls_sync(ctx)
+            refs.append((W.clone(), b.clone(), A[: (F + 1) * lda].view(F + 1, lda)[:, :R].clone()))
+        A = torch.full(((F + 1) * lda,), float("nan"), dtype=torch.float64, device="cuda")
+        A2 = torch.full_like(A, float("nan"))
+        W = torch.empty((F, d), dtype=torch.float64, device="cuda")
+        b = torch.empty((F,), dtype=torch.float64, device="cuda")
+        W2, b2 = torch.empty_like(W), torch.empty_like(b)
+
+        def seq():
+            for i in range(5):                       # seeds 0, 1, 0, 1, 0: ends on seed 0
+                fls.fls_features_assemble(ctx, d, F, p.sigma, i % 2, sets[i % 2],
+                                          W=W, b=b, A=A, lda=lda)
+            fls.fls_features_assemble(ctx, d, F, p.sigma, 1, sets[1], W=W2, b=b2, A=A2, lda=lda)
+
+        seq()                                        # warm-up outside the capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            seq()
+        for rep in range(3):
+            A.fill_(float("nan"))
+            A2.fill_(float("nan"))
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(W, refs[0][0]) and torch.equal(b, refs[0][1]), rep
+            assert torch.equal(A.view(F + 1, lda)[:, :R], refs[0][2]), rep
+            assert torch.equal(W2, refs[1][0]) and torch.equal(b2, refs[1][1]), rep
+            assert torch.equal(A2.view(F + 1, lda)[:, :R], refs[1][2]), rep
+        fls.fls_sync(ctx)
+        ctx.close()
+
+
 def test_maximum_operator_sizes(ctx):
     """the limits of the ABI at once: d = 8 (FLS_MAX_DIM), 64 terms (FLS_MAX_TERMS), 4 coefficient
     fields (FLS_MAX_FIELDS), and terms of order > 22 whose monomial the fold multiplies out
