@@ -1165,6 +1165,58 @@ def test_cuda_graph_replay_matches_eager_calls(name, size):
         ctx.close()
 
 
+def test_concurrent_contexts_on_two_threads():
+    """fls.h: calls on different contexts / streams are thread-safe -- two host threads, each
+    with its own ctx on its own stream, issue interleaved fused and two-launch calls (the host
+    plan state is thread-local; ctypes releases the GIL) and every buffer ends with the bits of
+    the same call made alone"""
+    import threading
+    probs = [wl.make_problem("c1_poisson1d", "full"), wl.make_problem("c2_poisson2d", "full")]
+    refs, setups = [], []
+    for p in probs:
+        d, F, R = p.dim, p.n_features, p.n_rows
+        s = torch.cuda.Stream()
+        ctx = fls.Context(stream=s)
+        bs = fls.BlockSet(dev_blocks(p), d)
+        lda = fls.round_up(R, 4)
+        with torch.cuda.stream(s):
+            W, b, A, _ = fls.fls_features_assemble(ctx, d, F, p.sigma, 3, bs, lda=lda)
+        fls.fls_sync(ctx)
+        refs.append((W.clone(), b.clone(), A.view(F + 1, lda)[:, :R].clone()))
+        setups.append((p, s, ctx, bs, lda))
+    outs = [None, None]
+    errs = []
+
+    def work(k):
+        try:
+            p, s, ctx, bs, lda = setups[k]
+            d, F = p.dim, p.n_features
+            W = torch.empty((F, d), dtype=torch.float64, device="cuda")
+            b = torch.empty((F,), dtype=torch.float64, device="cuda")
+            A = torch.full((((F + 1) * lda),), float("nan"), dtype=torch.float64, device="cuda")
+            with torch.cuda.stream(s):
+                for i in range(20):
+                    fls.fls_features_assemble(ctx, d, F, p.sigma, 3 if i % 2 == 1 else 5, bs,
+                                              W=W, b=b, A=A, lda=lda)
+            fls.fls_sync(ctx)
+            outs[k] = (W, b, A)
+        except Exception as ex:  # noqa: BLE001
+            errs.append(ex)
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for k, (p, s, ctx, bs, lda) in enumerate(setups):
+        F, R = p.n_features, p.n_rows
+        W, b, A = outs[k]
+        assert torch.equal(W, refs[k][0]) and torch.equal(b, refs[k][1]), k
+        assert torch.equal(A.view(F + 1, lda)[:, :R], refs[k][2]), k
+        ctx.close()
+
+
 def test_maximum_operator_sizes(ctx):
     """the limits of the ABI at once: d = 8 (FLS_MAX_DIM), 64 terms (FLS_MAX_TERMS), 4 coefficient
     fields (FLS_MAX_FIELDS), and terms of order > 22 whose monomial the fold multiplies out
