@@ -279,9 +279,9 @@ FLS_API fls_status fls_solve_mu(fls_ctx *ctx, double *Ab, int64_t n_rows, int64_
 
 /* ---------------------------------------------------------------------------------------- */
 /* Communicator for the multi-rank solve (row-sharded assembly needs no     */
-/* collective; the least-squares solve has one exchange step, TSQR).  One ctx per rank, one   */
-/* rank per GPU.  The communicator belongs to the ctx (freed by fls_comm_destroy or          */
-/* fls_ctx_destroy).                                                                          */
+/* collective; the least-squares solve of Alg. 1 line 5, has one exchange step,     */
+/* TSQR).  One ctx per rank, one rank per GPU.  The communicator belongs to the ctx (freed by */
+/* fls_comm_destroy or fls_ctx_destroy).                                                       */
 /* fls_comm_unique_id: an NCCL unique id (host, FLS_COMM_ID_BYTES) -- rank 0 creates it and   */
 /*   the caller distributes it to every rank by its own means (torch.distributed, MPI, file). */
 /* fls_comm_init: NCCL communicator of nranks ranks on the ctx's device and stream; blocks    */

@@ -115,3 +115,19 @@ def test_nccl_unique_id_on_host():
     from paper_2602_10541_b200 import fls
     a, b = fls.fls_comm_unique_id(), fls.fls_comm_unique_id()
     assert len(a) == len(b) == 128 and a != b
+
+
+def test_boundary_calls_cite_their_passage():
+    """include/fls.h: each SURVEY §8(b) call is declared under a comment that cites the
+    PAPER.md passage defining the operation (P:L<n>) and states its errors"""
+    import re
+    text = open(os.path.join(ROOT, "include", "fls.h")).read()
+    for name in ("fls_features", "fls_assemble", "fls_solve", "fls_eval", "fls_comm_init"):
+        m = re.search(r"FLS_API\s+fls_status\s+" + name + r"\s*\(", text)
+        assert m, name
+        # the documentation block (between two /* ---- */ rules) the declaration sits under
+        end = text.rfind("/* ----", 0, m.start())
+        start = text.rfind("/* ----", 0, end)
+        doc = text[start:end]
+        assert re.search(r"P:L\d+", doc), f"{name}: no P:L citation in its comment"
+        assert "FLS_E" in doc or "error" in doc.lower(), f"{name}: error behaviour not stated"
